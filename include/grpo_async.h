@@ -1,0 +1,221 @@
+/*
+ * grpo_async.h -- C ABI of the B200 (sm_100a) hot path of the asynchronous
+ * GRPO objective of arxiv 2604.26256 ("DORA"), §3.1.
+ *
+ *   J_async = E_x [ (1/G) sum_j sum_{i in B_j} (1/L_i) sum_t min(r A, clip_eps(r) A) ]
+ *             eq:grpo_async
+ *   r_{i,t} = pi_theta(y_t|.) / pi_{w_j}(y_t|.)            eq:ratio_async
+ *   C1 one version per trajectory, C2 no trajectory dropped and
+ *   N == TBS, C3 v(theta) - v(w_j) <= K
+ *   A_i = (R_i - mean) / std over the G responses           eq:group_advantage
+ *
+ * Conventions shared by every call
+ *   - All array pointers are DEVICE pointers unless the parameter name starts
+ *     with host_.  The caller owns every buffer; no call allocates device
+ *     memory or keeps a pointer after it returns.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t; NULL = the
+ *     legacy default stream) and never synchronizes, except *_sync.
+ *   - bf16 tensors are passed as uint16_t bit patterns (IEEE bfloat16).
+ *   - Status codes: GRPO_OK on success.  Argument errors are detected on the
+ *     host before any launch and leave every output untouched.  Data-dependent
+ *     violations (C1/C2/C3, bad targets) are never synchronous errors: they
+ *     land in the validate outputs; grpo_async_validate_sync converts them
+ *     into GRPO_ERR_VALIDATION.  grpo_last_error() returns a thread-local
+ *     description of the last non-OK status of the calling thread.
+ *   - The loss calls assume validated input (targets in [0, V)); an invalid
+ *     target never causes an out-of-bounds access, only a meaningless value.
+ *   - Functions are reentrant; distinct streams may run them concurrently on
+ *     disjoint outputs.
+ * Readings of the paper where it is silent or ambiguous (population std,
+ * A = 0 for a group with bitwise-equal rewards, per-prompt weight 1/P,
+ * symmetric eps, ties at the clip boundary let the gradient flow, loss = -J)
+ * are listed in DESIGN.md "Readings" (Z1-Z20).
+ */
+#ifndef GRPO_ASYNC_H
+#define GRPO_ASYNC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *grpo_stream_t; /* a cudaStream_t */
+
+typedef enum {
+    GRPO_OK = 0,
+    GRPO_ERR_VALIDATION = 1,  /* C1/C2/C3 or structural violation (validate_sync only)       */
+    GRPO_ERR_INVALID_ARG = 2, /* NULL required pointer, N <= 0, eps not in (0,1), K < 0, ...  */
+    GRPO_ERR_ALIGNMENT = 3,   /* logits/dlogits not 16-byte aligned, or ld % 8 != 0, ld < V   */
+    GRPO_ERR_WORKSPACE = 4,   /* workspace NULL or smaller than grpo_async_workspace_size()   */
+    GRPO_ERR_CUDA = 5         /* a CUDA runtime error (text in grpo_last_error)               */
+} grpo_status_t;
+
+/* Per-trajectory validation flags (traj_flags bits). */
+#define GRPO_FLAG_STALE          (1u << 0) /* v_theta - v_i > K              (C3)  */
+#define GRPO_FLAG_FUTURE         (1u << 1) /* v_theta - v_i < 0              (C3 reading) */
+#define GRPO_FLAG_ZERO_LEN       (1u << 2) /* L_i = cu[i+1] - cu[i] <= 0                  */
+#define GRPO_FLAG_BAD_GROUP_ID   (1u << 3) /* group id not in [0, P)                      */
+#define GRPO_FLAG_GROUP_SIZE     (1u << 4) /* its group does not have exactly G members (C2) */
+#define GRPO_FLAG_C1_MIXED       (1u << 5) /* a token version differs from v_i   (C1) */
+#define GRPO_FLAG_BAD_TARGET     (1u << 6) /* a target id not in [0, V)                   */
+#define GRPO_FLAG_BAD_LOGP_BEHAV (1u << 7) /* a behaviour log-prob not finite or > 0      */
+
+/* Validation summary (all int64; mirrors SPEC metrics.audit S:619-625). */
+typedef struct {
+    int64_t n_traj;              /* N                                                   */
+    int64_t n_tokens;            /* cu[N]                                               */
+    int64_t n_stale, n_future, n_zero_len, n_bad_group_id, n_group_size,
+            n_c1_mixed, n_bad_target, n_bad_logp_behav; /* trajectories per flag      */
+    int64_t n_groups_wrong_size; /* #{p : count_p != G}                                 */
+    int64_t c2_dropped;          /* sum_p max(0, G - count_p)                           */
+    int64_t max_staleness;       /* max_i (v_theta - v_i)   (0 when N == 0)             */
+    int64_t min_staleness;       /* min_i (v_theta - v_i)                               */
+    int64_t cu_ok;               /* cu[0] == 0, cu non-decreasing, cu[N] == T           */
+    int64_t tbs_ok;              /* N == tbs                                            */
+    int64_t c1_ok, c2_ok, c3_ok; /* the paper's constraints (C2: tbs_ok, all groups G,   */
+                                 /*  all group ids valid; C3: no STALE/FUTURE)          */
+    int64_t valid;               /* all of the above and no ZERO_LEN/BAD_TARGET/BAD_LOGP */
+} grpo_validate_summary_t;
+
+/* Index of the per-chunk statistics accumulated by grpo_async_loss_fwd into stats[]. */
+enum {
+    GRPO_STAT_J = 0,         /* sum over rows of inv_norm_i * term_t (this chunk's part of J) */
+    GRPO_STAT_ROWS = 1,      /* rows processed                                                */
+    GRPO_STAT_CLIPPED = 2,   /* rows whose clipped branch binds: (A>0, r>1+eps) or (A<0, r<1-eps) */
+    GRPO_STAT_ACTIVE = 3,    /* rows with nonzero gradient: not clipped and A != 0            */
+    GRPO_STAT_ABS = 4,       /* sum of inv_norm_i * |term_t| (L1 mass of J's summands)        */
+    GRPO_STAT_LOGP = 5,      /* sum of log pi_theta(y_t) (diagnostic)                         */
+    GRPO_NUM_STATS = 6
+};
+
+/* Optional tuning of the fused loss kernel (NULL = automatic). */
+typedef struct {
+    int32_t kernel;        /* 0 auto, 1 cluster-resident fused (roofline design), 2 row-wise two-pass */
+    int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
+    int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1)                                    */
+    int32_t stages;        /* 0 auto, else 1..8 shared-memory row stages per CTA (kernel 1)   */
+} grpo_tune_t;
+
+/*
+ * grpo_async_validate -- bit-exact integer checks of C1, C2, C3 and batch
+ * structure.
+ *   version_ids   int64[N]  behaviour version v(w_j) of trajectory i
+ *   token_version int64[T]  per-token behaviour version, or NULL (C1 check skipped)
+ *   cu_seqlens    int64[N+1] packed row offsets: trajectory i owns rows [cu[i], cu[i+1])
+ *   group_ids     int32[N]  prompt index of trajectory i, any order
+ *   target_ids    int64[T]  sampled token y_t
+ *   logp_behav    float[T]  log pi_{w_j}(y_t), or NULL (check skipped)
+ *   N, T, P, V, G, tbs      sizes; v_theta = v(theta); K = staleness bound
+ * Outputs (device): traj_flags uint32[N], group_count int32[P],
+ *   stale_hist int32[P*(K+1)] (|B_j| per prompt p and gap v_theta-v in [0,K]),
+ *   summary (one grpo_validate_summary_t).
+ * Errors: GRPO_ERR_INVALID_ARG for NULL required pointers, N < 0, T < 0, P <= 0,
+ *   V <= 0, G <= 0, K < 0.
+ */
+grpo_status_t grpo_async_validate(const int64_t *version_ids, const int64_t *token_version,
+                                  const int64_t *cu_seqlens, const int32_t *group_ids,
+                                  const int64_t *target_ids, const float *logp_behav,
+                                  int32_t N, int64_t T, int32_t P, int32_t V, int32_t G,
+                                  int32_t tbs, int64_t v_theta, int32_t K,
+                                  uint32_t *traj_flags, int32_t *group_count,
+                                  int32_t *stale_hist, grpo_validate_summary_t *summary,
+                                  grpo_stream_t stream);
+
+/* Same, then synchronizes `stream` and copies the summary to host_summary.
+ * Returns GRPO_ERR_VALIDATION when host_summary->valid == 0. */
+grpo_status_t grpo_async_validate_sync(const int64_t *version_ids, const int64_t *token_version,
+                                       const int64_t *cu_seqlens, const int32_t *group_ids,
+                                       const int64_t *target_ids, const float *logp_behav,
+                                       int32_t N, int64_t T, int32_t P, int32_t V, int32_t G,
+                                       int32_t tbs, int64_t v_theta, int32_t K,
+                                       uint32_t *traj_flags, int32_t *group_count,
+                                       int32_t *stale_hist, grpo_validate_summary_t *summary,
+                                       grpo_validate_summary_t *host_summary,
+                                       grpo_stream_t stream);
+
+/*
+ * grpo_async_advantage -- group-relative advantages, eq:group_advantage.
+ *   rewards float[N], group_ids int32[N] (any order), cu_seqlens int64[N+1].
+ *   For each group p: fp64 mean and population std over its members in
+ *   ascending i; A_i = (R_i - mean) / max(std, std_floor), and A_i = 0 exactly
+ *   when all rewards of the group are bitwise equal (Z1, Z2).
+ *   inv_norm_i = 1 / (P * count_p * L_i): the weight of one token of i in J
+ *   (eq:grpo_async's 1/L_i, 1/G and the mean over prompts, Z5, Z6).
+ * Outputs: adv float[N], inv_norm float[N], group_count int32[P] (nullable).
+ * A trajectory with an invalid group id or L_i <= 0 gets A = 0 and inv_norm = 0.
+ * Errors: GRPO_ERR_INVALID_ARG for NULL pointers, N < 0, P <= 0, std_floor <= 0.
+ */
+grpo_status_t grpo_async_advantage(const float *rewards, const int32_t *group_ids,
+                                   const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                   float std_floor, float *adv, float *inv_norm,
+                                   int32_t *group_count, grpo_stream_t stream);
+
+/*
+ * grpo_async_loss_fwd -- fused log-softmax + target gather + ratio + clip +
+ * min + segmented mean, and (if dlogits != NULL) the backward in the same pass.
+ * The chunk is rows [row_begin, row_begin + n_rows) of this rank's packing.
+ *   logits      bf16[n_rows, ld] row k scores target_ids[k] (caller-shifted,
+ *               response tokens only); ld >= V, ld % 8 == 0, 16-byte aligned.
+ *   target_ids  int64[n_rows], logp_behav float[n_rows]   (chunk-local, row k)
+ *   cu_seqlens  int64[N+1] over this rank's N trajectories (row_begin is an
+ *               offset into this packing; a trajectory may straddle chunks).
+ *   traj_index  int32[N] or NULL: trajectory i of this packing reads
+ *               adv[traj_index[i]] / inv_norm[traj_index[i]] (NULL = identity),
+ *               so replicated whole-batch advantages can feed a shard.
+ *   adv, inv_norm  float[*] from grpo_async_advantage.
+ *   eps in (0,1); grad_scale multiplies the gradient (1 = d(-J)/dz).
+ * Outputs (each nullable): logp_out, lse_out, token_scale_out float[n_rows]
+ *   (token_scale s_t = grad_scale * inv_norm * A * r * [not clipped]);
+ *   traj_sum double[N]: += sum of term_t over this chunk's rows of i;
+ *   stats double[GRPO_NUM_STATS]: += this chunk's GRPO_STAT_* values;
+ *   dlogits bf16[n_rows, ld]: d(-J)/dz = s_t (softmax - onehot(y_t)), written
+ *   once per element in [0, V) (padding columns untouched).  dlogits may
+ *   equal logits (in place).
+ * workspace: device scratch of grpo_async_workspace_size(n_rows, V, N) bytes.
+ * tune: NULL or kernel selection (grpo_tune_t).
+ * Errors: GRPO_ERR_INVALID_ARG (NULL logits/targets/logp_behav/cu/adv/inv_norm/
+ *   traj_sum/stats, n_rows < 0, N <= 0, V <= 0, eps not in (0,1)),
+ *   GRPO_ERR_ALIGNMENT, GRPO_ERR_WORKSPACE, GRPO_ERR_CUDA.
+ */
+grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int64_t n_rows,
+                                  int32_t V, int64_t ld, const int64_t *target_ids,
+                                  const float *logp_behav, const int64_t *cu_seqlens,
+                                  int32_t N, const int32_t *traj_index, const float *adv,
+                                  const float *inv_norm, float eps, float grad_scale,
+                                  float *logp_out, float *lse_out, float *token_scale_out,
+                                  double *traj_sum, double *stats, uint16_t *dlogits,
+                                  void *workspace, size_t workspace_bytes,
+                                  const grpo_tune_t *tune, grpo_stream_t stream);
+
+/*
+ * grpo_async_loss_bwd -- unfused backward: one streaming pass that re-reads
+ * the logits and writes dlogits = grad_scale_mult * s_t * (exp(z - lse_t) - onehot(y_t))
+ * from the lse and token_scale saved by grpo_async_loss_fwd.
+ *   logits, dlogits bf16[n_rows, ld] (may alias), target_ids int64[n_rows],
+ *   lse, token_scale float[n_rows].
+ * Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_CUDA.
+ */
+grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
+                                  const int64_t *target_ids, const float *lse,
+                                  const float *token_scale, float grad_scale_mult,
+                                  uint16_t *dlogits, grpo_stream_t stream);
+
+/* Bytes of device workspace grpo_async_loss_fwd needs for a chunk. */
+size_t grpo_async_workspace_size(int64_t n_rows, int32_t V, int32_t N);
+
+/* Number of kernels the last successful call of the calling thread launched
+ * (for launch accounting in benchmarks). */
+int32_t grpo_last_launch_count(void);
+
+/* Thread-local text of the last error ("" if none). */
+const char *grpo_last_error(void);
+
+/* Library version string. */
+const char *grpo_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRPO_ASYNC_H */

@@ -1,0 +1,202 @@
+"""Thin ctypes binding of include/grpo_async.h (argument marshalling only).
+
+Every function here has the name of the C entry point it calls and does
+nothing but turn torch device tensors into pointers, pick the current CUDA
+stream, and raise on a non-OK status.  All arithmetic happens in the CUDA
+kernels of libgrpo_async.so.  There is no fallback: if the library is
+missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgrpo_async.so")
+
+GRPO_OK, GRPO_ERR_VALIDATION, GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_WORKSPACE, \
+    GRPO_ERR_CUDA = range(6)
+STATUS_NAMES = ["OK", "VALIDATION", "INVALID_ARG", "ALIGNMENT", "WORKSPACE", "CUDA"]
+
+FLAG_NAMES = ["STALE", "FUTURE", "ZERO_LEN", "BAD_GROUP_ID", "GROUP_SIZE", "C1_MIXED",
+              "BAD_TARGET", "BAD_LOGP_BEHAV"]
+STAT_J, STAT_ROWS, STAT_CLIPPED, STAT_ACTIVE, STAT_ABS, STAT_LOGP = range(6)
+NUM_STATS = 6
+
+SUMMARY_FIELDS = ("n_traj", "n_tokens", "n_stale", "n_future", "n_zero_len", "n_bad_group_id",
+                  "n_group_size", "n_c1_mixed", "n_bad_target", "n_bad_logp_behav",
+                  "n_groups_wrong_size", "c2_dropped", "max_staleness", "min_staleness",
+                  "cu_ok", "tbs_ok", "c1_ok", "c2_ok", "c3_ok", "valid")
+
+EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advantage",
+            "grpo_async_loss_fwd", "grpo_async_loss_bwd", "grpo_async_workspace_size",
+            "grpo_last_launch_count", "grpo_last_error", "grpo_version")
+
+
+class ValidateSummary(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in SUMMARY_FIELDS]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n in SUMMARY_FIELDS}
+
+
+class Tune(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("cluster_size", C.c_int32),
+                ("ctas_per_sm", C.c_int32), ("stages", C.c_int32)]
+
+
+class GrpoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 6 else status}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m "
+                          "paper_2604_26256_b200.build` (there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, i32, i64, f32, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_size_t
+    st = C.c_int
+    lib.grpo_async_validate.argtypes = [P, P, P, P, P, P, i32, i64, i32, i32, i32, i32, i64, i32,
+                                        P, P, P, P, P]
+    lib.grpo_async_validate.restype = st
+    lib.grpo_async_validate_sync.argtypes = [P, P, P, P, P, P, i32, i64, i32, i32, i32, i32, i64,
+                                             i32, P, P, P, P, P, P]
+    lib.grpo_async_validate_sync.restype = st
+    lib.grpo_async_advantage.argtypes = [P, P, P, i32, i32, f32, P, P, P, P]
+    lib.grpo_async_advantage.restype = st
+    lib.grpo_async_loss_fwd.argtypes = [P, i64, i64, i32, i64, P, P, P, i32, P, P, P, f32, f32,
+                                        P, P, P, P, P, P, P, sz, P, P]
+    lib.grpo_async_loss_fwd.restype = st
+    lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
+    lib.grpo_async_loss_bwd.restype = st
+    lib.grpo_async_workspace_size.argtypes = [i64, i32, i32]
+    lib.grpo_async_workspace_size.restype = sz
+    lib.grpo_last_launch_count.argtypes = []
+    lib.grpo_last_launch_count.restype = i32
+    lib.grpo_last_error.argtypes = []
+    lib.grpo_last_error.restype = C.c_char_p
+    lib.grpo_version.argtypes = []
+    lib.grpo_version.restype = C.c_char_p
+    return lib
+
+
+LIB = _load()
+
+
+def _ptr(t, dtype=None, name="tensor"):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check(status):
+    if status != GRPO_OK:
+        raise GrpoError(status, LIB.grpo_last_error().decode())
+
+
+def grpo_last_launch_count() -> int:
+    return int(LIB.grpo_last_launch_count())
+
+
+def grpo_last_error() -> str:
+    return LIB.grpo_last_error().decode()
+
+
+def grpo_version() -> str:
+    return LIB.grpo_version().decode()
+
+
+def grpo_async_workspace_size(n_rows: int, V: int, N: int) -> int:
+    return int(LIB.grpo_async_workspace_size(n_rows, V, N))
+
+
+def grpo_async_validate(version_ids, token_version, cu_seqlens, group_ids, target_ids, logp_behav,
+                        N, T, P, V, G, tbs, v_theta, K, traj_flags, group_count, stale_hist,
+                        summary, stream=None):
+    """summary: int64 device tensor of len(SUMMARY_FIELDS)."""
+    _check(LIB.grpo_async_validate(
+        _ptr(version_ids, torch.int64, "version_ids"), _ptr(token_version, torch.int64, "token_version"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), _ptr(group_ids, torch.int32, "group_ids"),
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(logp_behav, torch.float32, "logp_behav"),
+        N, T, P, V, G, tbs, v_theta, K, _ptr(traj_flags, torch.int32, "traj_flags"),
+        _ptr(group_count, torch.int32, "group_count"), _ptr(stale_hist, torch.int32, "stale_hist"),
+        _ptr(summary, torch.int64, "summary"), _stream(stream)))
+
+
+def grpo_async_validate_sync(version_ids, token_version, cu_seqlens, group_ids, target_ids,
+                             logp_behav, N, T, P, V, G, tbs, v_theta, K, traj_flags, group_count,
+                             stale_hist, summary, stream=None, raise_on_invalid=False):
+    """Returns (status, summary dict); GRPO_ERR_VALIDATION is returned, not raised, unless asked."""
+    host = ValidateSummary()
+    status = LIB.grpo_async_validate_sync(
+        _ptr(version_ids, torch.int64, "version_ids"), _ptr(token_version, torch.int64, "token_version"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), _ptr(group_ids, torch.int32, "group_ids"),
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(logp_behav, torch.float32, "logp_behav"),
+        N, T, P, V, G, tbs, v_theta, K, _ptr(traj_flags, torch.int32, "traj_flags"),
+        _ptr(group_count, torch.int32, "group_count"), _ptr(stale_hist, torch.int32, "stale_hist"),
+        _ptr(summary, torch.int64, "summary"), C.byref(host), _stream(stream))
+    if status != GRPO_OK and (status != GRPO_ERR_VALIDATION or raise_on_invalid):
+        _check(status)
+    return status, host.as_dict()
+
+
+def grpo_async_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor, adv, inv_norm,
+                         group_count=None, stream=None):
+    _check(LIB.grpo_async_advantage(
+        _ptr(rewards, torch.float32, "rewards"), _ptr(group_ids, torch.int32, "group_ids"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, P, float(std_floor),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"),
+        _ptr(group_count, torch.int32, "group_count"), _stream(stream)))
+
+
+def grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens, N,
+                        traj_index, adv, inv_norm, eps, grad_scale, logp_out, lse_out,
+                        token_scale_out, traj_sum, stats, dlogits, workspace, tune=None,
+                        stream=None):
+    """logits/dlogits: bf16 (or int16/uint16 bit patterns) [n_rows, ld] device tensors."""
+    tune_p = None
+    if tune is not None:
+        t = Tune(*[int(tune.get(k, 0)) for k in ("kernel", "cluster_size", "ctas_per_sm", "stages")])
+        tune_p = C.byref(t)
+    for name, x in (("logits", logits), ("dlogits", dlogits)):
+        if x is not None and x.element_size() != 2:
+            raise TypeError(f"{name}: expected a 16-bit (bf16) tensor")
+    _check(LIB.grpo_async_loss_fwd(
+        _ptr(logits, None, "logits"), row_begin, n_rows, V, ld,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(logp_behav, torch.float32, "logp_behav"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, _ptr(traj_index, torch.int32, "traj_index"),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"), float(eps),
+        float(grad_scale), _ptr(logp_out, torch.float32, "logp_out"),
+        _ptr(lse_out, torch.float32, "lse_out"), _ptr(token_scale_out, torch.float32, "token_scale_out"),
+        _ptr(traj_sum, torch.float64, "traj_sum"), _ptr(stats, torch.float64, "stats"),
+        _ptr(dlogits, None, "dlogits"), _ptr(workspace, torch.uint8, "workspace"),
+        workspace.numel() if workspace is not None else 0, tune_p, _stream(stream)))
+
+
+def grpo_async_loss_bwd(logits, n_rows, V, ld, target_ids, lse, token_scale, grad_scale_mult,
+                        dlogits, stream=None):
+    for name, x in (("logits", logits), ("dlogits", dlogits)):
+        if x is not None and x.element_size() != 2:
+            raise TypeError(f"{name}: expected a 16-bit (bf16) tensor")
+    _check(LIB.grpo_async_loss_bwd(
+        _ptr(logits, None, "logits"), n_rows, V, ld, _ptr(target_ids, torch.int64, "target_ids"),
+        _ptr(lse, torch.float32, "lse"), _ptr(token_scale, torch.float32, "token_scale"),
+        float(grad_scale_mult), _ptr(dlogits, None, "dlogits"), _stream(stream)))

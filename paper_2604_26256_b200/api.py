@@ -1,0 +1,162 @@
+"""Python plumbing above the C ABI: device buffers for one training batch and
+the order of calls of one step of the hot path (validate -> advantage ->
+fused loss over row chunks).  Every numeric step runs in the CUDA kernels of
+libgrpo_async.so; this module only allocates torch tensors and calls the
+binding (paper_2604_26256_b200._lib).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+@dataclass
+class DeviceBatch:
+    """Packed batch metadata on the device (trajectories of
+    up to K versions, G responses per prompt; response rows only)."""
+    P: int
+    G: int
+    K: int
+    V: int
+    ld: int
+    tbs: int
+    v_theta: int
+    cu_seqlens: torch.Tensor       # int64 [N+1]
+    group_ids: torch.Tensor        # int32 [N]
+    version_ids: torch.Tensor      # int64 [N]
+    rewards: torch.Tensor          # float32 [N]
+    target_ids: torch.Tensor       # int64 [T]
+    logp_behav: torch.Tensor       # float32 [T]
+    token_version: torch.Tensor | None = None  # int64 [T]
+
+    @property
+    def N(self):
+        return self.group_ids.numel()
+
+    @property
+    def T(self):
+        return self.target_ids.numel()
+
+    @staticmethod
+    def from_host(b, device, pin=False):
+        """b: any object with the synth.gen.Batch fields (numpy arrays)."""
+        def t(x, dt):
+            if x is None:
+                return None
+            h = torch.from_numpy(np.ascontiguousarray(x)).to(dt)
+            if pin:
+                h = h.pin_memory()
+            return h.to(device, non_blocking=pin)
+        return DeviceBatch(b.P, b.G, b.K, b.V, b.ld, b.tbs, b.v_theta,
+                           t(b.cu_seqlens, torch.int64), t(b.group_ids, torch.int32),
+                           t(b.version_ids, torch.int64), t(b.rewards, torch.float32),
+                           t(b.target_ids, torch.int64), t(b.logp_behav, torch.float32),
+                           t(b.token_version, torch.int64))
+
+
+class ValidateOut:
+    def __init__(self, N, P, K, device):
+        self.traj_flags = torch.zeros(max(N, 1), dtype=torch.int32, device=device)
+        self.group_count = torch.zeros(P, dtype=torch.int32, device=device)
+        self.stale_hist = torch.zeros(P * (K + 1), dtype=torch.int32, device=device)
+        self.summary = torch.zeros(len(L.SUMMARY_FIELDS), dtype=torch.int64, device=device)
+
+    def summary_dict(self):
+        return dict(zip(L.SUMMARY_FIELDS, self.summary.cpu().tolist()))
+
+
+class GrpoAsyncLoss:
+    """One step of the hot path over a DeviceBatch.
+
+    eps: clip range; grad_scale multiplies dlogits; std_floor: Z2.
+    tune: optional dict for grpo_tune_t (kernel / cluster_size / ctas_per_sm / stages).
+    """
+
+    def __init__(self, eps=0.2, std_floor=1e-8, grad_scale=1.0, tune=None):
+        self.eps = float(eps)
+        self.std_floor = float(std_floor)
+        self.grad_scale = float(grad_scale)
+        self.tune = tune
+        self._ws = None
+        self.launches = 0
+
+    # ---- validate (C1/C2/C3)
+    def validate(self, db: DeviceBatch, out: ValidateOut | None = None, stream=None):
+        out = out or ValidateOut(db.N, db.P, db.K, db.target_ids.device)
+        L.grpo_async_validate(db.version_ids, db.token_version, db.cu_seqlens, db.group_ids,
+                              db.target_ids, db.logp_behav, db.N, db.T, db.P, db.V, db.G, db.tbs,
+                              db.v_theta, db.K, out.traj_flags, out.group_count, out.stale_hist,
+                              out.summary, stream)
+        self.launches += L.grpo_last_launch_count()
+        return out
+
+    # ---- advantages, eq:group_advantage P:153-156
+    def advantage(self, db: DeviceBatch, adv=None, inv_norm=None, stream=None):
+        dev = db.rewards.device
+        adv = adv if adv is not None else torch.empty(db.N, dtype=torch.float32, device=dev)
+        inv = inv_norm if inv_norm is not None else torch.empty(db.N, dtype=torch.float32, device=dev)
+        L.grpo_async_advantage(db.rewards, db.group_ids, db.cu_seqlens, db.N, db.P, self.std_floor,
+                               adv, inv, None, stream)
+        self.launches += L.grpo_last_launch_count()
+        return adv, inv
+
+    def workspace(self, n_rows, V, N, device):
+        need = L.grpo_async_workspace_size(n_rows, V, N)
+        if self._ws is None or self._ws.numel() < need or self._ws.device != device:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+        return self._ws
+
+    # ---- fused loss fwd (+ bwd when dlogits is given), eq:grpo_async P:9-26
+    def loss_chunk(self, logits, row_begin, n_rows, target_ids, logp_behav, cu_seqlens, adv,
+                   inv_norm, traj_sum, stats, dlogits=None, traj_index=None, logp_out=None,
+                   lse_out=None, scale_out=None, V=None, stream=None):
+        V = V if V is not None else logits.shape[1]
+        ld = logits.shape[1]
+        N = cu_seqlens.numel() - 1
+        ws = self.workspace(n_rows, V, N, logits.device)
+        L.grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav,
+                              cu_seqlens, N, traj_index, adv, inv_norm, self.eps, self.grad_scale,
+                              logp_out, lse_out, scale_out, traj_sum, stats, dlogits, ws,
+                              self.tune, stream)
+        self.launches += L.grpo_last_launch_count()
+
+    def loss_bwd(self, logits, n_rows, V, target_ids, lse, token_scale, dlogits, mult=1.0,
+                 stream=None):
+        L.grpo_async_loss_bwd(logits, n_rows, V, logits.shape[1], target_ids, lse, token_scale,
+                              mult, dlogits, stream)
+        self.launches += L.grpo_last_launch_count()
+
+
+def lpt_partition(lengths, world_size):
+    """Token-balanced, trajectory-atomic partition (longest processing time first).
+
+    Sort trajectories by length descending (ties: lower index first) and give
+    each to the currently least-loaded rank (ties: lower rank).  Returns a list
+    of ascending index arrays, one per rank.  Long-tailed lengths make a
+    count-balanced split skewed.
+    """
+    lengths = np.asarray(lengths, np.int64)
+    order = np.lexsort((np.arange(len(lengths)), -lengths))
+    load = np.zeros(world_size, np.int64)
+    owner = np.empty(len(lengths), np.int64)
+    for i in order:
+        r = int(np.argmin(load))          # argmin returns the lowest rank on ties
+        owner[i] = r
+        load[r] += lengths[i]
+    return [np.nonzero(owner == r)[0] for r in range(world_size)]
+
+
+def shard_rows(cu_seqlens, traj_ids):
+    """Global row indices of the given trajectories, in order, and the local cu_seqlens."""
+    cu = np.asarray(cu_seqlens, np.int64)
+    L_ = cu[1:] - cu[:-1]
+    Ls = L_[traj_ids]
+    local_cu = np.zeros(len(traj_ids) + 1, np.int64)
+    local_cu[1:] = np.cumsum(Ls)
+    rows = np.concatenate([np.arange(cu[i], cu[i + 1]) for i in traj_ids]) if len(traj_ids) else \
+        np.zeros(0, np.int64)
+    return rows, local_cu

@@ -1,0 +1,103 @@
+// advantage.cu -- group-relative advantages, eq:group_advantage:
+//   A_i = (R_i - mean_p) / std_p  over the members of prompt group p,
+// population std (Z1), A = 0 exactly for a group whose rewards are
+// bitwise equal, else denominator max(std, floor) (Z2), and the token weight
+// inv_norm_i = 1 / (P * G_p * L_i) of eq:grpo_async (Z5, Z6).
+//
+// One warp per group.  The warp scans group_ids 32 at a time; the ballot of
+// members is consumed lowest lane first, so the fp64 sums run over members
+// in ascending trajectory index, one add at a time -- the same order as the
+// plain definition, which makes the results bit-identical to it.
+#include "common.cuh"
+
+namespace grpo {
+
+__global__ void __launch_bounds__(256)
+    advantage_kernel(const float *__restrict__ rewards, const int32_t *__restrict__ group_ids,
+                     const int64_t *__restrict__ cu, int32_t N, int32_t P, float std_floor,
+                     float *__restrict__ adv, float *__restrict__ inv_norm,
+                     int32_t *__restrict__ group_count) {
+    const int lane = threadIdx.x & 31;
+    const int32_t p = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (p >= P) return;
+    // pass 1: count, sum, bitwise equality
+    int32_t n = 0;
+    double sum = 0.0;
+    bool all_equal = true;
+    uint32_t first = 0;
+    for (int32_t base = 0; base < N; base += 32) {
+        const int32_t i = base + lane;
+        const bool mine = (i < N) && (group_ids[i] == p);
+        const float r = mine ? rewards[i] : 0.0f;
+        uint32_t mask = __ballot_sync(0xFFFFFFFFu, mine);
+        while (mask) {
+            const int j = __ffs(mask) - 1;
+            const float rj = __shfl_sync(0xFFFFFFFFu, r, j);
+            const uint32_t bits = __float_as_uint(rj);
+            if (n == 0) first = bits;
+            else if (bits != first) all_equal = false;
+            sum += (double)rj;
+            n += 1;
+            mask &= mask - 1;
+        }
+    }
+    if (lane == 0 && group_count) group_count[p] = n;
+    if (n == 0) return;
+    const double mean = sum / (double)n;
+    // pass 2: sum of squared deviations
+    double ss = 0.0;
+    for (int32_t base = 0; base < N; base += 32) {
+        const int32_t i = base + lane;
+        const bool mine = (i < N) && (group_ids[i] == p);
+        const float r = mine ? rewards[i] : 0.0f;
+        uint32_t mask = __ballot_sync(0xFFFFFFFFu, mine);
+        while (mask) {
+            const int j = __ffs(mask) - 1;
+            const double d = (double)__shfl_sync(0xFFFFFFFFu, r, j) - mean;
+            ss = __dadd_rn(ss, __dmul_rn(d, d));  // no FMA contraction
+            mask &= mask - 1;
+        }
+    }
+    const double sd = sqrt(ss / (double)n);
+    const double den = sd > (double)std_floor ? sd : (double)std_floor;
+    // pass 3: outputs of the members (each lane writes its own)
+    for (int32_t base = 0; base < N; base += 32) {
+        const int32_t i = base + lane;
+        if (i < N && group_ids[i] == p) {
+            const double a = all_equal ? 0.0 : ((double)rewards[i] - mean) / den;
+            const int64_t L = cu[i + 1] - cu[i];
+            adv[i] = (float)a;
+            inv_norm[i] = L > 0 ? (float)(1.0 / __dmul_rn(__dmul_rn((double)P, (double)n), (double)L))
+                                : 0.0f;
+        }
+    }
+}
+
+// trajectories whose group id is invalid get A = 0, inv_norm = 0
+__global__ void advantage_invalid_kernel(const int32_t *__restrict__ group_ids, int32_t N,
+                                         int32_t P, float *__restrict__ adv,
+                                         float *__restrict__ inv_norm) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        const int32_t p = group_ids[i];
+        if (p < 0 || p >= P) {
+            adv[i] = 0.0f;
+            inv_norm[i] = 0.0f;
+        }
+    }
+}
+
+cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, const int64_t *cu,
+                             int32_t N, int32_t P, float std_floor, float *adv, float *inv_norm,
+                             int32_t *group_count, cudaStream_t s, int *launches) {
+    if (N > 0) {
+        advantage_invalid_kernel<<<(N + 255) / 256, 256, 0, s>>>(group_ids, N, P, adv, inv_norm);
+        *launches += 1;
+    }
+    const int64_t threads = (int64_t)P * 32;
+    advantage_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+        rewards, group_ids, cu, N, P, std_floor, adv, inv_norm, group_count);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace grpo

@@ -1,0 +1,232 @@
+// api.cu -- the extern "C" boundary declared in include/grpo_async.h.
+// Host-side argument checks, workspace carve-up, kernel selection, error text.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int32_t g_last_launches = 0;
+
+grpo_status_t fail(grpo_status_t st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+grpo_status_t ok(int launches) {
+    g_last_error.clear();
+    g_last_launches = launches;
+    return GRPO_OK;
+}
+
+grpo_status_t cuda_fail(cudaError_t e, const char *where, const char *why = nullptr) {
+    return fail(GRPO_ERR_CUDA, "%s: %s%s%s", where, cudaGetErrorString(e), why && *why ? " -- " : "",
+                why ? why : "");
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace
+
+extern "C" {
+
+const char *grpo_last_error(void) { return g_last_error.c_str(); }
+
+int32_t grpo_last_launch_count(void) { return g_last_launches; }
+
+const char *grpo_version(void) { return "grpo_async 0.1.0 (sm_100a)"; }
+
+size_t grpo_async_workspace_size(int64_t n_rows, int32_t V, int32_t N) {
+    (void)V;
+    if (n_rows < 0) n_rows = 0;
+    if (N < 0) N = 0;
+    return align256((size_t)n_rows * sizeof(grpo::RowInfo)) + align256((size_t)n_rows * 4) +
+           align256((size_t)n_rows * 4) + align256((size_t)n_rows) +
+           align256((size_t)N * 5 * sizeof(double)) + 256;
+}
+
+grpo_status_t grpo_async_validate(const int64_t *version_ids, const int64_t *token_version,
+                                  const int64_t *cu_seqlens, const int32_t *group_ids,
+                                  const int64_t *target_ids, const float *logp_behav,
+                                  int32_t N, int64_t T, int32_t P, int32_t V, int32_t G,
+                                  int32_t tbs, int64_t v_theta, int32_t K,
+                                  uint32_t *traj_flags, int32_t *group_count,
+                                  int32_t *stale_hist, grpo_validate_summary_t *summary,
+                                  grpo_stream_t stream) {
+    if (!cu_seqlens || !summary || !group_count || !stale_hist)
+        return fail(GRPO_ERR_INVALID_ARG, "validate: NULL cu_seqlens/group_count/stale_hist/summary");
+    if (N < 0 || T < 0 || P <= 0 || V <= 0 || G <= 0 || K < 0)
+        return fail(GRPO_ERR_INVALID_ARG, "validate: bad sizes N=%d T=%lld P=%d V=%d G=%d K=%d", N,
+                    (long long)T, P, V, G, K);
+    if (N > 0 && (!version_ids || !group_ids || !traj_flags))
+        return fail(GRPO_ERR_INVALID_ARG, "validate: NULL version_ids/group_ids/traj_flags");
+    if (T > 0 && !target_ids) return fail(GRPO_ERR_INVALID_ARG, "validate: NULL target_ids");
+    int launches = 0;
+    cudaError_t e = grpo::launch_validate(version_ids, token_version, cu_seqlens, group_ids,
+                                          target_ids, logp_behav, N, T, P, V, G, tbs, v_theta, K,
+                                          traj_flags, group_count, stale_hist, summary,
+                                          (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "validate");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_validate_sync(const int64_t *version_ids, const int64_t *token_version,
+                                       const int64_t *cu_seqlens, const int32_t *group_ids,
+                                       const int64_t *target_ids, const float *logp_behav,
+                                       int32_t N, int64_t T, int32_t P, int32_t V, int32_t G,
+                                       int32_t tbs, int64_t v_theta, int32_t K,
+                                       uint32_t *traj_flags, int32_t *group_count,
+                                       int32_t *stale_hist, grpo_validate_summary_t *summary,
+                                       grpo_validate_summary_t *host_summary,
+                                       grpo_stream_t stream) {
+    if (!host_summary) return fail(GRPO_ERR_INVALID_ARG, "validate_sync: NULL host_summary");
+    grpo_status_t st = grpo_async_validate(version_ids, token_version, cu_seqlens, group_ids,
+                                           target_ids, logp_behav, N, T, P, V, G, tbs, v_theta, K,
+                                           traj_flags, group_count, stale_hist, summary, stream);
+    if (st != GRPO_OK) return st;
+    const int launches = g_last_launches;
+    cudaError_t e = cudaMemcpyAsync(host_summary, summary, sizeof(grpo_validate_summary_t),
+                                    cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "validate_sync");
+    if (!host_summary->valid) {
+        g_last_launches = launches;
+        return fail(GRPO_ERR_VALIDATION,
+                    "batch violates constraints: c1_ok=%lld c2_ok=%lld c3_ok=%lld cu_ok=%lld "
+                    "stale=%lld future=%lld zero_len=%lld bad_target=%lld bad_logp=%lld",
+                    (long long)host_summary->c1_ok, (long long)host_summary->c2_ok,
+                    (long long)host_summary->c3_ok, (long long)host_summary->cu_ok,
+                    (long long)host_summary->n_stale, (long long)host_summary->n_future,
+                    (long long)host_summary->n_zero_len, (long long)host_summary->n_bad_target,
+                    (long long)host_summary->n_bad_logp_behav);
+    }
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_advantage(const float *rewards, const int32_t *group_ids,
+                                   const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                   float std_floor, float *adv, float *inv_norm,
+                                   int32_t *group_count, grpo_stream_t stream) {
+    if (N < 0 || P <= 0) return fail(GRPO_ERR_INVALID_ARG, "advantage: N=%d P=%d", N, P);
+    if (!(std_floor > 0.0f)) return fail(GRPO_ERR_INVALID_ARG, "advantage: std_floor must be > 0");
+    if (N > 0 && (!rewards || !group_ids || !cu_seqlens || !adv || !inv_norm))
+        return fail(GRPO_ERR_INVALID_ARG, "advantage: NULL pointer");
+    int launches = 0;
+    cudaError_t e = grpo::launch_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor, adv,
+                                           inv_norm, group_count, (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "advantage");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int64_t n_rows,
+                                  int32_t V, int64_t ld, const int64_t *target_ids,
+                                  const float *logp_behav, const int64_t *cu_seqlens,
+                                  int32_t N, const int32_t *traj_index, const float *adv,
+                                  const float *inv_norm, float eps, float grad_scale,
+                                  float *logp_out, float *lse_out, float *token_scale_out,
+                                  double *traj_sum, double *stats, uint16_t *dlogits,
+                                  void *workspace, size_t workspace_bytes,
+                                  const grpo_tune_t *tune, grpo_stream_t stream) {
+    if (n_rows < 0 || N <= 0 || V <= 0 || row_begin < 0)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: n_rows=%lld N=%d V=%d row_begin=%lld",
+                    (long long)n_rows, N, V, (long long)row_begin);
+    if (!(eps > 0.0f && eps < 1.0f)) return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: eps not in (0,1)");
+    if (!cu_seqlens || !adv || !inv_norm || !traj_sum || !stats)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: NULL cu_seqlens/adv/inv_norm/traj_sum/stats");
+    if (n_rows > 0 && (!logits || !target_ids || !logp_behav))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: NULL logits/target_ids/logp_behav");
+    if (ld < V || (ld % 8) != 0)
+        return fail(GRPO_ERR_ALIGNMENT, "loss_fwd: ld=%lld must be >= V=%d and a multiple of 8",
+                    (long long)ld, V);
+    if ((logits && !aligned16(logits)) || (dlogits && !aligned16(dlogits)))
+        return fail(GRPO_ERR_ALIGNMENT, "loss_fwd: logits/dlogits must be 16-byte aligned");
+    const size_t need = grpo_async_workspace_size(n_rows, V, N);
+    if (!workspace || workspace_bytes < need)
+        return fail(GRPO_ERR_WORKSPACE, "loss_fwd: workspace %zu B < required %zu B",
+                    workspace_bytes, need);
+    if (tune && (tune->kernel < 0 || tune->kernel > 2))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: tune->kernel %d", tune->kernel);
+
+    grpo::LossArgs a;
+    a.logits = logits;
+    a.dlogits = dlogits;
+    a.ld = ld;
+    a.V = V;
+    a.row_begin = row_begin;
+    a.n_rows = n_rows;
+    a.target_ids = target_ids;
+    a.logp_behav = logp_behav;
+    a.cu_seqlens = cu_seqlens;
+    a.N = N;
+    a.traj_index = traj_index;
+    a.adv = adv;
+    a.inv_norm = inv_norm;
+    a.eps = eps;
+    a.grad_scale = grad_scale;
+    a.logp_out = logp_out;
+    a.lse_out = lse_out;
+    a.scale_out = token_scale_out;
+    a.traj_sum = traj_sum;
+    a.stats = stats;
+    uint8_t *w = static_cast<uint8_t *>(workspace);
+    w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(w)));
+    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
+    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
+    a.term_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.logp_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.flag_ws = w;
+    w += align256((size_t)n_rows);
+    a.part_ws = reinterpret_cast<double *>(w);
+
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    cudaError_t e = grpo::launch_rowinfo(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowinfo");
+    const int kernel = tune ? tune->kernel : 0;
+    char why[256] = {0};
+    if (kernel == 2) {
+        e = grpo::launch_fused_rowwise(a, s, &launches);
+        if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");
+    } else {
+        e = grpo::launch_fused_cluster(a, tune, s, &launches, why, sizeof why);
+        if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/fused_cluster", why);
+    }
+    e = grpo::launch_segment_reduce(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/segment_reduce");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
+                                  const int64_t *target_ids, const float *lse,
+                                  const float *token_scale, float grad_scale_mult,
+                                  uint16_t *dlogits, grpo_stream_t stream) {
+    if (n_rows < 0 || V <= 0) return fail(GRPO_ERR_INVALID_ARG, "loss_bwd: n_rows/V");
+    if (n_rows > 0 && (!logits || !target_ids || !lse || !token_scale || !dlogits))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_bwd: NULL pointer");
+    if (ld < V || (ld % 8) != 0)
+        return fail(GRPO_ERR_ALIGNMENT, "loss_bwd: ld=%lld must be >= V and a multiple of 8",
+                    (long long)ld);
+    if ((logits && !aligned16(logits)) || (dlogits && !aligned16(dlogits)))
+        return fail(GRPO_ERR_ALIGNMENT, "loss_bwd: logits/dlogits must be 16-byte aligned");
+    int launches = 0;
+    cudaError_t e = grpo::launch_loss_bwd(logits, n_rows, V, ld, target_ids, lse, token_scale,
+                                          grad_scale_mult, dlogits, (cudaStream_t)stream,
+                                          &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "loss_bwd");
+    return ok(launches);
+}
+
+}  // extern "C"

@@ -1,0 +1,353 @@
+// common.cuh -- sm_100a PTX helpers and shared declarations of the GRPO-async
+// CUDA path (mbarrier, 1-D bulk TMA, cluster/DSMEM, bf16 packing, MUFU ex2).
+// Product code: shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "grpo_async.h"
+
+namespace grpo {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr uint32_t kBf16NegInfPair = 0xFF80FF80u;
+
+// Per-row metadata staged by the row-info kernel (16 bytes, one vector load).
+struct __align__(16) RowInfo {
+    int32_t target;   // y_t (validated to be in [0, V))
+    float logp_w;     // log pi_{w_j}(y_t)
+    float adv;        // A_i of the row's trajectory
+    float inv_norm;   // 1 / (P * G_p * L_i)
+};
+
+// Per-row flags written by the loss kernels (workspace, one byte per row).
+enum : uint8_t { kRowClipped = 1, kRowActive = 2 };
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init_cluster() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile(
+        "{\n\t.reg .b64 st;\n\t"
+        "mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .b64 st;\n\t"
+        "mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "r"(bytes)
+        : "memory");
+}
+
+// Wait for the completion of the phase with the given parity (CTA-local producers).
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Same, with cluster-scope acquire (the phase is completed by peer CTAs' st.async).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// 1-D bulk TMA global -> shared, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t ncluster_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+
+// Shared-memory address of the same variable in CTA `rank` of this cluster.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+// 16-byte remote store that completes 16 bytes of transaction on the remote mbarrier.
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t rbar, float a, float b,
+                                            float c, float d) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, "
+        "[%5];" ::"r"(raddr),
+        "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)),
+        "r"(__float_as_uint(d)), "r"(rbar)
+        : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// 128-bit global load, L1 bypassed, with an L2 eviction-priority policy
+// (evict_first for read-once streams, evict_last for a row re-read from L2).
+__device__ __forceinline__ uint4 ldg_policy(const void *p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+// Streaming 128-bit global store (written once, not re-read by this kernel).
+__device__ __forceinline__ void stg_stream(void *p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// Round-to-nearest-even pack of two floats into bf16x2 (lo in the low half).
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    uint32_t d;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+    return d;
+}
+
+__device__ __forceinline__ uint16_t f2bf(float x) {
+    return static_cast<uint16_t>(pack_bf16x2(x, 0.0f) & 0xFFFFu);
+}
+
+__device__ __forceinline__ uint32_t word_of(const uint4 &x, int q) {
+    return q == 0 ? x.x : (q == 1 ? x.y : (q == 2 ? x.z : x.w));
+}
+
+// Set the bf16 elements e >= valid of an 8-element vector to -inf (ragged row tail).
+__device__ __forceinline__ uint4 mask_tail(uint4 x, int valid) {
+    const uint32_t lo_inf = 0x0000FF80u, hi_inf = 0xFF800000u;
+    x.x = (valid <= 0 ? (x.x & 0xFFFF0000u) | lo_inf : x.x);
+    x.x = (valid <= 1 ? (x.x & 0x0000FFFFu) | hi_inf : x.x);
+    x.y = (valid <= 2 ? (x.y & 0xFFFF0000u) | lo_inf : x.y);
+    x.y = (valid <= 3 ? (x.y & 0x0000FFFFu) | hi_inf : x.y);
+    x.z = (valid <= 4 ? (x.z & 0xFFFF0000u) | lo_inf : x.z);
+    x.z = (valid <= 5 ? (x.z & 0x0000FFFFu) | hi_inf : x.z);
+    x.w = (valid <= 6 ? (x.w & 0xFFFF0000u) | lo_inf : x.w);
+    x.w = (valid <= 7 ? (x.w & 0x0000FFFFu) | hi_inf : x.w);
+    return x;
+}
+
+// Store the first `valid` bf16 elements of an 8-element vector, one 2-byte store each.
+__device__ __forceinline__ void store_tail(uint16_t *dst, const uint4 &d, int valid) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        if (e < valid) {
+            const uint32_t w = word_of(d, e >> 1);
+            dst[e] = (uint16_t)((e & 1) ? (w >> 16) : (w & 0xFFFFu));
+        }
+    }
+}
+
+// Softmax partials live in the log2 domain: a partial (a, s) stands for
+// s * 2^a, i.e. a = a reference point in units of log2(e)*z and
+// s = sum_v 2^(z_v*log2e - a).  A thread takes a = m*log2e rounded UP
+// (__fmul_ru) so that every exponent z*log2e - a it feeds to ex2 is <= 0
+// (no overflow for any finite logit) and the per-element exponent is one FFMA.
+// The same reference is used when partials merge and when the backward
+// recomputes p = 2^(z*log2e - lse2), so forward and backward agree exactly.
+__device__ __forceinline__ float log2_ref(float m) {
+    return m == -INFINITY ? -INFINITY : __fmul_ru(m, kLog2e);
+}
+
+// Merge (a, s) with (b, t).  Symmetric in its two arguments bit for bit, so
+// butterfly reductions leave every lane with the identical result.
+__device__ __forceinline__ void lse2_merge(float &a, float &s, float b, float t) {
+    const float mn = fmaxf(a, b);
+    if (mn == -INFINITY) {
+        a = mn;
+        s = 0.0f;
+        return;
+    }
+    s = s * ex2(a - mn) + t * ex2(b - mn);
+    a = mn;
+}
+
+__device__ __forceinline__ void warp_lse2_allreduce(float &a, float &s) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float b = __shfl_xor_sync(0xFFFFFFFFu, a, off);
+        const float t = __shfl_xor_sync(0xFFFFFFFFu, s, off);
+        lse2_merge(a, s, b, t);
+    }
+}
+
+// Per-row epilogue of eq:grpo_async / eq:ratio_async:
+// r = exp(logp - logp_w), term = min(r A, clip(r) A), clipped iff the clip
+// branch binds strictly, s = grad_scale * inv_norm * A * r * !clipped.
+struct RowOut {
+    float r, term, s;
+    uint8_t flags;
+};
+
+// logp_t = z_y - lse from the row's log2-domain reference M and l2s = log2(S):
+//   logp = (z_y*log2e - M - l2s) * ln2,
+// formed in fp64 (a few DFMA per row) so the ratio r = exp(logp - logp_w) keeps
+// full fp32 accuracy even for very unlikely tokens (|logp| ~ 100).
+__device__ __forceinline__ double row_logp(float zy, float M, float l2s) {
+    const double kLog2eD = 1.4426950408889634074, kLn2D = 0.69314718055994530942;
+    return (fma((double)zy, kLog2eD, -(double)M) - (double)l2s) * kLn2D;
+}
+
+__device__ __forceinline__ RowOut row_epilogue(double logp, const RowInfo &ri, float eps,
+                                               float grad_scale) {
+    RowOut o;
+    const float r = expf((float)(logp - (double)ri.logp_w));
+    const float lo = 1.0f - eps, hi = 1.0f + eps;
+    const float c = fminf(fmaxf(r, lo), hi);
+    const float A = ri.adv;
+    o.r = r;
+    o.term = fminf(r * A, c * A);
+    const bool clipped = (A > 0.0f && r > hi) || (A < 0.0f && r < lo);
+    o.s = clipped ? 0.0f : grad_scale * ri.inv_norm * A * r;
+    o.flags = (clipped ? kRowClipped : 0) | ((!clipped && A != 0.0f) ? kRowActive : 0);
+    return o;
+}
+
+// ------------------------------------------------------------ host launchers
+// All return cudaGetLastError() of their launch; `launches` counts kernels.
+struct LossArgs {
+    const uint16_t *logits;
+    uint16_t *dlogits;
+    int64_t ld;
+    int32_t V;
+    int64_t row_begin;
+    int64_t n_rows;
+    const int64_t *target_ids;
+    const float *logp_behav;
+    const int64_t *cu_seqlens;
+    int32_t N;
+    const int32_t *traj_index;
+    const float *adv;
+    const float *inv_norm;
+    float eps;
+    float grad_scale;
+    float *logp_out;
+    float *lse_out;
+    float *scale_out;
+    double *traj_sum;
+    double *stats;
+    // workspace carve-up
+    RowInfo *rowinfo;      // [n_rows]
+    float *term_ws;        // [n_rows]
+    float *logp_ws;        // [n_rows]
+    uint8_t *flag_ws;      // [n_rows]
+    double *part_ws;       // [N * 5]
+};
+
+cudaError_t launch_rowinfo(const LossArgs &a, cudaStream_t s, int *launches);
+cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
+                                 int *launches, char *why, size_t why_len);
+cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launches);
+cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches);
+cudaError_t launch_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
+                            const int64_t *target_ids, const float *lse, const float *scale,
+                            float mult, uint16_t *dlogits, cudaStream_t s, int *launches);
+cudaError_t launch_validate(const int64_t *version_ids, const int64_t *token_version,
+                            const int64_t *cu, const int32_t *group_ids, const int64_t *targets,
+                            const float *logp_behav, int32_t N, int64_t T, int32_t P, int32_t V,
+                            int32_t G, int32_t tbs, int64_t v_theta, int32_t K, uint32_t *flags,
+                            int32_t *group_count, int32_t *stale_hist,
+                            grpo_validate_summary_t *summary, cudaStream_t s, int *launches);
+cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, const int64_t *cu,
+                             int32_t N, int32_t P, float std_floor, float *adv, float *inv_norm,
+                             int32_t *group_count, cudaStream_t s, int *launches);
+
+}  // namespace grpo

@@ -1,0 +1,338 @@
+// loss_aux.cu -- the smaller kernels around the fused loss:
+//   rowinfo_kernel      row -> trajectory lookup (binary search over cu_seqlens) and
+//                       the per-row metadata the fused kernel streams (16 B per row)
+//   rowwise_kernel      a simple fused fwd+bwd variant: one CTA per row, two
+//                       passes over the row (the second re-reads from L2)
+//   segsum_kernel       deterministic per-trajectory segmented sums of term_t
+//                       (eq:grpo_async's sum_t) and per-chunk counters
+//   stats_kernel        fixed-order reduction of the trajectory partials into
+//                       J's chunk contribution  sum_i inv_norm_i * sum_t term_t
+//   bwd_kernel          unfused backward: dlogits = s (exp(z - lse) - onehot)
+#include "common.cuh"
+
+namespace grpo {
+
+// ------------------------------------------------------------------ row info
+__global__ void rowinfo_kernel(int64_t row_begin, int64_t n_rows, const int64_t *__restrict__ cu,
+                               int32_t N, const int32_t *__restrict__ traj_index,
+                               const int64_t *__restrict__ targets,
+                               const float *__restrict__ logp_behav,
+                               const float *__restrict__ adv,
+                               const float *__restrict__ inv_norm, RowInfo *__restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_rows;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = row_begin + k;
+        RowInfo ri;
+        const int64_t y = targets[k];
+        ri.target = (y >= 0 && y < 0x7FFFFFFF) ? (int32_t)y : -1;
+        ri.logp_w = logp_behav[k];
+        ri.adv = 0.0f;
+        ri.inv_norm = 0.0f;
+        if (t >= cu[0] && t < cu[N]) {
+            // largest i with cu[i] <= t  (then cu[i+1] > t)
+            int32_t lo = 0, hi = N;
+            while (hi - lo > 1) {
+                const int32_t mid = (lo + hi) >> 1;
+                if (cu[mid] <= t) lo = mid;
+                else hi = mid;
+            }
+            const int32_t ti = traj_index ? traj_index[lo] : lo;
+            ri.adv = adv[ti];
+            ri.inv_norm = inv_norm[ti];
+        }
+        out[k] = ri;
+    }
+}
+
+cudaError_t launch_rowinfo(const LossArgs &a, cudaStream_t s, int *launches) {
+    if (a.n_rows == 0) return cudaSuccess;
+    int64_t blocks = (a.n_rows + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    rowinfo_kernel<<<(unsigned)blocks, 256, 0, s>>>(a.row_begin, a.n_rows, a.cu_seqlens, a.N,
+                                                    a.traj_index, a.target_ids, a.logp_behav,
+                                                    a.adv, a.inv_norm, a.rowinfo);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ row-wise fused variant
+struct RowwiseParams {
+    const uint16_t *logits;
+    uint16_t *dlogits;
+    int64_t ld;
+    int32_t V;
+    int64_t n_rows;
+    const RowInfo *rowinfo;
+    float eps, grad_scale;
+    float *logp_out, *lse_out, *scale_out, *term_ws, *logp_ws;
+    uint8_t *flag_ws;
+};
+
+__global__ void __launch_bounds__(256) rowwise_kernel(const RowwiseParams p) {
+    __shared__ float2 red[8];
+    __shared__ float row_scalars[3];  // lse2 (log2 domain), s, zy
+    const int n_vec = (p.V + 7) / 8;
+    const int tail_valid = p.V - (n_vec - 1) * 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+    for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
+        const uint16_t *zrow = p.logits + row * p.ld;
+        float a = -INFINITY, s = 0.0f;   // log2-domain partial (common.cuh)
+        for (int vi = threadIdx.x; vi < n_vec; vi += blockDim.x) {
+            uint4 x = ldg_policy(zrow + (int64_t)vi * 8, pol_keep);
+            if (vi == n_vec - 1 && tail_valid < 8) x = mask_tail(x, tail_valid);
+            const uint32_t mx2 = bmax2(bmax2(x.x, x.y), bmax2(x.z, x.w));
+            const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
+            if (va == -INFINITY) continue;
+            float t = 0.0f;
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                t += ex2(fmaf(bf_lo(w[q]), kLog2e, -va)) + ex2(fmaf(bf_hi(w[q]), kLog2e, -va));
+            lse2_merge(a, s, va, t);
+        }
+        warp_lse2_allreduce(a, s);
+        if (lane == 0) red[warp] = make_float2(a, s);
+        __syncthreads();
+        if (warp == 0) {
+            float cm = -INFINITY, cs = 0.0f;
+            if (lane < 8) {
+                cm = red[lane].x;
+                cs = red[lane].y;
+            }
+            warp_lse2_allreduce(cm, cs);
+            if (lane == 0) {
+                const RowInfo ri = p.rowinfo[row];
+                const bool y_valid = ri.target >= 0 && ri.target < p.V;
+                const float zy = y_valid ? __uint_as_float(((uint32_t)zrow[ri.target]) << 16)
+                                         : __int_as_float(0x7FC00000);
+                const float l2s = log2f(cs);
+                const float lse2 = cm + l2s;
+                const float lse = lse2 * kLn2;
+                const double logp_d = row_logp(zy, cm, l2s);
+                const float logp = (float)logp_d;
+                const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
+                if (p.logp_out) p.logp_out[row] = logp;
+                if (p.lse_out) p.lse_out[row] = lse;
+                if (p.scale_out) p.scale_out[row] = o.s;
+                p.term_ws[row] = o.term;
+                p.logp_ws[row] = logp;
+                p.flag_ws[row] = o.flags;
+                row_scalars[0] = lse2;
+                row_scalars[1] = o.s;
+                row_scalars[2] = zy;
+            }
+        }
+        __syncthreads();
+        if (p.dlogits) {
+            const float off = row_scalars[0];
+            const float sc = row_scalars[1];
+            const int32_t y = p.rowinfo[row].target;
+            uint16_t *drow = p.dlogits + row * p.ld;
+            for (int vi = threadIdx.x; vi < n_vec; vi += blockDim.x) {
+                uint4 d = make_uint4(0u, 0u, 0u, 0u);
+                if (sc != 0.0f) {
+                    const uint4 x = ldg_policy(zrow + (int64_t)vi * 8, pol_stream);
+                    d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.x), kLog2e, -off)),
+                                      sc * ex2(fmaf(bf_hi(x.x), kLog2e, -off)));
+                    d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.y), kLog2e, -off)),
+                                      sc * ex2(fmaf(bf_hi(x.y), kLog2e, -off)));
+                    d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.z), kLog2e, -off)),
+                                      sc * ex2(fmaf(bf_hi(x.z), kLog2e, -off)));
+                    d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.w), kLog2e, -off)),
+                                      sc * ex2(fmaf(bf_hi(x.w), kLog2e, -off)));
+                }
+                if (vi == n_vec - 1 && tail_valid < 8) {
+                    store_tail(drow + (int64_t)vi * 8, d, tail_valid);
+                } else {
+                    stg_stream(drow + (int64_t)vi * 8, d);
+                }
+                if (y >= 0 && y < p.V && (y >> 3) == vi) {
+                    const float py = ex2(fmaf(row_scalars[2], kLog2e, -off));
+                    drow[y] = f2bf(sc * (py - 1.0f));
+                }
+            }
+        }
+        __syncthreads();  // row_scalars / red reused by the next row
+    }
+}
+
+cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launches) {
+    if (a.n_rows == 0) return cudaSuccess;
+    RowwiseParams p;
+    p.logits = a.logits;
+    p.dlogits = a.dlogits;
+    p.ld = a.ld;
+    p.V = a.V;
+    p.n_rows = a.n_rows;
+    p.rowinfo = a.rowinfo;
+    p.eps = a.eps;
+    p.grad_scale = a.grad_scale;
+    p.logp_out = a.logp_out;
+    p.lse_out = a.lse_out;
+    p.scale_out = a.scale_out;
+    p.term_ws = a.term_ws;
+    p.logp_ws = a.logp_ws;
+    p.flag_ws = a.flag_ws;
+    int64_t blocks = a.n_rows < 148 * 8 ? a.n_rows : 148 * 8;
+    rowwise_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ segmented reduce
+// One warp per trajectory i: its rows inside this chunk, summed in fp64 in a
+// fixed order (lane-strided sequential sums, then an xor butterfly whose
+// result is identical in every lane).  part[i*5 + {0..4}] =
+// {inv_norm*sum term, inv_norm*sum |term|, sum logp, #clipped, #active}.
+__global__ void segsum_kernel(int64_t row_begin, int64_t n_rows, const int64_t *__restrict__ cu,
+                              int32_t N, const int32_t *__restrict__ traj_index,
+                              const float *__restrict__ inv_norm,
+                              const float *__restrict__ term, const float *__restrict__ logp,
+                              const uint8_t *__restrict__ flags, double *__restrict__ traj_sum,
+                              double *__restrict__ part) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (i >= N) return;
+    const int64_t row_end = row_begin + n_rows;
+    const int64_t b = max(cu[i], row_begin), e = min(cu[i + 1], row_end);
+    double st = 0.0, sa = 0.0, sl = 0.0, nc = 0.0, na = 0.0;
+    for (int64_t t = b + lane; t < e; t += 32) {
+        const int64_t k = t - row_begin;
+        const double x = (double)term[k];
+        st += x;
+        sa += fabs(x);
+        sl += (double)logp[k];
+        const uint8_t f = flags[k];
+        nc += (f & kRowClipped) ? 1.0 : 0.0;
+        na += (f & kRowActive) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        st += __shfl_xor_sync(0xFFFFFFFFu, st, off);
+        sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
+        sl += __shfl_xor_sync(0xFFFFFFFFu, sl, off);
+        nc += __shfl_xor_sync(0xFFFFFFFFu, nc, off);
+        na += __shfl_xor_sync(0xFFFFFFFFu, na, off);
+    }
+    if (lane == 0) {
+        const double w = (double)inv_norm[traj_index ? traj_index[i] : i];
+        if (e > b) traj_sum[i] += st;
+        part[i * 5 + 0] = w * st;
+        part[i * 5 + 1] = w * sa;
+        part[i * 5 + 2] = sl;
+        part[i * 5 + 3] = nc;
+        part[i * 5 + 4] = na;
+    }
+}
+
+// One CTA: fixed-order sums of the N partials into stats[] (deterministic).
+__global__ void __launch_bounds__(1024) stats_kernel(int32_t N, int64_t n_rows,
+                                                     const double *__restrict__ part,
+                                                     double *__restrict__ stats) {
+    __shared__ double sh[5][1024];
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t i = threadIdx.x; i < N; i += 1024)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[q] += part[i * 5 + q];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) sh[q][threadIdx.x] = acc[q];
+    __syncthreads();
+    for (int w = 512; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w)
+#pragma unroll
+            for (int q = 0; q < 5; ++q) sh[q][threadIdx.x] += sh[q][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        stats[GRPO_STAT_J] += sh[0][0];
+        stats[GRPO_STAT_ABS] += sh[1][0];
+        stats[GRPO_STAT_LOGP] += sh[2][0];
+        stats[GRPO_STAT_CLIPPED] += sh[3][0];
+        stats[GRPO_STAT_ACTIVE] += sh[4][0];
+        stats[GRPO_STAT_ROWS] += (double)n_rows;
+    }
+}
+
+cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches) {
+    const int64_t threads = (int64_t)a.N * 32;
+    segsum_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+        a.row_begin, a.n_rows, a.cu_seqlens, a.N, a.traj_index, a.inv_norm, a.term_ws, a.logp_ws,
+        a.flag_ws, a.traj_sum, a.part_ws);
+    stats_kernel<<<1, 1024, 0, s>>>(a.N, a.n_rows, a.part_ws, a.stats);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ unfused backward
+constexpr int kBwdVecPerThread = 4;
+
+__global__ void __launch_bounds__(256)
+    bwd_kernel(const uint16_t *__restrict__ logits, int64_t n_rows, int32_t V, int64_t ld,
+               const int64_t *__restrict__ targets, const float *__restrict__ lse,
+               const float *__restrict__ scale, float mult, uint16_t *dlogits,
+               int32_t tiles_per_row) {
+    const int n_vec = (V + 7) / 8;
+    const int tail_valid = V - (n_vec - 1) * 8;
+    const int64_t n_items = n_rows * tiles_per_row;
+    const uint64_t pol_stream = policy_evict_first();
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int64_t row = item / tiles_per_row;
+        const int tile = (int)(item - row * tiles_per_row);
+        const float sc = scale[row] * mult;
+        const float off = lse[row] * kLog2e;
+        const int64_t y = targets[row];
+        const uint16_t *zrow = logits + row * ld;
+        uint16_t *drow = dlogits + row * ld;
+        const int v0 = tile * 256 * kBwdVecPerThread + threadIdx.x;
+        // z_y is read before any store of this thread (dlogits may alias logits)
+        const int yv = (y >= 0 && y < V) ? (int)(y >> 3) : -1;
+        const bool y_mine = yv >= v0 && (yv - v0) % 256 == 0 && (yv - v0) / 256 < kBwdVecPerThread;
+        const float zy = y_mine ? __uint_as_float(((uint32_t)zrow[y]) << 16) : 0.0f;
+        uint4 x[kBwdVecPerThread];
+#pragma unroll
+        for (int j = 0; j < kBwdVecPerThread; ++j) {
+            const int vi = v0 + j * 256;
+            x[j] = (vi < n_vec && sc != 0.0f) ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream)
+                                              : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int j = 0; j < kBwdVecPerThread; ++j) {
+            const int vi = v0 + j * 256;
+            if (vi >= n_vec) break;
+            uint4 d = make_uint4(0u, 0u, 0u, 0u);
+            if (sc != 0.0f) {
+                d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].x), kLog2e, -off)),
+                                  sc * ex2(fmaf(bf_hi(x[j].x), kLog2e, -off)));
+                d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].y), kLog2e, -off)),
+                                  sc * ex2(fmaf(bf_hi(x[j].y), kLog2e, -off)));
+                d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].z), kLog2e, -off)),
+                                  sc * ex2(fmaf(bf_hi(x[j].z), kLog2e, -off)));
+                d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].w), kLog2e, -off)),
+                                  sc * ex2(fmaf(bf_hi(x[j].w), kLog2e, -off)));
+            }
+            if (vi == n_vec - 1 && tail_valid < 8) {
+                store_tail(drow + (int64_t)vi * 8, d, tail_valid);
+            } else {
+                stg_stream(drow + (int64_t)vi * 8, d);
+            }
+            if (y_mine && yv == vi) drow[y] = f2bf(sc * (ex2(fmaf(zy, kLog2e, -off)) - 1.0f));
+        }
+    }
+}
+
+cudaError_t launch_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
+                            const int64_t *target_ids, const float *lse, const float *scale,
+                            float mult, uint16_t *dlogits, cudaStream_t s, int *launches) {
+    if (n_rows == 0) return cudaSuccess;
+    const int n_vec = (V + 7) / 8;
+    const int tiles = (n_vec + 256 * kBwdVecPerThread - 1) / (256 * kBwdVecPerThread);
+    int64_t items = n_rows * tiles;
+    int64_t blocks = items < 148 * 8 ? items : 148 * 8;
+    bwd_kernel<<<(unsigned)blocks, 256, 0, s>>>(logits, n_rows, V, ld, target_ids, lse, scale,
+                                                mult, dlogits, tiles);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace grpo

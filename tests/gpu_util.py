@@ -1,0 +1,138 @@
+"""Helpers shared by the -m gpu parity tests: run the CUDA path through the C ABI
+and the fp64 oracle on the same seeded inputs, and compare them under the
+tolerances of BASELINE.json north_star / DESIGN.md "Parity"."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import oracle.oracle as O
+import paper_2604_26256_b200 as G
+from synth.gen import bf16_bits_to_f32
+
+EPS32 = float(np.float32(0.2))
+
+
+def to_dev_bits(bits: np.ndarray, device) -> torch.Tensor:
+    """uint16 numpy bf16 bit patterns -> int16 CUDA tensor (same bits)."""
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).to(device)
+
+
+def dev_bits_to_f64(t: torch.Tensor, V: int) -> np.ndarray:
+    b = t.cpu().numpy().view(np.uint16)[:, :V]
+    return bf16_bits_to_f32(b).astype(np.float64)
+
+
+def run_gpu(batch, logits_bits, device, tune=None, chunks=1, inplace=False, want_dlogits=True,
+            grad_scale=1.0, eps=0.2):
+    """Whole path on the GPU: validate, advantage, fused loss over `chunks` row chunks."""
+    db = G.DeviceBatch.from_host(batch, device)
+    loss = G.GrpoAsyncLoss(eps=eps, grad_scale=grad_scale, tune=tune)
+    vo = loss.validate(db)
+    adv, inv = loss.advantage(db)
+    T, ld, V = batch.T, batch.ld, batch.V
+    lg = to_dev_bits(logits_bits, device)
+    assert lg.shape == (T, ld)
+    dl = None
+    if want_dlogits:
+        dl = lg if inplace else torch.full((T, ld), 0x7FC3, dtype=torch.int16, device=device)
+    logp = torch.full((T,), float("nan"), device=device)
+    lse = torch.full((T,), float("nan"), device=device)
+    scale = torch.full((T,), float("nan"), device=device)
+    traj_sum = torch.zeros(batch.N, dtype=torch.float64, device=device)
+    stats = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=device)
+    bounds = np.linspace(0, T, chunks + 1).astype(np.int64)
+    for c in range(chunks):
+        b, e = int(bounds[c]), int(bounds[c + 1])
+        loss.loss_chunk(lg[b:e] if e > b else lg[:0], b, e - b, db.target_ids[b:e],
+                        db.logp_behav[b:e], db.cu_seqlens, adv, inv, traj_sum, stats,
+                        dlogits=(dl[b:e] if dl is not None else None), logp_out=logp[b:e],
+                        lse_out=lse[b:e], scale_out=scale[b:e], V=V)
+    torch.cuda.synchronize()
+    out = dict(
+        traj_flags=vo.traj_flags.cpu().numpy().view(np.uint32)[:batch.N],
+        group_count=vo.group_count.cpu().numpy(),
+        stale_hist=vo.stale_hist.cpu().numpy().reshape(batch.P, batch.K + 1),
+        summary=vo.summary_dict(),
+        adv=adv.cpu().numpy(), inv_norm=inv.cpu().numpy(),
+        logp=logp.cpu().numpy().astype(np.float64), lse=lse.cpu().numpy().astype(np.float64),
+        scale=scale.cpu().numpy().astype(np.float64),
+        traj_sum=traj_sum.cpu().numpy(), stats=stats.cpu().numpy(),
+        launches=loss.launches, inplace=inplace)
+    if want_dlogits:
+        out["dlogits_raw"] = dl.cpu().numpy().view(np.uint16)
+        out["dlogits"] = bf16_bits_to_f32(out["dlogits_raw"][:, :V]).astype(np.float64)
+    return out
+
+
+def run_oracle(batch, logits_bits, want_dlogits=True, eps=0.2, grad_scale=1.0):
+    return O.run_batch(batch, logits_bits, eps=eps, grad_scale=grad_scale,
+                       std_floor=float(np.float32(1e-8)), want_dlogits=want_dlogits)
+
+
+def near_boundary(r, eps=EPS32, tol=1e-5):
+    return (np.abs(r - (1 + eps)) <= tol) | (np.abs(r - (1 - eps)) <= tol)
+
+
+def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5, dl_rel=1e-2,
+            logits_pad=None):
+    """Assert the north_star criteria; returns a dict of measured errors."""
+    rr = ref["rows"]
+    errs = {}
+    # bit-exact integer outputs
+    assert np.array_equal(gpu["traj_flags"], ref["validate"]["traj_flags"]), "traj_flags"
+    assert np.array_equal(gpu["group_count"], ref["validate"]["group_count"]), "group_count"
+    assert np.array_equal(gpu["stale_hist"], ref["validate"]["stale_hist"]), "stale_hist"
+    assert gpu["summary"] == ref["validate"]["summary"], (gpu["summary"], ref["validate"]["summary"])
+    # advantages: same fp64 order -> identical after rounding to f32
+    assert np.array_equal(gpu["adv"], ref["adv"].astype(np.float32)), "adv"
+    assert np.array_equal(gpu["inv_norm"], ref["inv_norm"].astype(np.float32)), "inv_norm"
+    # per-token log-probs
+    errs["logp_max_abs"] = float(np.max(np.abs(gpu["logp"] - rr.logp))) if batch.T else 0.0
+    assert errs["logp_max_abs"] <= logp_atol, errs
+    errs["lse_max_abs"] = float(np.max(np.abs(gpu["lse"] - rr.lse))) if batch.T else 0.0
+    assert errs["lse_max_abs"] <= logp_atol
+    # loss (guarded relative criterion, Z17)
+    J_ref = ref["J"]
+    S_abs = float(np.sum(ref["inv_norm"][np.repeat(np.arange(batch.N), batch.lengths)] *
+                         np.abs(rr.term)))
+    J_gpu = gpu["stats"][G.STAT_J]
+    errs["J_ref"], errs["J_gpu"] = J_ref, J_gpu
+    errs["J_rel_guarded"] = abs(J_gpu - J_ref) / max(abs(J_ref), 1e-2 * S_abs, 1e-300)
+    errs["J_rel_raw"] = abs(J_gpu - J_ref) / max(abs(J_ref), 1e-300)
+    assert errs["J_rel_guarded"] <= loss_rtol, errs
+    assert abs(gpu["stats"][G.STAT_ABS] - S_abs) <= 1e-5 * S_abs + 1e-300
+    # per-trajectory sums of terms (fp64 reductions of fp32 terms)
+    ts_scale = np.maximum(np.abs(ref["traj_sum"]), 1e-3 * batch.lengths)
+    assert np.all(np.abs(gpu["traj_sum"] - ref["traj_sum"]) <= 1e-5 * ts_scale + 1e-6), "traj_sum"
+    # clip decisions: fp32 vs fp64 may differ only within 1e-5 of a clip boundary
+    nb = near_boundary(rr.r)
+    clipped_gpu_s = gpu["scale"] == 0.0
+    oracle_zero_s = rr.s == 0.0
+    mism = (clipped_gpu_s != oracle_zero_s) & ~nb
+    assert not mism.any(), f"{mism.sum()} clip decisions differ away from a boundary"
+    errs["boundary_flips"] = int(((clipped_gpu_s != oracle_zero_s) & nb).sum())
+    assert abs(gpu["stats"][G.STAT_CLIPPED] - ref["n_clipped"]) <= errs["boundary_flips"]
+    assert gpu["stats"][G.STAT_ROWS] == batch.T
+    # token scale s_t (fp32) vs oracle
+    ok_s = ~nb
+    if ok_s.any():
+        ds = np.abs(gpu["scale"][ok_s] - rr.s[ok_s])
+        errs["scale_max_rel"] = float(np.max(ds / np.maximum(np.abs(rr.s[ok_s]), 1e-30)))
+        assert np.all(ds <= 1e-4 * np.abs(rr.s[ok_s]) + 1e-12)
+    if check_dlogits and "dlogits" in gpu:
+        ref_dl = rr.dlogits
+        got = gpu["dlogits"]
+        num = np.linalg.norm(got - ref_dl)
+        den = np.linalg.norm(ref_dl)
+        errs["dlogits_rel_l2"] = float(num / den) if den > 0 else float(num)
+        assert (errs["dlogits_rel_l2"] <= dl_rel) if den > 0 else num == 0.0, errs
+        zero_rows = (rr.s == 0.0) & ~nb
+        assert np.all(got[zero_rows] == 0.0), "rows with s = 0 must be exactly zero"
+        # padding columns [V, ld) are never written
+        raw = gpu["dlogits_raw"]
+        if raw.shape[1] > batch.V:
+            pad = raw[:, batch.V:]
+            expect = logits_pad if gpu["inplace"] else np.uint16(0x7FC3)
+            assert np.all(pad == expect), "padding columns of dlogits were written"
+    return errs
