@@ -205,6 +205,19 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
 /* Bytes of device workspace grpo_async_loss_fwd needs for a chunk. */
 size_t grpo_async_workspace_size(int64_t n_rows, int32_t V, int32_t N);
 
+/*
+ * Kernel tracing for benchmarks.  While enabled (process-wide), every launch
+ * of the fused loss kernel (grpo_async_loss_fwd's main kernel, whichever
+ * variant tune selects) is bracketed by two CUDA events recorded on the
+ * launch's stream.  grpo_profile_collect() waits for the recorded events,
+ * returns how many launches were traced since the last collect and the sum of
+ * their durations in milliseconds, and recycles the events.
+ * Errors: GRPO_ERR_CUDA (event creation/synchronization), GRPO_ERR_INVALID_ARG
+ * (NULL outputs).
+ */
+grpo_status_t grpo_profile_enable(int32_t on);
+grpo_status_t grpo_profile_collect(int32_t *n_launches, double *total_ms);
+
 /* Number of kernels the last successful call of the calling thread launched
  * (for launch accounting in benchmarks). */
 int32_t grpo_last_launch_count(void);

@@ -32,7 +32,8 @@ SUMMARY_FIELDS = ("n_traj", "n_tokens", "n_stale", "n_future", "n_zero_len", "n_
 
 EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advantage",
             "grpo_async_loss_fwd", "grpo_async_loss_bwd", "grpo_async_workspace_size",
-            "grpo_last_launch_count", "grpo_last_error", "grpo_version")
+            "grpo_profile_enable", "grpo_profile_collect", "grpo_last_launch_count",
+            "grpo_last_error", "grpo_version")
 
 
 class ValidateSummary(C.Structure):
@@ -55,8 +56,8 @@ class GrpoError(RuntimeError):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m "
-                          "paper_2604_26256_b200.build` (there is no CPU fallback)")
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python "
+                          "paper_2604_26256_b200/build.py` (there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     P, i32, i64, f32, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_size_t
     st = C.c_int
@@ -75,6 +76,10 @@ def _load():
     lib.grpo_async_loss_bwd.restype = st
     lib.grpo_async_workspace_size.argtypes = [i64, i32, i32]
     lib.grpo_async_workspace_size.restype = sz
+    lib.grpo_profile_enable.argtypes = [i32]
+    lib.grpo_profile_enable.restype = st
+    lib.grpo_profile_collect.argtypes = [P, P]
+    lib.grpo_profile_collect.restype = st
     lib.grpo_last_launch_count.argtypes = []
     lib.grpo_last_launch_count.restype = i32
     lib.grpo_last_error.argtypes = []
@@ -110,6 +115,18 @@ def _stream(stream):
 def _check(status):
     if status != GRPO_OK:
         raise GrpoError(status, LIB.grpo_last_error().decode())
+
+
+def grpo_profile_enable(on: bool) -> None:
+    _check(LIB.grpo_profile_enable(1 if on else 0))
+
+
+def grpo_profile_collect():
+    """(launches traced since the last collect, their total duration in ms)."""
+    n = C.c_int32()
+    ms = C.c_double()
+    _check(LIB.grpo_profile_collect(C.byref(n), C.byref(ms)))
+    return int(n.value), float(ms.value)
 
 
 def grpo_last_launch_count() -> int:

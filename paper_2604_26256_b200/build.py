@@ -1,6 +1,6 @@
 """Build the in-tree CUDA shared library libgrpo_async.so for sm_100a.
 
-    python -m paper_2604_26256_b200.build        # or __graft_entry__.build()
+    python paper_2604_26256_b200/build.py [--force]     # or __graft_entry__.build()
 
 nvcc cross-compiles here without a GPU; the .so travels to the GPU box with
 the gpurun snapshot.  cudart is linked statically so the library does not

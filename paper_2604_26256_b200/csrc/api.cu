@@ -3,7 +3,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -33,6 +36,40 @@ grpo_status_t cuda_fail(cudaError_t e, const char *where, const char *why = null
                 why ? why : "");
 }
 
+// ---- kernel tracing (grpo_profile_*)
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_pending, g_prof_free;
+
+bool prof_on() {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    return g_prof_on;
+}
+
+cudaError_t prof_begin(cudaStream_t s, std::pair<cudaEvent_t, cudaEvent_t> *ev) {
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        if (!g_prof_free.empty()) {
+            *ev = g_prof_free.back();
+            g_prof_free.pop_back();
+        } else {
+            ev->first = ev->second = nullptr;
+        }
+    }
+    cudaError_t e = cudaSuccess;
+    if (!ev->first) e = cudaEventCreate(&ev->first);
+    if (e == cudaSuccess && !ev->second) e = cudaEventCreate(&ev->second);
+    if (e == cudaSuccess) e = cudaEventRecord(ev->first, s);
+    return e;
+}
+
+cudaError_t prof_end(cudaStream_t s, const std::pair<cudaEvent_t, cudaEvent_t> &ev) {
+    cudaError_t e = cudaEventRecord(ev.second, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_pending.push_back(ev);
+    return e;
+}
+
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -42,6 +79,38 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 extern "C" {
 
 const char *grpo_last_error(void) { return g_last_error.c_str(); }
+
+grpo_status_t grpo_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+    return ok(0);
+}
+
+grpo_status_t grpo_profile_collect(int32_t *n_launches, double *total_ms) {
+    if (!n_launches || !total_ms) return fail(GRPO_ERR_INVALID_ARG, "profile_collect: NULL output");
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pend;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        pend.swap(g_prof_pending);
+    }
+    double tot = 0.0;
+    cudaError_t err = cudaSuccess;
+    for (auto &ev : pend) {
+        float ms = 0.0f;
+        cudaError_t e = cudaEventSynchronize(ev.second);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev.first, ev.second);
+        if (e != cudaSuccess && err == cudaSuccess) err = e;
+        tot += ms;
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_prof_free.insert(g_prof_free.end(), pend.begin(), pend.end());
+    }
+    if (err != cudaSuccess) return cuda_fail(err, "profile_collect");
+    *n_launches = (int32_t)pend.size();
+    *total_ms = tot;
+    return ok(0);
+}
 
 int32_t grpo_last_launch_count(void) { return g_last_launches; }
 
@@ -197,6 +266,9 @@ grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int
     if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowinfo");
     const int kernel = tune ? tune->kernel : 0;
     char why[256] = {0};
+    const bool traced = n_rows > 0 && prof_on();
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
     if (kernel == 2) {
         e = grpo::launch_fused_rowwise(a, s, &launches);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");
@@ -204,6 +276,7 @@ grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int
         e = grpo::launch_fused_cluster(a, tune, s, &launches, why, sizeof why);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/fused_cluster", why);
     }
+    if (traced && (e = prof_end(s, ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
     e = grpo::launch_segment_reduce(a, s, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/segment_reduce");
     return ok(launches);

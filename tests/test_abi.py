@@ -1,0 +1,94 @@
+"""-m "not gpu": the C-ABI library loads and exports every symbol include/grpo_async.h
+declares; host-side argument checks return their documented status codes without
+touching the GPU (no compute calls here)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "grpo_async.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(grpo_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for n in ("grpo_async_advantage", "grpo_async_loss_fwd", "grpo_async_loss_bwd",
+              "grpo_async_validate"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2604_26256_b200._lib as L
+    lib = C.CDLL(L.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(L.EXPORTED) == set(declared_functions())
+
+
+def test_binding_names_match_c_entry_points():
+    import paper_2604_26256_b200 as G
+    for n in declared_functions():
+        assert hasattr(G._lib, n), n
+
+
+def test_host_side_errors_without_gpu():
+    """Argument errors are detected on the host before any CUDA call."""
+    import paper_2604_26256_b200._lib as L
+    lib = L.LIB
+    ws = L.LIB.grpo_async_workspace_size(100, 1000, 4)
+    assert ws >= 100 * 16
+    fake = C.c_void_p(16)  # never dereferenced: every call below fails its host checks first
+    # N <= 0
+    st = lib.grpo_async_loss_fwd(fake, 0, 10, 1000, 1000, fake, fake, fake, 0, None, fake, fake,
+                                 0.2, 1.0, None, None, None, fake, fake, None, fake, ws, None, None)
+    assert st == L.GRPO_ERR_INVALID_ARG and b"N=0" in lib.grpo_last_error()
+    # eps out of range
+    st = lib.grpo_async_loss_fwd(fake, 0, 10, 1000, 1000, fake, fake, fake, 4, None, fake, fake,
+                                 1.5, 1.0, None, None, None, fake, fake, None, fake, ws, None, None)
+    assert st == L.GRPO_ERR_INVALID_ARG
+    # ld % 8 != 0 and ld < V
+    for ld in (1001, 999):
+        st = lib.grpo_async_loss_fwd(fake, 0, 10, 1000, ld, fake, fake, fake, 4, None, fake, fake,
+                                     0.2, 1.0, None, None, None, fake, fake, None, fake, ws, None,
+                                     None)
+        assert st == L.GRPO_ERR_ALIGNMENT
+    # misaligned logits pointer
+    st = lib.grpo_async_loss_fwd(C.c_void_p(18), 0, 10, 1000, 1000, fake, fake, fake, 4, None, fake,
+                                 fake, 0.2, 1.0, None, None, None, fake, fake, None, fake, ws, None,
+                                 None)
+    assert st == L.GRPO_ERR_ALIGNMENT
+    # workspace too small
+    st = lib.grpo_async_loss_fwd(fake, 0, 10, 1000, 1000, fake, fake, fake, 4, None, fake, fake,
+                                 0.2, 1.0, None, None, None, fake, fake, None, fake, 8, None, None)
+    assert st == L.GRPO_ERR_WORKSPACE
+    # advantage: std_floor <= 0, P <= 0
+    assert lib.grpo_async_advantage(fake, fake, fake, 4, 1, 0.0, fake, fake, None,
+                                    None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_advantage(fake, fake, fake, 4, 0, 1e-8, fake, fake, None,
+                                    None) == L.GRPO_ERR_INVALID_ARG
+    # validate: K < 0, NULL summary
+    assert lib.grpo_async_validate(fake, None, fake, fake, fake, None, 4, 10, 1, 100, 4, 4, 1000,
+                                   -1, fake, fake, fake, fake, None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_validate(fake, None, fake, fake, fake, None, 4, 10, 1, 100, 4, 4, 1000,
+                                   1, fake, fake, fake, None, None) == L.GRPO_ERR_INVALID_ARG
+    # loss_bwd: NULL lse
+    assert lib.grpo_async_loss_bwd(fake, 10, 100, 104, fake, None, fake, 1.0, fake,
+                                   None) == L.GRPO_ERR_INVALID_ARG
+    # profile collect with NULL outputs
+    assert lib.grpo_profile_collect(None, None) == L.GRPO_ERR_INVALID_ARG
+
+
+def test_package_has_no_cpu_fallback():
+    """The product package never imports the oracle; the binding only marshals."""
+    pkg = os.path.join(ROOT, "paper_2604_26256_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in src.replace("oracle/", "").lower() or fn == "build.py", fn
