@@ -95,7 +95,9 @@ typedef struct {
     int32_t kernel;        /* 0 auto, 1 cluster-resident fused (roofline design), 2 row-wise two-pass */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
     int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1)                                    */
-    int32_t stages;        /* 0 auto, else 1..8 shared-memory row stages per CTA (kernel 1)   */
+    int32_t stages;        /* 0 auto, else lag+2..8 shared-memory row stages per CTA (kernel 1) */
+    int32_t lag;           /* 0 auto (1), else 1..2: rows between a row's reduction and its   */
+                           /* backward, hiding the cluster exchange (kernel 1)               */
 } grpo_tune_t;
 
 /*
@@ -201,6 +203,21 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
                                   const int64_t *target_ids, const float *lse,
                                   const float *token_scale, float grad_scale_mult,
                                   uint16_t *dlogits, grpo_stream_t stream);
+
+/* Launch plan of the last fused-loss launch made by the calling thread. */
+typedef struct {
+    int32_t kernel;        /* 1 cluster-resident, 2 row-wise                          */
+    int32_t cluster_size;  /* CTAs per row (kernel 1)                                 */
+    int32_t ctas_per_sm;   /* requested residency (kernel 1)                          */
+    int32_t stages;        /* shared-memory row stages per CTA (kernel 1)             */
+    int32_t vec_per_thread;/* 8-element vectors held in registers per thread          */
+    int32_t grid;          /* CTAs launched                                           */
+    int32_t max_clusters;  /* co-resident clusters the occupancy query allows         */
+    int32_t smem_bytes;    /* dynamic shared memory per CTA                           */
+    int32_t lag;           /* reduction-to-backward lag in rows (kernel 1)            */
+} grpo_plan_t;
+
+grpo_status_t grpo_async_last_plan(grpo_plan_t *out);
 
 /* Bytes of device workspace grpo_async_loss_fwd needs for a chunk. */
 size_t grpo_async_workspace_size(int64_t n_rows, int32_t V, int32_t N);

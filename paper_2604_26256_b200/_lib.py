@@ -32,7 +32,8 @@ SUMMARY_FIELDS = ("n_traj", "n_tokens", "n_stale", "n_future", "n_zero_len", "n_
 
 EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advantage",
             "grpo_async_loss_fwd", "grpo_async_loss_bwd", "grpo_async_workspace_size",
-            "grpo_profile_enable", "grpo_profile_collect", "grpo_last_launch_count",
+            "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
+            "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
 
 
@@ -45,7 +46,15 @@ class ValidateSummary(C.Structure):
 
 class Tune(C.Structure):
     _fields_ = [("kernel", C.c_int32), ("cluster_size", C.c_int32),
-                ("ctas_per_sm", C.c_int32), ("stages", C.c_int32)]
+                ("ctas_per_sm", C.c_int32), ("stages", C.c_int32), ("lag", C.c_int32)]
+
+
+class Plan(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("kernel", "cluster_size", "ctas_per_sm", "stages",
+                                         "vec_per_thread", "grid", "max_clusters", "smem_bytes", "lag")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
 class GrpoError(RuntimeError):
@@ -80,6 +89,8 @@ def _load():
     lib.grpo_profile_enable.restype = st
     lib.grpo_profile_collect.argtypes = [P, P]
     lib.grpo_profile_collect.restype = st
+    lib.grpo_async_last_plan.argtypes = [P]
+    lib.grpo_async_last_plan.restype = st
     lib.grpo_last_launch_count.argtypes = []
     lib.grpo_last_launch_count.restype = i32
     lib.grpo_last_error.argtypes = []
@@ -127,6 +138,12 @@ def grpo_profile_collect():
     ms = C.c_double()
     _check(LIB.grpo_profile_collect(C.byref(n), C.byref(ms)))
     return int(n.value), float(ms.value)
+
+
+def grpo_async_last_plan() -> dict:
+    p = Plan()
+    _check(LIB.grpo_async_last_plan(C.byref(p)))
+    return p.as_dict()
 
 
 def grpo_last_launch_count() -> int:
@@ -191,7 +208,8 @@ def grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav
     """logits/dlogits: bf16 (or int16/uint16 bit patterns) [n_rows, ld] device tensors."""
     tune_p = None
     if tune is not None:
-        t = Tune(*[int(tune.get(k, 0)) for k in ("kernel", "cluster_size", "ctas_per_sm", "stages")])
+        t = Tune(*[int(tune.get(k, 0)) for k in ("kernel", "cluster_size", "ctas_per_sm", "stages",
+                                                  "lag")])
         tune_p = C.byref(t)
     for name, x in (("logits", logits), ("dlogits", dlogits)):
         if x is not None and x.element_size() != 2:

@@ -14,6 +14,7 @@ namespace {
 
 thread_local std::string g_last_error;
 thread_local int32_t g_last_launches = 0;
+thread_local grpo_plan_t g_last_plan = {};
 
 grpo_status_t fail(grpo_status_t st, const char *fmt, ...) {
     char buf[512];
@@ -113,6 +114,12 @@ grpo_status_t grpo_profile_collect(int32_t *n_launches, double *total_ms) {
 }
 
 int32_t grpo_last_launch_count(void) { return g_last_launches; }
+
+grpo_status_t grpo_async_last_plan(grpo_plan_t *out) {
+    if (!out) return fail(GRPO_ERR_INVALID_ARG, "last_plan: NULL output");
+    *out = g_last_plan;
+    return GRPO_OK;
+}
 
 const char *grpo_version(void) { return "grpo_async 0.1.0 (sm_100a)"; }
 
@@ -270,10 +277,10 @@ grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
     if (kernel == 2) {
-        e = grpo::launch_fused_rowwise(a, s, &launches);
+        e = grpo::launch_fused_rowwise(a, s, &launches, &g_last_plan);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");
     } else {
-        e = grpo::launch_fused_cluster(a, tune, s, &launches, why, sizeof why);
+        e = grpo::launch_fused_cluster(a, tune, s, &launches, why, sizeof why, &g_last_plan);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/fused_cluster", why);
     }
     if (traced && (e = prof_end(s, ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");

@@ -269,6 +269,27 @@ __device__ __forceinline__ void warp_lse2_allreduce(float &a, float &s) {
     }
 }
 
+// Warp-wide (all lanes get the identical result: max and + are commutative,
+// so both partners of every butterfly step compute the same bits).
+__device__ __forceinline__ float warp_max_all(float x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x = fmaxf(x, __shfl_xor_sync(0xFFFFFFFFu, x, off));
+    return x;
+}
+__device__ __forceinline__ float warp_sum_all(float x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, off);
+    return x;
+}
+// Combine log2-domain partials (a, s) of the 32 lanes: one max reduction,
+// one rescale per lane, one sum reduction.
+__device__ __forceinline__ void warp_lse2_combine(float &a, float &s) {
+    const float amax = warp_max_all(a);
+    s = (amax == -INFINITY) ? 0.0f : s * ex2(a - amax);
+    s = warp_sum_all(s);
+    a = amax;
+}
+
 // Per-row epilogue of eq:grpo_async / eq:ratio_async:
 // r = exp(logp - logp_w), term = min(r A, clip(r) A), clipped iff the clip
 // branch binds strictly, s = grad_scale * inv_norm * A * r * !clipped.
@@ -334,8 +355,9 @@ struct LossArgs {
 
 cudaError_t launch_rowinfo(const LossArgs &a, cudaStream_t s, int *launches);
 cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
-                                 int *launches, char *why, size_t why_len);
-cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launches);
+                                 int *launches, char *why, size_t why_len, grpo_plan_t *plan);
+cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launches,
+                                 grpo_plan_t *plan);
 cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches);
 cudaError_t launch_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
                             const int64_t *target_ids, const float *lse, const float *scale,

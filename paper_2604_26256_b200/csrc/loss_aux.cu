@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(256) rowwise_kernel(const RowwiseParams p) {
     }
 }
 
-cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launches) {
+cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launches,
+                                 grpo_plan_t *plan) {
     if (a.n_rows == 0) return cudaSuccess;
     RowwiseParams p;
     p.logits = a.logits;
@@ -175,6 +176,11 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launche
     p.logp_ws = a.logp_ws;
     p.flag_ws = a.flag_ws;
     int64_t blocks = a.n_rows < 148 * 8 ? a.n_rows : 148 * 8;
+    if (plan) {
+        *plan = grpo_plan_t{};
+        plan->kernel = 2;
+        plan->grid = (int32_t)blocks;
+    }
     rowwise_kernel<<<(unsigned)blocks, 256, 0, s>>>(p);
     *launches += 1;
     return cudaGetLastError();

@@ -42,6 +42,7 @@ struct FusedParams {
     int32_t n_vec_row;  // ceil(V / 8)
     int32_t slice_vec;  // vectors of 8 bf16 per CTA (last CTA may hold fewer)
     int32_t stages;
+    int32_t lag;        // B(k) runs `lag` iterations after A(k)
     uint32_t stage_bytes;
 };
 
@@ -59,17 +60,54 @@ __device__ __forceinline__ RowInfo load_rowinfo(const RowInfo *p) {
     return r;
 }
 
+constexpr int kMaxSlots = 6;  // exchange slots 2*lag + 2, lag <= 2
+
+__device__ __forceinline__ size_t round16(size_t x) { return (x + 15) / 16 * 16; }
+
+// Shared-memory carve-up (host and device agree through this one function).
+struct FusedSmem {
+    size_t bars, xch, red, meta, rowsc, total;
+};
+__host__ __device__ __forceinline__ FusedSmem fused_smem_layout(int S, uint32_t stage_bytes) {
+    FusedSmem L;
+    L.bars = (size_t)S * stage_bytes;
+    L.xch = L.bars + (((size_t)(S + kMaxSlots) * 8 + 15) / 16) * 16;
+    L.red = L.xch + (size_t)kMaxSlots * kMaxCluster * sizeof(XMsg);
+    L.meta = L.red + 2 * kWarps * sizeof(float2);
+    L.rowsc = L.meta + kMaxSlots * sizeof(RowInfo);
+    L.total = L.rowsc + kMaxSlots * sizeof(float4);
+    return L;
+}
+
+// Row k of this cluster is processed in three parts:
+//   A(k)  all warps: wait for the slice in stage k % S, reduce it to a
+//         log2-domain partial (a, s); warp 0 sends the CTA's partial and the
+//         target logit (if this CTA owns column y) to every CTA of the cluster;
+//   E(k)  warp 0, one iteration later: all C partials of row k are in; form
+//         lse, logp, r, clip, term and the token scale s_k, publish them in
+//         shared memory (and to global memory from cluster rank 0);
+//   B(k)  all warps, `lag` iterations after A(k): dlogits of the slice from
+//         the stage and the published scalars.
+// One __syncthreads per iteration orders everything: it publishes the
+// partials of A(it) to warp 0, the scalars of E(it - lag) to every warp, and
+// tells thread 0 that B(it - lag - 1) has released its stage (refilled with
+// row it - lag - 1 + S).  A peer runs at most `lag` rows ahead, so the
+// exchange needs 2*lag + 2 slots.
 template <int VPT>
 __global__ void __launch_bounds__(kThreads, 2)
     fused_cluster_kernel(const FusedParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int S = p.stages;
+    const int D = p.lag;
+    const int NX = 2 * D + 2;
+    const FusedSmem lay = fused_smem_layout(S, p.stage_bytes);
     uint8_t *stage_base = smem;
-    uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + (size_t)S * p.stage_bytes);
-    uint64_t *xbar = full_bar + S;                                     // [2]
-    XMsg *xch = reinterpret_cast<XMsg *>(                              // [2][kMaxCluster]
-        smem + (size_t)S * p.stage_bytes + (((size_t)(S + 2) * 8 + 15) / 16) * 16);
-    float2 *red = reinterpret_cast<float2 *>(xch + 2 * kMaxCluster);   // [kWarps]
+    uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + lay.bars);  // [S]
+    uint64_t *xbar = full_bar + S;                                        // [NX]
+    XMsg *xch = reinterpret_cast<XMsg *>(smem + lay.xch);                // [kMaxSlots][kMaxCluster]
+    float2 *red = reinterpret_cast<float2 *>(smem + lay.red);            // [2][kWarps]
+    RowInfo *meta = reinterpret_cast<RowInfo *>(smem + lay.meta);        // [kMaxSlots]
+    float4 *rowsc = reinterpret_cast<float4 *>(smem + lay.rowsc);        // [kMaxSlots]
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -83,172 +121,210 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int32_t my_vecs = max(0, min(p.slice_vec, p.n_vec_row - vec_begin));
     const uint32_t my_bytes = (uint32_t)my_vecs * 16u;
     const int32_t col_begin = vec_begin * 8;
+    const int32_t col_end = col_begin + my_vecs * 8;
     // the row's last vector holds V % 8 valid columns (if nonzero)
     const int32_t tail_valid = p.V - (p.n_vec_row - 1) * 8;
-    const int64_t my_rows = (g < p.n_rows) ? (p.n_rows - 1 - g) / n_cl + 1 : 0;
+    const int32_t tail_vi = (tail_valid < 8) ? (p.n_vec_row - 1 - vec_begin) : -1;
+    const int32_t my_rows = (g < p.n_rows) ? (int32_t)((p.n_rows - 1 - g) / n_cl + 1) : 0;
+    const uint32_t xbytes = C * (uint32_t)sizeof(XMsg);
+    const int64_t row_stride = n_cl * p.ld;            // elements between my consecutive rows
+    const uint16_t *src0 = p.logits + g * p.ld + col_begin;
     uint64_t pol = 0;
+    RowInfo ri_cur{}, ri_nxt{};   // thread 0: row info of rows it and it + 1
 
     if (tid == 0) {
         for (int i = 0; i < S; ++i) mbar_init(&full_bar[i], 1);
-        mbar_init(&xbar[0], 1);
-        mbar_init(&xbar[1], 1);
+        for (int i = 0; i < NX; ++i) mbar_init(&xbar[i], 1);
         fence_mbar_init_cluster();
-        mbar_arrive_expect_tx(&xbar[0], C * (uint32_t)sizeof(XMsg));  // arm row 0's exchange
+        for (int k = 0; k < D && k < my_rows; ++k)                // rows a peer may send at once
+            mbar_arrive_expect_tx(&xbar[k], xbytes);
         pol = policy_evict_first();
-        for (int64_t it = 0; it < S && it < my_rows; ++it) {          // fill the ring
-            mbar_arrive_expect_tx(&full_bar[it], my_bytes);
+        for (int k = 0; k < S && k < my_rows; ++k) {               // fill the ring
+            mbar_arrive_expect_tx(&full_bar[k], my_bytes);
             if (my_bytes)
-                bulk_g2s(stage_base + (size_t)it * p.stage_bytes,
-                         p.logits + (g + it * n_cl) * p.ld + col_begin, my_bytes, &full_bar[it],
-                         pol);
+                bulk_g2s(stage_base + (size_t)k * p.stage_bytes, src0 + k * row_stride, my_bytes,
+                         &full_bar[k], pol);
         }
+        if (my_rows > 0) ri_cur = load_rowinfo(p.rowinfo + g);
+        if (my_rows > 1) ri_nxt = load_rowinfo(p.rowinfo + g + n_cl);
     }
     cluster_sync_all();  // barriers of every CTA exist and are armed before any st.async
 
-    RowInfo ri_next = my_rows > 0 ? load_rowinfo(p.rowinfo + g) : RowInfo{};
-    for (int64_t it = 0; it < my_rows; ++it) {
-        const int64_t row = g + it * n_cl;
-        const int st = (int)(it % S);
-        const uint32_t ph = (uint32_t)((it / S) & 1);
-        const int xb = (int)(it & 1);
-        const RowInfo ri = ri_next;
-        if (it + 1 < my_rows) ri_next = load_rowinfo(p.rowinfo + row + n_cl);  // prefetch
-        mbar_wait(&full_bar[st], ph);
-
-        const uint32_t sbase = smem_u32(stage_base + (size_t)st * p.stage_bytes);
-        uint4 v[VPT];
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            const int vi = tid + j * kThreads;
-            if (vi < my_vecs) {
-                v[j] = lds128(sbase + (uint32_t)vi * 16u);
-                // mask columns >= V of the row's ragged last vector to -inf
-                if (vec_begin + vi == p.n_vec_row - 1 && tail_valid < 8)
-                    v[j] = mask_tail(v[j], tail_valid);
-            } else {
-                v[j] = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
-                                  kBf16NegInfPair);
-            }
-        }
-        // the CTA owning column y reads z_y from the stage
-        const int32_t y = ri.target;
-        const bool y_valid = (y >= 0) && (y < p.V);
-        const int32_t y_owner = y_valid ? (y >> 3) / p.slice_vec : -1;
-        float zy_local = 0.0f;
-        if (tid == 0 && y_owner == (int32_t)crank) {
-            const uint32_t a = sbase + (uint32_t)(y - col_begin) * 2u;
-            uint16_t hv;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hv) : "r"(a) : "memory");
-            zy_local = __uint_as_float(((uint32_t)hv) << 16);
-        }
-
-        // ---- thread-local max (packed bf16x2) then sum of exp
-        uint32_t mx2 = kBf16NegInfPair;
-#pragma unroll
-        for (int j = 0; j < VPT; ++j)
-            mx2 = bmax2(bmax2(mx2, bmax2(v[j].x, v[j].y)), bmax2(v[j].z, v[j].w));
-        float a = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
-        const float mL = (a == -INFINITY) ? 0.0f : a;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-        for (int j = 0; j < VPT; ++j) {
-            s0 += ex2(fmaf(bf_lo(v[j].x), kLog2e, -mL)) + ex2(fmaf(bf_hi(v[j].x), kLog2e, -mL));
-            s1 += ex2(fmaf(bf_lo(v[j].y), kLog2e, -mL)) + ex2(fmaf(bf_hi(v[j].y), kLog2e, -mL));
-            s2 += ex2(fmaf(bf_lo(v[j].z), kLog2e, -mL)) + ex2(fmaf(bf_hi(v[j].z), kLog2e, -mL));
-            s3 += ex2(fmaf(bf_lo(v[j].w), kLog2e, -mL)) + ex2(fmaf(bf_hi(v[j].w), kLog2e, -mL));
-        }
-        float s = (s0 + s1) + (s2 + s3);
-        warp_lse2_allreduce(a, s);
-        if (lane == 0) red[warp] = make_float2(a, s);
-        __syncthreads();  // every warp has its slice in registers: stage st is free
-
-        if (warp == 0) {
-            if (lane == 0 && it + S < my_rows) {  // refill stage st with row it + S
-                mbar_arrive_expect_tx(&full_bar[st], my_bytes);
-                if (my_bytes)
-                    bulk_g2s(stage_base + (size_t)st * p.stage_bytes,
-                             p.logits + (row + S * n_cl) * p.ld + col_begin, my_bytes,
-                             &full_bar[st], pol);
-            }
-            // combine the warps, arm the exchange for row it+1, send to every peer
-            float cm = -INFINITY, cs = 0.0f;
-            if (lane < kWarps) {
-                const float2 r2 = red[lane];
-                cm = r2.x;
-                cs = r2.y;
-            }
-            warp_lse2_allreduce(cm, cs);
-            const float zy = __shfl_sync(0xFFFFFFFFu, zy_local, 0);
-            if (lane == 0 && it + 1 < my_rows)
-                mbar_arrive_expect_tx(&xbar[xb ^ 1], C * (uint32_t)sizeof(XMsg));
-            __syncwarp();
-            if (lane < (int)C) {
-                const uint32_t laddr = smem_u32(&xch[xb * kMaxCluster + crank]);
-                const uint32_t lbar = smem_u32(&xbar[xb]);
-                st_async_v4(mapa_shared(laddr, lane), mapa_shared(lbar, lane), cm, cs, zy, 0.0f);
-            }
-        }
-
-        // ---- the row's lse from the C partials (identical in every warp and CTA)
-        mbar_wait_cluster(&xbar[xb], (uint32_t)((it >> 1) & 1));
-        float M = -INFINITY, Ssum = 0.0f, zsrc = 0.0f;
-        if (lane < (int)C) {
-            const XMsg msg = xch[xb * kMaxCluster + lane];
-            M = msg.m;
-            Ssum = msg.s;
-            zsrc = msg.zy;
-        }
-        warp_lse2_allreduce(M, Ssum);
-        const float zy = y_valid ? __shfl_sync(0xFFFFFFFFu, zsrc, max(y_owner, 0))
-                                 : __int_as_float(0x7FC00000);
-        const float l2s = log2f(Ssum);
-        const float lse2 = M + l2s;           // log2-domain logsumexp of the row
-        const float lse = lse2 * kLn2;
-        const double logp_d = row_logp(zy, M, l2s);
-        const float logp = (float)logp_d;
-        const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
-        if (crank == 0 && tid == 0) {
-            if (p.logp_out) p.logp_out[row] = logp;
-            if (p.lse_out) p.lse_out[row] = lse;
-            if (p.scale_out) p.scale_out[row] = o.s;
-            p.term_ws[row] = o.term;
-            p.logp_ws[row] = logp;
-            p.flag_ws[row] = o.flags;
-        }
-
-        // ---- backward: dlogits = s (softmax - onehot), one write per element
-        if (p.dlogits) {
-            uint16_t *drow = p.dlogits + row * p.ld;
-            const float off = lse2;
-            const float sc = o.s;
+    // ring positions, advanced incrementally (no integer division in the loop)
+    int a_st = 0, a_slot = 0, arm_slot = D % NX, e_slot = 0, b_st = 0, b_slot = 0;
+    uint32_t a_ph = 0, e_ph = 0;
+    int refill_st = 0;  // stage released by the previous B
+    for (int it = 0; it < my_rows + D; ++it) {
+        // ================================================================ A(it)
+        float zy_local = 0.0f, owner = 0.0f;
+        if (it < my_rows) {
+            mbar_wait(&full_bar[a_st], a_ph);
+            const uint32_t sbase = smem_u32(stage_base + (size_t)a_st * p.stage_bytes);
+            uint32_t mx2 = kBf16NegInfPair;
+            uint4 v[VPT];
 #pragma unroll
             for (int j = 0; j < VPT; ++j) {
                 const int vi = tid + j * kThreads;
-                if (vi >= my_vecs) continue;
-                uint4 d;
-                if (sc == 0.0f) {
-                    d = make_uint4(0u, 0u, 0u, 0u);
+                if (vi < my_vecs) {
+                    v[j] = lds128(sbase + (uint32_t)vi * 16u);
+                    // columns >= V of the row's ragged last vector count as -inf
+                    if (vi == tail_vi) v[j] = mask_tail(v[j], tail_valid);
                 } else {
-                    d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(v[j].x), kLog2e, -off)),
-                                      sc * ex2(fmaf(bf_hi(v[j].x), kLog2e, -off)));
-                    d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(v[j].y), kLog2e, -off)),
-                                      sc * ex2(fmaf(bf_hi(v[j].y), kLog2e, -off)));
-                    d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(v[j].z), kLog2e, -off)),
-                                      sc * ex2(fmaf(bf_hi(v[j].z), kLog2e, -off)));
-                    d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(v[j].w), kLog2e, -off)),
-                                      sc * ex2(fmaf(bf_hi(v[j].w), kLog2e, -off)));
+                    v[j] = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
+                                      kBf16NegInfPair);
                 }
-                const int32_t col = (vec_begin + vi) * 8;
-                if (vec_begin + vi == p.n_vec_row - 1 && tail_valid < 8)
-                    store_tail(drow + col, d, tail_valid);
-                else
-                    stg_stream(drow + col, d);
-                if (y_valid && (y >> 3) == vec_begin + vi) {
-                    // target entry: s (p_y - 1), from the unrounded probability
-                    const float py = ex2(fmaf(zy, kLog2e, -off));
-                    drow[y] = f2bf(sc * (py - 1.0f));
+                mx2 = bmax2(bmax2(mx2, bmax2(v[j].x, v[j].y)), bmax2(v[j].z, v[j].w));
+            }
+            float a = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
+            const float aL = (a == -INFINITY) ? 0.0f : a;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int j = 0; j < VPT; ++j) {
+                s0 += ex2(fmaf(bf_lo(v[j].x), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].x), kLog2e, -aL));
+                s1 += ex2(fmaf(bf_lo(v[j].y), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].y), kLog2e, -aL));
+                s2 += ex2(fmaf(bf_lo(v[j].z), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].z), kLog2e, -aL));
+                s3 += ex2(fmaf(bf_lo(v[j].w), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].w), kLog2e, -aL));
+            }
+            float s = (s0 + s1) + (s2 + s3);
+            warp_lse2_combine(a, s);
+            if (lane == 0) red[(it & 1) * kWarps + warp] = make_float2(a, s);
+            if (tid == 0) {
+                meta[a_slot] = ri_cur;
+                const int32_t y = ri_cur.target;
+                if (y >= col_begin && y < col_end && y < p.V) {
+                    uint16_t hv;
+                    asm volatile("ld.shared.u16 %0, [%1];"
+                                 : "=h"(hv)
+                                 : "r"(sbase + (uint32_t)(y - col_begin) * 2u)
+                                 : "memory");
+                    zy_local = __uint_as_float(((uint32_t)hv) << 16);
+                    owner = 1.0f;
                 }
             }
+        }
+        __syncthreads();  // red of A(it); rowsc of E(it - D); B(it - D - 1) done everywhere
+
+        if (warp == 0) {
+            if (it < my_rows) {
+                if (lane == 0) {
+                    // refill the stage B(it - D - 1) released with row it - D - 1 + S
+                    const int done = it - D - 1;
+                    if (done >= 0 && done + S < my_rows) {
+                        mbar_arrive_expect_tx(&full_bar[refill_st], my_bytes);
+                        if (my_bytes)
+                            bulk_g2s(stage_base + (size_t)refill_st * p.stage_bytes,
+                                     src0 + (int64_t)(done + S) * row_stride, my_bytes,
+                                     &full_bar[refill_st], pol);
+                    }
+                    // arm the exchange of row it + D before any peer can send it
+                    if (it + D < my_rows) mbar_arrive_expect_tx(&xbar[arm_slot], xbytes);
+                }
+                float cm = -INFINITY, cs = 0.0f;
+                if (lane < kWarps) {
+                    const float2 r2 = red[(it & 1) * kWarps + lane];
+                    cm = r2.x;
+                    cs = r2.y;
+                }
+                warp_lse2_combine(cm, cs);
+                const float zy = __shfl_sync(0xFFFFFFFFu, zy_local, 0);
+                const float own = __shfl_sync(0xFFFFFFFFu, owner, 0);
+                __syncwarp();
+                if (lane < (int)C) {
+                    const uint32_t laddr = smem_u32(&xch[a_slot * kMaxCluster + crank]);
+                    const uint32_t lbar = smem_u32(&xbar[a_slot]);
+                    st_async_v4(mapa_shared(laddr, lane), mapa_shared(lbar, lane), cm, cs, zy, own);
+                }
+                if (lane == 0) {
+                    ri_cur = ri_nxt;
+                    if (it + 2 < my_rows)
+                        ri_nxt = load_rowinfo(p.rowinfo + g + (int64_t)(it + 2) * n_cl);
+                }
+            }
+            // ============================================================ E(it - D + 1)
+            const int ke = it - D + 1;
+            if (ke >= 0 && ke < my_rows) {
+                mbar_wait(&xbar[e_slot], e_ph);
+                float M = -INFINITY, Ssum = 0.0f, zsrc = 0.0f;
+                bool own = false;
+                if (lane < (int)C) {
+                    const XMsg msg = xch[e_slot * kMaxCluster + lane];
+                    M = msg.m;
+                    Ssum = msg.s;
+                    zsrc = msg.zy;
+                    own = msg.pad != 0.0f;
+                }
+                warp_lse2_combine(M, Ssum);
+                const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
+                const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
+                if (lane == 0) {
+                    const RowInfo ri = meta[e_slot];
+                    const bool y_valid = own_mask != 0u;   // column y lies in [0, V)
+                    const float zy = y_valid ? zsh : __int_as_float(0x7FC00000);
+                    const float l2s = log2f(Ssum);
+                    const float lse2 = M + l2s;           // log2-domain logsumexp of the row
+                    const double logp_d = row_logp(zy, M, l2s);
+                    const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
+                    rowsc[e_slot] = make_float4(lse2, o.s, zy,
+                                                __int_as_float(y_valid ? ri.target : -1));
+                    if (crank == 0) {
+                        const int64_t row = g + (int64_t)ke * n_cl;
+                        const float logp = (float)logp_d;
+                        if (p.logp_out) p.logp_out[row] = logp;
+                        if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
+                        if (p.scale_out) p.scale_out[row] = o.s;
+                        p.term_ws[row] = o.term;
+                        p.logp_ws[row] = logp;
+                        p.flag_ws[row] = o.flags;
+                    }
+                }
+                if (++e_slot == NX) { e_slot = 0; e_ph ^= 1u; }
+            }
+        }
+        if (it < my_rows) {
+            if (++a_st == S) { a_st = 0; a_ph ^= 1u; }
+            if (++a_slot == NX) a_slot = 0;
+            if (++arm_slot == NX) arm_slot = 0;
+        }
+        // ================================================================ B(it - D)
+        if (it >= D) {
+            const int64_t row = g + (int64_t)(it - D) * n_cl;
+            const float4 sc4 = rowsc[b_slot];
+            const float lse2 = sc4.x, sc = sc4.y, zy = sc4.z;
+            const int32_t y = __float_as_int(sc4.w);
+            if (p.dlogits) {
+                uint16_t *drow = p.dlogits + row * p.ld + col_begin;
+                const uint32_t sbase = smem_u32(stage_base + (size_t)b_st * p.stage_bytes);
+                const int32_t yv = (y >= col_begin && y < col_end) ? ((y - col_begin) >> 3) : -1;
+#pragma unroll
+                for (int j = 0; j < VPT; ++j) {
+                    const int vi = tid + j * kThreads;
+                    if (vi >= my_vecs) continue;
+                    uint4 d = make_uint4(0u, 0u, 0u, 0u);
+                    if (sc != 0.0f) {
+                        const uint4 x = lds128(sbase + (uint32_t)vi * 16u);
+                        d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.x), kLog2e, -lse2)),
+                                          sc * ex2(fmaf(bf_hi(x.x), kLog2e, -lse2)));
+                        d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.y), kLog2e, -lse2)),
+                                          sc * ex2(fmaf(bf_hi(x.y), kLog2e, -lse2)));
+                        d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.z), kLog2e, -lse2)),
+                                          sc * ex2(fmaf(bf_hi(x.z), kLog2e, -lse2)));
+                        d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.w), kLog2e, -lse2)),
+                                          sc * ex2(fmaf(bf_hi(x.w), kLog2e, -lse2)));
+                    }
+                    if (vi == tail_vi)
+                        store_tail(drow + vi * 8, d, tail_valid);
+                    else
+                        stg_stream(drow + vi * 8, d);
+                    if (vi == yv) {
+                        // target entry: s (p_y - 1), from the unrounded probability
+                        const float py = ex2(fmaf(zy, kLog2e, -lse2));
+                        drow[y - col_begin] = f2bf(sc * (py - 1.0f));
+                    }
+                }
+            }
+            refill_st = b_st;
+            if (++b_st == S) b_st = 0;
+            if (++b_slot == NX) b_slot = 0;
         }
     }
     __syncthreads();
@@ -267,7 +343,8 @@ int pick_cluster(int32_t n_vec_row) {
 
 template <int VPT>
 cudaError_t launch_vpt(const FusedParams &fp, int C, int ctas_per_sm, size_t smem,
-                       cudaStream_t s, int64_t n_rows, char *why, size_t why_len) {
+                       cudaStream_t s, int64_t n_rows, char *why, size_t why_len,
+                       grpo_plan_t *plan) {
     auto kern = fused_cluster_kernel<VPT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -301,13 +378,24 @@ cudaError_t launch_vpt(const FusedParams &fp, int C, int ctas_per_sm, size_t sme
     int64_t n_cl = (int64_t)max_clusters;
     if (n_cl > n_rows) n_cl = n_rows;
     cfg.gridDim = dim3((unsigned)(n_cl * C));
+    if (plan) {
+        plan->kernel = 1;
+        plan->cluster_size = C;
+        plan->ctas_per_sm = ctas_per_sm;
+        plan->stages = fp.stages;
+        plan->lag = fp.lag;
+        plan->vec_per_thread = VPT;
+        plan->grid = (int32_t)(n_cl * C);
+        plan->max_clusters = max_clusters;
+        plan->smem_bytes = (int32_t)smem;
+    }
     return cudaLaunchKernelEx(&cfg, kern, fp);
 }
 
 }  // namespace
 
 cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
-                                 int *launches, char *why, size_t why_len) {
+                                 int *launches, char *why, size_t why_len, grpo_plan_t *plan) {
     if (a.n_rows == 0) return cudaSuccess;
     FusedParams fp;
     fp.logits = a.logits;
@@ -331,18 +419,29 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
     fp.slice_vec = (fp.n_vec_row + C - 1) / C;
     const int vpt_needed = (fp.slice_vec + kThreads - 1) / kThreads;
     fp.stage_bytes = (uint32_t)(((size_t)fp.slice_vec * 16 + 127) / 128 * 128);
-    const size_t fixed = 8 * 8 + 2 * 8 + 2 * kMaxCluster * sizeof(XMsg) + kWarps * 8 + 256;
+    const bool auto_lag = !(tune && tune->lag > 0);
+    int lag = auto_lag ? 2 : tune->lag;
+    if (lag > 2) {
+        if (why) snprintf(why, why_len, "lag %d > 2", lag);
+        return cudaErrorInvalidValue;
+    }
     const size_t per_sm = 227 * 1024;
     int stages = (tune && tune->stages > 0) ? tune->stages : 0;
     if (stages == 0) {
+        const size_t fixed = fused_smem_layout(0, fp.stage_bytes).total + 8 * 8;
         const size_t budget = per_sm / ctas_per_sm - 1024 - fixed;
         stages = (int)(budget / fp.stage_bytes);
-        if (stages > 4) stages = 4;
-        if (stages < 1) stages = 1;
+        if (stages > 8) stages = 8;
+    }
+    if (auto_lag && stages < lag + 2) lag = stages - 2 >= 1 ? stages - 2 : 1;
+    fp.lag = lag;
+    if (stages < lag + 2) {
+        if (why) snprintf(why, why_len, "%d stages < lag + 2 = %d (slice %u B)", stages, lag + 2,
+                          fp.stage_bytes);
+        return cudaErrorInvalidConfiguration;
     }
     fp.stages = stages;
-    const size_t smem = (size_t)stages * fp.stage_bytes + (((size_t)(stages + 2) * 8 + 15) / 16) * 16 +
-                        2 * kMaxCluster * sizeof(XMsg) + kWarps * sizeof(float2);
+    const size_t smem = fused_smem_layout(stages, fp.stage_bytes).total;
     if (C < 1 || C > kMaxCluster || (C & (C - 1)) != 0) {
         if (why) snprintf(why, why_len, "cluster_size %d not a power of two <= 16", C);
         return cudaErrorInvalidValue;
@@ -352,13 +451,13 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
         return cudaErrorInvalidConfiguration;
     }
     cudaError_t e;
-    if (vpt_needed <= 2) e = launch_vpt<2>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len);
-    else if (vpt_needed <= 4) e = launch_vpt<4>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len);
-    else if (vpt_needed <= 6) e = launch_vpt<6>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len);
-    else if (vpt_needed <= 8) e = launch_vpt<8>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len);
-    else if (vpt_needed <= 10) e = launch_vpt<10>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len);
-    else if (vpt_needed <= 12) e = launch_vpt<12>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len);
-    else if (vpt_needed <= 16) e = launch_vpt<16>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len);
+    if (vpt_needed <= 2) e = launch_vpt<2>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len, plan);
+    else if (vpt_needed <= 4) e = launch_vpt<4>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len, plan);
+    else if (vpt_needed <= 6) e = launch_vpt<6>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len, plan);
+    else if (vpt_needed <= 8) e = launch_vpt<8>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len, plan);
+    else if (vpt_needed <= 10) e = launch_vpt<10>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len, plan);
+    else if (vpt_needed <= 12) e = launch_vpt<12>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len, plan);
+    else if (vpt_needed <= 16) e = launch_vpt<16>(fp, C, ctas_per_sm, smem, s, a.n_rows, why, why_len, plan);
     else {
         if (why) snprintf(why, why_len, "slice of %d vectors too large for cluster %d", fp.slice_vec, C);
         return cudaErrorInvalidConfiguration;

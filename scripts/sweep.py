@@ -1,0 +1,55 @@
+"""Time the fused loss kernel over one resident chunk for several launch plans."""
+import argparse, json, sys, os
+import numpy as np
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_26256_b200 as G
+import synth.gpu as SG
+from synth.gen import make_batch, CONFIGS
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="prod")
+ap.add_argument("--rows", type=int, default=65536)
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--plans", default="")
+ap.add_argument("--fwd-only", action="store_true")
+args = ap.parse_args()
+dev = torch.device("cuda:0")
+b = make_batch(args.config, 0, period=args.rows)
+R = args.rows
+V, ld = b.V, b.ld
+lg = torch.empty((R, ld), dtype=torch.int16, device=dev)
+dl = torch.empty_like(lg)
+SG.fill_logits(lg, b.logits, 0, R, V)
+db = G.DeviceBatch.from_host(b, dev)
+loss = G.GrpoAsyncLoss()
+adv, inv = loss.advantage(db)
+ts = torch.zeros(b.N, dtype=torch.float64, device=dev)
+st = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
+plans = [json.loads(p) for p in args.plans.split(";")] if args.plans else [
+    {"kernel": 1}, {"kernel": 2},
+    {"kernel": 1, "cluster_size": 8}, {"kernel": 1, "cluster_size": 16, "ctas_per_sm": 1},
+    {"kernel": 1, "cluster_size": 8, "ctas_per_sm": 1}, {"kernel": 1, "cluster_size": 4, "ctas_per_sm": 1},
+    {"kernel": 1, "cluster_size": 16, "stages": 2}, {"kernel": 1, "cluster_size": 16, "ctas_per_sm": 3},
+]
+bytes_row = 4 * V + 25 if not args.fwd_only else 2 * V + 25
+for plan in plans:
+    loss.tune = plan
+    try:
+        times = []
+        for r in range(args.reps + 1 if args.reps > 0 else 1):
+            G.grpo_profile_enable(True); G.grpo_profile_collect()
+            loss.loss_chunk(lg, 0, R, db.target_ids[:R], db.logp_behav[:R], db.cu_seqlens, adv, inv, ts, st,
+                            dlogits=None if args.fwd_only else dl, V=V)
+            torch.cuda.synchronize()
+            n, ms = G.grpo_profile_collect()
+            if r > 0 or args.reps == 0:
+                times.append(ms)
+        pl = G.grpo_async_last_plan()
+        ms = float(np.median(times))
+        print(json.dumps({"tune": plan, "plan": pl, "ms": round(ms, 3),
+                          "GBps": round(bytes_row * R / ms / 1e6, 1),
+                          "frac": round(bytes_row * R / ms / 1e6 / 6546.6, 3)}), flush=True)
+    except Exception as e:
+        print(json.dumps({"tune": plan, "error": str(e)}), flush=True)
+G.grpo_profile_enable(False)
