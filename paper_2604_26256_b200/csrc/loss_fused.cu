@@ -7,27 +7,40 @@
 //   PAPER.md P:9-34, P:151    term = min(r A, clip_eps(r) A), r = exp(logp - logp_w)
 //   DESIGN.md Z19             dlogits = d(-J)/dz = s_t (softmax - onehot)
 //
-// Design: a row of V bf16 logits (297 KiB at
+// Design.  A row of V bf16 logits (297 KiB at
 // V = 152064) does not fit one SM, so a thread-block cluster of C CTAs owns a
-// row: CTA c holds columns [c*slice, (c+1)*slice).  Thread 0 streams each
-// CTA's slice of the next rows into a ring of S shared-memory stages with 1-D
-// bulk TMA (cp.async.bulk + mbarrier transaction counts).  All warps copy the
-// slice into registers, reduce (max, sum exp) over it, and warp 0 exchanges
-// the 16-byte partial (m_c, s_c, z_y) with every CTA of the cluster through
-// DSMEM (st.async completing on the peer's mbarrier).  Every CTA then holds
-// the row's lse and writes its slice of dlogits straight from registers with
-// 128-bit streaming stores.  HBM sees one read of the logits and one write
-// of dlogits: 4V bytes per row.  Two CTAs per SM overlap one CTA's exchange
-// latency with the other's arithmetic; the TMA ring keeps S rows in flight.
+// row: CTA c holds columns [c*slice, (c+1)*slice) of it in a ring of S
+// shared-memory stages filled by 1-D bulk TMA (cp.async.bulk, mbarrier
+// transaction counts).  HBM sees one read of the logits and one write of
+// dlogits: 4V bytes per row.
+//
+// Warp specialisation, no CTA-wide barrier in the loop:
+//   compute warps (kComp):  A(k): reduce the slice of row k (stage k % S) to
+//       a log2-domain partial per warp; B(k - lag): once the row scalars of
+//       row k - lag are published, write its dlogits from the stage, then
+//       release the stage;
+//   control warp (1):  per row r: read z_y if this CTA owns the target
+//       column, combine the compute warps' partials, send the CTA partial
+//       (16 B) to every CTA of the cluster over DSMEM (st.async completing on
+//       the peer's mbarrier); E(r - lag + 1): once all C partials of that row
+//       are in, form lse, logp, r, clip, term and the token scale, publish
+//       them to the compute warps (and to global memory from cluster rank 0);
+//       refill the stage released by B(r - lag - 1) with row r - lag - 1 + S.
+// Hand-offs are mbarriers: full (TMA -> all), part (compute -> control),
+// scal (control -> compute), free (compute -> control), xbar (peers -> control).
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace grpo {
 
-constexpr int kWarps = 8;
+constexpr int kComp = 7;                    // compute warps
+constexpr int kWarps = kComp + 1;           // + the control warp
 constexpr int kThreads = kWarps * 32;
+constexpr int kCompThreads = kComp * 32;
 constexpr int kMaxCluster = 16;
+constexpr int kMaxSlots = 6;                // ring of per-row hand-off slots (>= 2*lag + 2)
 
 struct FusedParams {
     const uint16_t *logits;
@@ -42,12 +55,13 @@ struct FusedParams {
     int32_t n_vec_row;  // ceil(V / 8)
     int32_t slice_vec;  // vectors of 8 bf16 per CTA (last CTA may hold fewer)
     int32_t stages;
-    int32_t lag;        // B(k) runs `lag` iterations after A(k)
+    int32_t lag;        // B(k) runs `lag` rows after A(k)
+    uint32_t piece;     // bytes per bulk-copy request (a slice is split into pieces)
     uint32_t stage_bytes;
 };
 
 struct __align__(16) XMsg {
-    float m, s, zy, pad;
+    float m, s, zy, owner;
 };
 
 __device__ __forceinline__ RowInfo load_rowinfo(const RowInfo *p) {
@@ -60,39 +74,29 @@ __device__ __forceinline__ RowInfo load_rowinfo(const RowInfo *p) {
     return r;
 }
 
-constexpr int kMaxSlots = 6;  // exchange slots 2*lag + 2, lag <= 2
-
-__device__ __forceinline__ size_t round16(size_t x) { return (x + 15) / 16 * 16; }
-
 // Shared-memory carve-up (host and device agree through this one function).
 struct FusedSmem {
     size_t bars, xch, red, meta, rowsc, total;
 };
 __host__ __device__ __forceinline__ FusedSmem fused_smem_layout(int S, uint32_t stage_bytes) {
     FusedSmem L;
-    L.bars = (size_t)S * stage_bytes;
-    L.xch = L.bars + (((size_t)(S + kMaxSlots) * 8 + 15) / 16) * 16;
+    L.bars = (size_t)S * stage_bytes;  // full[S], free[S], part[6], scal[6], xbar[6]
+    L.xch = L.bars + (((size_t)(2 * S + 3 * kMaxSlots) * 8 + 15) / 16) * 16;
     L.red = L.xch + (size_t)kMaxSlots * kMaxCluster * sizeof(XMsg);
-    L.meta = L.red + 2 * kWarps * sizeof(float2);
+    L.meta = L.red + (size_t)kMaxSlots * kComp * sizeof(float2);
     L.rowsc = L.meta + kMaxSlots * sizeof(RowInfo);
     L.total = L.rowsc + kMaxSlots * sizeof(float4);
     return L;
 }
 
-// Row k of this cluster is processed in three parts:
-//   A(k)  all warps: wait for the slice in stage k % S, reduce it to a
-//         log2-domain partial (a, s); warp 0 sends the CTA's partial and the
-//         target logit (if this CTA owns column y) to every CTA of the cluster;
-//   E(k)  warp 0, one iteration later: all C partials of row k are in; form
-//         lse, logp, r, clip, term and the token scale s_k, publish them in
-//         shared memory (and to global memory from cluster rank 0);
-//   B(k)  all warps, `lag` iterations after A(k): dlogits of the slice from
-//         the stage and the published scalars.
-// One __syncthreads per iteration orders everything: it publishes the
-// partials of A(it) to warp 0, the scalars of E(it - lag) to every warp, and
-// tells thread 0 that B(it - lag - 1) has released its stage (refilled with
-// row it - lag - 1 + S).  A peer runs at most `lag` rows ahead, so the
-// exchange needs 2*lag + 2 slots.
+// One slice = bulk copies of at most `piece` bytes, all counted on one mbarrier.
+__device__ __forceinline__ void load_slice(void *dst, const void *src, uint32_t bytes,
+                                           uint32_t piece, uint64_t *bar, uint64_t pol) {
+    for (uint32_t o = 0; o < bytes; o += piece)
+        bulk_g2s(static_cast<uint8_t *>(dst) + o, static_cast<const uint8_t *>(src) + o,
+                 min(piece, bytes - o), bar, pol);
+}
+
 template <int VPT>
 __global__ void __launch_bounds__(kThreads, 2)
     fused_cluster_kernel(const FusedParams p) {
@@ -103,9 +107,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     const FusedSmem lay = fused_smem_layout(S, p.stage_bytes);
     uint8_t *stage_base = smem;
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + lay.bars);  // [S]
-    uint64_t *xbar = full_bar + S;                                        // [NX]
+    uint64_t *free_bar = full_bar + S;                                    // [S]
+    uint64_t *part_bar = free_bar + S;                                    // [NX]
+    uint64_t *scal_bar = part_bar + kMaxSlots;                            // [NX]
+    uint64_t *xbar = scal_bar + kMaxSlots;                                // [NX]
     XMsg *xch = reinterpret_cast<XMsg *>(smem + lay.xch);                // [kMaxSlots][kMaxCluster]
-    float2 *red = reinterpret_cast<float2 *>(smem + lay.red);            // [2][kWarps]
+    float2 *red = reinterpret_cast<float2 *>(smem + lay.red);            // [kMaxSlots][kComp]
     RowInfo *meta = reinterpret_cast<RowInfo *>(smem + lay.meta);        // [kMaxSlots]
     float4 *rowsc = reinterpret_cast<float4 *>(smem + lay.rowsc);        // [kMaxSlots]
 
@@ -129,119 +136,84 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t xbytes = C * (uint32_t)sizeof(XMsg);
     const int64_t row_stride = n_cl * p.ld;            // elements between my consecutive rows
     const uint16_t *src0 = p.logits + g * p.ld + col_begin;
-    uint64_t pol = 0;
-    RowInfo ri_cur{}, ri_nxt{};   // thread 0: row info of rows it and it + 1
+    const bool control = (warp == kComp);
 
-    if (tid == 0) {
-        for (int i = 0; i < S; ++i) mbar_init(&full_bar[i], 1);
-        for (int i = 0; i < NX; ++i) mbar_init(&xbar[i], 1);
+    if (control && lane == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&full_bar[i], 1);
+            mbar_init(&free_bar[i], kComp);
+        }
+        for (int i = 0; i < NX; ++i) {
+            mbar_init(&part_bar[i], kComp);
+            mbar_init(&scal_bar[i], 1);
+            mbar_init(&xbar[i], 1);
+        }
         fence_mbar_init_cluster();
         for (int k = 0; k < D && k < my_rows; ++k)                // rows a peer may send at once
             mbar_arrive_expect_tx(&xbar[k], xbytes);
-        pol = policy_evict_first();
+        const uint64_t pol = policy_evict_first();
         for (int k = 0; k < S && k < my_rows; ++k) {               // fill the ring
             mbar_arrive_expect_tx(&full_bar[k], my_bytes);
             if (my_bytes)
-                bulk_g2s(stage_base + (size_t)k * p.stage_bytes, src0 + k * row_stride, my_bytes,
-                         &full_bar[k], pol);
+                load_slice(stage_base + (size_t)k * p.stage_bytes, src0 + k * row_stride, my_bytes,
+                           p.piece, &full_bar[k], pol);
         }
-        if (my_rows > 0) ri_cur = load_rowinfo(p.rowinfo + g);
-        if (my_rows > 1) ri_nxt = load_rowinfo(p.rowinfo + g + n_cl);
     }
     cluster_sync_all();  // barriers of every CTA exist and are armed before any st.async
 
-    // ring positions, advanced incrementally (no integer division in the loop)
-    int a_st = 0, a_slot = 0, arm_slot = D % NX, e_slot = 0, b_st = 0, b_slot = 0;
-    uint32_t a_ph = 0, e_ph = 0;
-    int refill_st = 0;  // stage released by the previous B
-    for (int it = 0; it < my_rows + D; ++it) {
-        // ================================================================ A(it)
-        float zy_local = 0.0f, owner = 0.0f;
-        if (it < my_rows) {
-            mbar_wait(&full_bar[a_st], a_ph);
-            const uint32_t sbase = smem_u32(stage_base + (size_t)a_st * p.stage_bytes);
-            uint32_t mx2 = kBf16NegInfPair;
-            uint4 v[VPT];
-#pragma unroll
-            for (int j = 0; j < VPT; ++j) {
-                const int vi = tid + j * kThreads;
-                if (vi < my_vecs) {
-                    v[j] = lds128(sbase + (uint32_t)vi * 16u);
-                    // columns >= V of the row's ragged last vector count as -inf
-                    if (vi == tail_vi) v[j] = mask_tail(v[j], tail_valid);
-                } else {
-                    v[j] = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
-                                      kBf16NegInfPair);
-                }
-                mx2 = bmax2(bmax2(mx2, bmax2(v[j].x, v[j].y)), bmax2(v[j].z, v[j].w));
-            }
-            float a = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
-            const float aL = (a == -INFINITY) ? 0.0f : a;
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-            for (int j = 0; j < VPT; ++j) {
-                s0 += ex2(fmaf(bf_lo(v[j].x), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].x), kLog2e, -aL));
-                s1 += ex2(fmaf(bf_lo(v[j].y), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].y), kLog2e, -aL));
-                s2 += ex2(fmaf(bf_lo(v[j].z), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].z), kLog2e, -aL));
-                s3 += ex2(fmaf(bf_lo(v[j].w), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].w), kLog2e, -aL));
-            }
-            float s = (s0 + s1) + (s2 + s3);
-            warp_lse2_combine(a, s);
-            if (lane == 0) red[(it & 1) * kWarps + warp] = make_float2(a, s);
-            if (tid == 0) {
-                meta[a_slot] = ri_cur;
-                const int32_t y = ri_cur.target;
-                if (y >= col_begin && y < col_end && y < p.V) {
-                    uint16_t hv;
-                    asm volatile("ld.shared.u16 %0, [%1];"
-                                 : "=h"(hv)
-                                 : "r"(sbase + (uint32_t)(y - col_begin) * 2u)
-                                 : "memory");
-                    zy_local = __uint_as_float(((uint32_t)hv) << 16);
-                    owner = 1.0f;
-                }
-            }
-        }
-        __syncthreads();  // red of A(it); rowsc of E(it - D); B(it - D - 1) done everywhere
-
-        if (warp == 0) {
-            if (it < my_rows) {
+    if (control) {
+        // ================================================================ control warp
+        const uint64_t pol = policy_evict_first();
+        int c_st = 0, x_slot = 0, arm_slot = D % NX, e_slot = 0, f_st = 0;
+        uint32_t c_ph = 0, x_ph = 0, e_ph = 0, f_ph = 0;
+        RowInfo ri0{}, ri1{};                           // lane 0: rows r and r + 1
+        if (lane == 0 && my_rows > 0) ri0 = load_rowinfo(p.rowinfo + g);
+        if (lane == 0 && my_rows > 1) ri1 = load_rowinfo(p.rowinfo + g + n_cl);
+        for (int r = 0; r < my_rows + D; ++r) {
+            if (r < my_rows) {
+                // (a) the row's slice has landed: this CTA reads z_y if it owns column y
+                mbar_wait(&full_bar[c_st], c_ph);
+                float zy = 0.0f, own = 0.0f;
                 if (lane == 0) {
-                    // refill the stage B(it - D - 1) released with row it - D - 1 + S
-                    const int done = it - D - 1;
-                    if (done >= 0 && done + S < my_rows) {
-                        mbar_arrive_expect_tx(&full_bar[refill_st], my_bytes);
-                        if (my_bytes)
-                            bulk_g2s(stage_base + (size_t)refill_st * p.stage_bytes,
-                                     src0 + (int64_t)(done + S) * row_stride, my_bytes,
-                                     &full_bar[refill_st], pol);
+                    meta[x_slot] = ri0;
+                    const int32_t y = ri0.target;
+                    if (y >= col_begin && y < col_end && y < p.V) {
+                        uint16_t hv;
+                        asm volatile("ld.shared.u16 %0, [%1];"
+                                     : "=h"(hv)
+                                     : "r"(smem_u32(stage_base + (size_t)c_st * p.stage_bytes) +
+                                           (uint32_t)(y - col_begin) * 2u)
+                                     : "memory");
+                        zy = __uint_as_float(((uint32_t)hv) << 16);
+                        own = 1.0f;
                     }
-                    // arm the exchange of row it + D before any peer can send it
-                    if (it + D < my_rows) mbar_arrive_expect_tx(&xbar[arm_slot], xbytes);
+                    ri0 = ri1;
+                    if (r + 2 < my_rows) ri1 = load_rowinfo(p.rowinfo + g + (int64_t)(r + 2) * n_cl);
+                    // arm the exchange of row r + D before any peer can send it
+                    if (r + D < my_rows) mbar_arrive_expect_tx(&xbar[arm_slot], xbytes);
                 }
+                // (b) combine the compute warps' partials, send the CTA partial to every peer
+                mbar_wait(&part_bar[x_slot], x_ph);
                 float cm = -INFINITY, cs = 0.0f;
-                if (lane < kWarps) {
-                    const float2 r2 = red[(it & 1) * kWarps + lane];
+                if (lane < kComp) {
+                    const float2 r2 = red[x_slot * kComp + lane];
                     cm = r2.x;
                     cs = r2.y;
                 }
                 warp_lse2_combine(cm, cs);
-                const float zy = __shfl_sync(0xFFFFFFFFu, zy_local, 0);
-                const float own = __shfl_sync(0xFFFFFFFFu, owner, 0);
-                __syncwarp();
+                zy = __shfl_sync(0xFFFFFFFFu, zy, 0);
+                own = __shfl_sync(0xFFFFFFFFu, own, 0);
                 if (lane < (int)C) {
-                    const uint32_t laddr = smem_u32(&xch[a_slot * kMaxCluster + crank]);
-                    const uint32_t lbar = smem_u32(&xbar[a_slot]);
+                    const uint32_t laddr = smem_u32(&xch[x_slot * kMaxCluster + crank]);
+                    const uint32_t lbar = smem_u32(&xbar[x_slot]);
                     st_async_v4(mapa_shared(laddr, lane), mapa_shared(lbar, lane), cm, cs, zy, own);
                 }
-                if (lane == 0) {
-                    ri_cur = ri_nxt;
-                    if (it + 2 < my_rows)
-                        ri_nxt = load_rowinfo(p.rowinfo + g + (int64_t)(it + 2) * n_cl);
-                }
+                if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
+                if (++x_slot == NX) { x_slot = 0; x_ph ^= 1u; }
+                if (++arm_slot == NX) arm_slot = 0;
             }
-            // ============================================================ E(it - D + 1)
-            const int ke = it - D + 1;
+            // (c) E(r - D + 1): the row scalars, once every peer's partial is in
+            const int ke = r - D + 1;
             if (ke >= 0 && ke < my_rows) {
                 mbar_wait(&xbar[e_slot], e_ph);
                 float M = -INFINITY, Ssum = 0.0f, zsrc = 0.0f;
@@ -251,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     M = msg.m;
                     Ssum = msg.s;
                     zsrc = msg.zy;
-                    own = msg.pad != 0.0f;
+                    own = msg.owner != 0.0f;
                 }
                 warp_lse2_combine(M, Ssum);
                 const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
@@ -259,13 +231,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (lane == 0) {
                     const RowInfo ri = meta[e_slot];
                     const bool y_valid = own_mask != 0u;   // column y lies in [0, V)
-                    const float zy = y_valid ? zsh : __int_as_float(0x7FC00000);
+                    const float zyv = y_valid ? zsh : __int_as_float(0x7FC00000);
                     const float l2s = log2f(Ssum);
                     const float lse2 = M + l2s;           // log2-domain logsumexp of the row
-                    const double logp_d = row_logp(zy, M, l2s);
+                    const double logp_d = row_logp(zyv, M, l2s);
                     const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
-                    rowsc[e_slot] = make_float4(lse2, o.s, zy,
+                    rowsc[e_slot] = make_float4(lse2, o.s, zyv,
                                                 __int_as_float(y_valid ? ri.target : -1));
+                    mbar_arrive(&scal_bar[e_slot]);
                     if (crank == 0) {
                         const int64_t row = g + (int64_t)ke * n_cl;
                         const float logp = (float)logp_d;
@@ -277,54 +250,112 @@ __global__ void __launch_bounds__(kThreads, 2)
                         p.flag_ws[row] = o.flags;
                     }
                 }
+                __syncwarp();
                 if (++e_slot == NX) { e_slot = 0; e_ph ^= 1u; }
             }
+            // (d) refill the stage released by B(r - D - 1) with row r - D - 1 + S
+            const int kd = r - D - 1;
+            if (kd >= 0) {
+                if (kd + S < my_rows) {
+                    mbar_wait(&free_bar[f_st], f_ph);
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&full_bar[f_st], my_bytes);
+                        if (my_bytes)
+                            load_slice(stage_base + (size_t)f_st * p.stage_bytes,
+                                       src0 + (int64_t)(kd + S) * row_stride, my_bytes, p.piece,
+                                       &full_bar[f_st], pol);
+                    }
+                    __syncwarp();
+                }
+                if (++f_st == S) { f_st = 0; f_ph ^= 1u; }
+            }
         }
-        if (it < my_rows) {
-            if (++a_st == S) { a_st = 0; a_ph ^= 1u; }
-            if (++a_slot == NX) a_slot = 0;
-            if (++arm_slot == NX) arm_slot = 0;
-        }
-        // ================================================================ B(it - D)
-        if (it >= D) {
-            const int64_t row = g + (int64_t)(it - D) * n_cl;
-            const float4 sc4 = rowsc[b_slot];
-            const float lse2 = sc4.x, sc = sc4.y, zy = sc4.z;
-            const int32_t y = __float_as_int(sc4.w);
-            if (p.dlogits) {
-                uint16_t *drow = p.dlogits + row * p.ld + col_begin;
-                const uint32_t sbase = smem_u32(stage_base + (size_t)b_st * p.stage_bytes);
-                const int32_t yv = (y >= col_begin && y < col_end) ? ((y - col_begin) >> 3) : -1;
+    } else {
+        // ================================================================ compute warps
+        int a_st = 0, a_slot = 0, b_st = 0, b_slot = 0;
+        uint32_t a_ph = 0, b_ph = 0;
+        for (int it = 0; it < my_rows + D; ++it) {
+            if (it < my_rows) {
+                // ------------------------------------------------------------ A(it)
+                mbar_wait(&full_bar[a_st], a_ph);
+                const uint32_t sbase = smem_u32(stage_base + (size_t)a_st * p.stage_bytes);
+                uint32_t mx2 = kBf16NegInfPair;
+                uint4 v[VPT];
 #pragma unroll
                 for (int j = 0; j < VPT; ++j) {
-                    const int vi = tid + j * kThreads;
-                    if (vi >= my_vecs) continue;
-                    uint4 d = make_uint4(0u, 0u, 0u, 0u);
-                    if (sc != 0.0f) {
-                        const uint4 x = lds128(sbase + (uint32_t)vi * 16u);
-                        d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.x), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x.x), kLog2e, -lse2)));
-                        d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.y), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x.y), kLog2e, -lse2)));
-                        d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.z), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x.z), kLog2e, -lse2)));
-                        d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.w), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x.w), kLog2e, -lse2)));
+                    const int vi = tid + j * kCompThreads;
+                    if (vi < my_vecs) {
+                        v[j] = lds128(sbase + (uint32_t)vi * 16u);
+                        // columns >= V of the row's ragged last vector count as -inf
+                        if (vi == tail_vi) v[j] = mask_tail(v[j], tail_valid);
+                    } else {
+                        v[j] = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
+                                          kBf16NegInfPair);
                     }
-                    if (vi == tail_vi)
-                        store_tail(drow + vi * 8, d, tail_valid);
-                    else
-                        stg_stream(drow + vi * 8, d);
-                    if (vi == yv) {
-                        // target entry: s (p_y - 1), from the unrounded probability
-                        const float py = ex2(fmaf(zy, kLog2e, -lse2));
-                        drow[y - col_begin] = f2bf(sc * (py - 1.0f));
+                    mx2 = bmax2(bmax2(mx2, bmax2(v[j].x, v[j].y)), bmax2(v[j].z, v[j].w));
+                }
+                float a = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
+                const float aL = (a == -INFINITY) ? 0.0f : a;
+                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+                for (int j = 0; j < VPT; ++j) {
+                    s0 += ex2(fmaf(bf_lo(v[j].x), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].x), kLog2e, -aL));
+                    s1 += ex2(fmaf(bf_lo(v[j].y), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].y), kLog2e, -aL));
+                    s2 += ex2(fmaf(bf_lo(v[j].z), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].z), kLog2e, -aL));
+                    s3 += ex2(fmaf(bf_lo(v[j].w), kLog2e, -aL)) + ex2(fmaf(bf_hi(v[j].w), kLog2e, -aL));
+                }
+                float s = (s0 + s1) + (s2 + s3);
+                warp_lse2_combine(a, s);
+                if (lane == 0) {
+                    red[a_slot * kComp + warp] = make_float2(a, s);
+                    mbar_arrive(&part_bar[a_slot]);
+                }
+                if (++a_st == S) { a_st = 0; a_ph ^= 1u; }
+                if (++a_slot == NX) a_slot = 0;
+            }
+            if (it >= D) {
+                // ------------------------------------------------------------ B(it - D)
+                const int64_t row = g + (int64_t)(it - D) * n_cl;
+                mbar_wait(&scal_bar[b_slot], b_ph);
+                const float4 sc4 = rowsc[b_slot];
+                const float lse2 = sc4.x, sc = sc4.y, zy = sc4.z;
+                const int32_t y = __float_as_int(sc4.w);
+                if (p.dlogits) {
+                    uint16_t *drow = p.dlogits + row * p.ld + col_begin;
+                    const uint32_t sbase = smem_u32(stage_base + (size_t)b_st * p.stage_bytes);
+                    const int32_t yv = (y >= col_begin && y < col_end) ? ((y - col_begin) >> 3) : -1;
+#pragma unroll
+                    for (int j = 0; j < VPT; ++j) {
+                        const int vi = tid + j * kCompThreads;
+                        if (vi >= my_vecs) continue;
+                        uint4 d = make_uint4(0u, 0u, 0u, 0u);
+                        if (sc != 0.0f) {
+                            const uint4 x = lds128(sbase + (uint32_t)vi * 16u);
+                            d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.x), kLog2e, -lse2)),
+                                              sc * ex2(fmaf(bf_hi(x.x), kLog2e, -lse2)));
+                            d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.y), kLog2e, -lse2)),
+                                              sc * ex2(fmaf(bf_hi(x.y), kLog2e, -lse2)));
+                            d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.z), kLog2e, -lse2)),
+                                              sc * ex2(fmaf(bf_hi(x.z), kLog2e, -lse2)));
+                            d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.w), kLog2e, -lse2)),
+                                              sc * ex2(fmaf(bf_hi(x.w), kLog2e, -lse2)));
+                        }
+                        if (vi == tail_vi)
+                            store_tail(drow + vi * 8, d, tail_valid);
+                        else
+                            stg_stream(drow + vi * 8, d);
+                        if (vi == yv) {
+                            // target entry: s (p_y - 1), from the unrounded probability
+                            const float py = ex2(fmaf(zy, kLog2e, -lse2));
+                            drow[y - col_begin] = f2bf(sc * (py - 1.0f));
+                        }
                     }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&free_bar[b_st]);   // this warp is done with the stage
+                if (++b_st == S) b_st = 0;
+                if (++b_slot == NX) { b_slot = 0; b_ph ^= 1u; }
             }
-            refill_st = b_st;
-            if (++b_st == S) b_st = 0;
-            if (++b_slot == NX) b_slot = 0;
         }
     }
     __syncthreads();
@@ -337,7 +368,7 @@ namespace {
 int pick_cluster(int32_t n_vec_row) {
     // smallest power of two keeping a CTA slice <= 8 vectors (64 bf16) per thread
     int C = 1;
-    while (C < kMaxCluster && (n_vec_row + C - 1) / C > 8 * kThreads) C *= 2;
+    while (C < kMaxCluster && (n_vec_row + C - 1) / C > 8 * kCompThreads) C *= 2;
     return C;
 }
 
@@ -417,7 +448,7 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
     int C = (tune && tune->cluster_size > 0) ? tune->cluster_size : pick_cluster(fp.n_vec_row);
     int ctas_per_sm = (tune && tune->ctas_per_sm > 0) ? tune->ctas_per_sm : 2;
     fp.slice_vec = (fp.n_vec_row + C - 1) / C;
-    const int vpt_needed = (fp.slice_vec + kThreads - 1) / kThreads;
+    const int vpt_needed = (fp.slice_vec + kCompThreads - 1) / kCompThreads;
     fp.stage_bytes = (uint32_t)(((size_t)fp.slice_vec * 16 + 127) / 128 * 128);
     const bool auto_lag = !(tune && tune->lag > 0);
     int lag = auto_lag ? 2 : tune->lag;
@@ -435,6 +466,11 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
     }
     if (auto_lag && stages < lag + 2) lag = stages - 2 >= 1 ? stages - 2 : 1;
     fp.lag = lag;
+    {
+        const char *pc = getenv("GRPO_FUSED_PIECE");
+        fp.piece = pc ? (uint32_t)atoi(pc) : 0u;
+        fp.piece = fp.piece ? (fp.piece + 15u) / 16u * 16u : fp.stage_bytes;
+    }
     if (stages < lag + 2) {
         if (why) snprintf(why, why_len, "%d stages < lag + 2 = %d (slice %u B)", stages, lag + 2,
                           fp.stage_bytes);
