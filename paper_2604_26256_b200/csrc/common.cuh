@@ -145,6 +145,15 @@ __device__ __forceinline__ void st_async_v4(uint32_t raddr, uint32_t rbar, float
         : "memory");
 }
 
+// 8-byte remote store completing 8 bytes of transaction on the remote mbarrier.
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t rbar, float a, float b) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(
+            raddr),
+        "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(rbar)
+        : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -15,19 +15,22 @@
 // dlogits: 4V bytes per row.
 //
 // Warp specialisation, no CTA-wide barrier in the loop:
-//   compute warps (kComp):  A(k): reduce the slice of row k (stage k % S) to
-//       a log2-domain partial per warp; B(k - lag): once the row scalars of
-//       row k - lag are published, write its dlogits from the stage, then
-//       release the stage;
-//   control warp (1):  per row r: read z_y if this CTA owns the target
-//       column, combine the compute warps' partials, send the CTA partial
-//       (16 B) to every CTA of the cluster over DSMEM (st.async completing on
-//       the peer's mbarrier); E(r - lag + 1): once all C partials of that row
-//       are in, form lse, logp, r, clip, term and the token scale, publish
-//       them to the compute warps (and to global memory from cluster rank 0);
-//       refill the stage released by B(r - lag - 1) with row r - lag - 1 + S.
-// Hand-offs are mbarriers: full (TMA -> all), part (compute -> control),
-// scal (control -> compute), free (compute -> control), xbar (peers -> control).
+//   compute warps (kComp), per row k:
+//     A(k): reduce the warp's share of the slice (stage k % S) to a
+//           log2-domain partial (a, s) and st.async it (8 B) straight into
+//           every CTA of the cluster (DSMEM, completing on the peer's xbar);
+//     B(k - lag): when the row scalars of row k - lag are published, write
+//           its dlogits from the stage; the last warp to finish a stage
+//           refills it with row k - lag + S (bulk TMA).
+//   control warp, per row r:  read z_y if this CTA owns the target column and
+//     st.async (z_y, owner) to every CTA; E(r - lag + 1): once all C x kComp
+//     partials of that row are in, form lse, logp, r, clip, term and the token
+//     scale, publish them (smem + mbarrier), write the per-row outputs (cluster
+//     rank 0), and re-arm the exchange slot.
+// A peer's A(k) needs this CTA's partials of row k - S, and this CTA's A(j)
+// comes after its B(j - lag - 1), i.e. after E(j - lag - 1); so with
+// NX = S + lag + 1 exchange slots a slot is consumed and re-armed (in E(k))
+// before any peer can write it for row k + NX.
 #include <cstdio>
 #include <cstdlib>
 
@@ -40,7 +43,8 @@ constexpr int kWarps = kComp + 1;           // + the control warp
 constexpr int kThreads = kWarps * 32;
 constexpr int kCompThreads = kComp * 32;
 constexpr int kMaxCluster = 16;
-constexpr int kMaxSlots = 6;                // ring of per-row hand-off slots (>= 2*lag + 2)
+constexpr int kMaxStages = 8;
+constexpr int kMaxSlots = kMaxStages + 3;   // exchange slots NX = S + lag + 1
 
 struct FusedParams {
     const uint16_t *logits;
@@ -60,10 +64,6 @@ struct FusedParams {
     uint32_t stage_bytes;
 };
 
-struct __align__(16) XMsg {
-    float m, s, zy, owner;
-};
-
 __device__ __forceinline__ RowInfo load_rowinfo(const RowInfo *p) {
     const int4 q = __ldg(reinterpret_cast<const int4 *>(p));
     RowInfo r;
@@ -76,14 +76,15 @@ __device__ __forceinline__ RowInfo load_rowinfo(const RowInfo *p) {
 
 // Shared-memory carve-up (host and device agree through this one function).
 struct FusedSmem {
-    size_t bars, xch, red, meta, rowsc, total;
+    size_t bars, cnt, part, zmsg, meta, rowsc, total;
 };
 __host__ __device__ __forceinline__ FusedSmem fused_smem_layout(int S, uint32_t stage_bytes) {
     FusedSmem L;
-    L.bars = (size_t)S * stage_bytes;  // full[S], free[S], part[6], scal[6], xbar[6]
-    L.xch = L.bars + (((size_t)(2 * S + 3 * kMaxSlots) * 8 + 15) / 16) * 16;
-    L.red = L.xch + (size_t)kMaxSlots * kMaxCluster * sizeof(XMsg);
-    L.meta = L.red + (size_t)kMaxSlots * kComp * sizeof(float2);
+    L.bars = (size_t)S * stage_bytes;  // full[S], scal[kMaxSlots], xbar[kMaxSlots]
+    L.cnt = L.bars + (size_t)(kMaxStages + 2 * kMaxSlots) * 8;                 // free counters
+    L.part = L.cnt + (((size_t)kMaxStages * 4 + 15) / 16) * 16;
+    L.zmsg = L.part + (size_t)kMaxSlots * kMaxCluster * kComp * sizeof(float2);
+    L.meta = L.zmsg + (size_t)kMaxSlots * kMaxCluster * sizeof(float2);
     L.rowsc = L.meta + kMaxSlots * sizeof(RowInfo);
     L.total = L.rowsc + kMaxSlots * sizeof(float4);
     return L;
@@ -103,18 +104,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     extern __shared__ __align__(128) uint8_t smem[];
     const int S = p.stages;
     const int D = p.lag;
-    const int NX = 2 * D + 2;
+    const int NX = S + D + 1;
     const FusedSmem lay = fused_smem_layout(S, p.stage_bytes);
     uint8_t *stage_base = smem;
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(smem + lay.bars);  // [S]
-    uint64_t *free_bar = full_bar + S;                                    // [S]
-    uint64_t *part_bar = free_bar + S;                                    // [NX]
-    uint64_t *scal_bar = part_bar + kMaxSlots;                            // [NX]
+    uint64_t *scal_bar = full_bar + kMaxStages;                           // [NX]
     uint64_t *xbar = scal_bar + kMaxSlots;                                // [NX]
-    XMsg *xch = reinterpret_cast<XMsg *>(smem + lay.xch);                // [kMaxSlots][kMaxCluster]
-    float2 *red = reinterpret_cast<float2 *>(smem + lay.red);            // [kMaxSlots][kComp]
-    RowInfo *meta = reinterpret_cast<RowInfo *>(smem + lay.meta);        // [kMaxSlots]
-    float4 *rowsc = reinterpret_cast<float4 *>(smem + lay.rowsc);        // [kMaxSlots]
+    int *free_cnt = reinterpret_cast<int *>(smem + lay.cnt);             // [S]
+    float2 *part = reinterpret_cast<float2 *>(smem + lay.part);          // [NX][C][kComp]
+    float2 *zmsg = reinterpret_cast<float2 *>(smem + lay.zmsg);          // [NX][C]
+    RowInfo *meta = reinterpret_cast<RowInfo *>(smem + lay.meta);        // [NX]
+    float4 *rowsc = reinterpret_cast<float4 *>(smem + lay.rowsc);        // [NX]
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int32_t tail_valid = p.V - (p.n_vec_row - 1) * 8;
     const int32_t tail_vi = (tail_valid < 8) ? (p.n_vec_row - 1 - vec_begin) : -1;
     const int32_t my_rows = (g < p.n_rows) ? (int32_t)((p.n_rows - 1 - g) / n_cl + 1) : 0;
-    const uint32_t xbytes = C * (uint32_t)sizeof(XMsg);
+    const uint32_t xbytes = C * (uint32_t)((kComp + 1) * sizeof(float2));
     const int64_t row_stride = n_cl * p.ld;            // elements between my consecutive rows
     const uint16_t *src0 = p.logits + g * p.ld + col_begin;
     const bool control = (warp == kComp);
@@ -141,18 +141,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (control && lane == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&full_bar[i], 1);
-            mbar_init(&free_bar[i], kComp);
+            free_cnt[i] = 0;
         }
         for (int i = 0; i < NX; ++i) {
-            mbar_init(&part_bar[i], kComp);
             mbar_init(&scal_bar[i], 1);
             mbar_init(&xbar[i], 1);
         }
         fence_mbar_init_cluster();
-        for (int k = 0; k < D && k < my_rows; ++k)                // rows a peer may send at once
+        for (int k = 0; k < NX && k < my_rows; ++k)   // every slot armed for its first row
             mbar_arrive_expect_tx(&xbar[k], xbytes);
         const uint64_t pol = policy_evict_first();
-        for (int k = 0; k < S && k < my_rows; ++k) {               // fill the ring
+        for (int k = 0; k < S && k < my_rows; ++k) {   // fill the ring
             mbar_arrive_expect_tx(&full_bar[k], my_bytes);
             if (my_bytes)
                 load_slice(stage_base + (size_t)k * p.stage_bytes, src0 + k * row_stride, my_bytes,
@@ -163,19 +162,18 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (control) {
         // ================================================================ control warp
-        const uint64_t pol = policy_evict_first();
-        int c_st = 0, x_slot = 0, arm_slot = D % NX, e_slot = 0, f_st = 0;
-        uint32_t c_ph = 0, x_ph = 0, e_ph = 0, f_ph = 0;
+        int c_st = 0, z_slot = 0, e_slot = 0;
+        uint32_t c_ph = 0, e_ph = 0;
         RowInfo ri0{}, ri1{};                           // lane 0: rows r and r + 1
         if (lane == 0 && my_rows > 0) ri0 = load_rowinfo(p.rowinfo + g);
         if (lane == 0 && my_rows > 1) ri1 = load_rowinfo(p.rowinfo + g + n_cl);
         for (int r = 0; r < my_rows + D; ++r) {
             if (r < my_rows) {
-                // (a) the row's slice has landed: this CTA reads z_y if it owns column y
+                // (a) the row's slice has landed: z_y if this CTA owns column y, to every CTA
                 mbar_wait(&full_bar[c_st], c_ph);
                 float zy = 0.0f, own = 0.0f;
                 if (lane == 0) {
-                    meta[x_slot] = ri0;
+                    meta[z_slot] = ri0;
                     const int32_t y = ri0.target;
                     if (y >= col_begin && y < col_end && y < p.V) {
                         uint16_t hv;
@@ -189,43 +187,34 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                     ri0 = ri1;
                     if (r + 2 < my_rows) ri1 = load_rowinfo(p.rowinfo + g + (int64_t)(r + 2) * n_cl);
-                    // arm the exchange of row r + D before any peer can send it
-                    if (r + D < my_rows) mbar_arrive_expect_tx(&xbar[arm_slot], xbytes);
                 }
-                // (b) combine the compute warps' partials, send the CTA partial to every peer
-                mbar_wait(&part_bar[x_slot], x_ph);
-                float cm = -INFINITY, cs = 0.0f;
-                if (lane < kComp) {
-                    const float2 r2 = red[x_slot * kComp + lane];
-                    cm = r2.x;
-                    cs = r2.y;
-                }
-                warp_lse2_combine(cm, cs);
                 zy = __shfl_sync(0xFFFFFFFFu, zy, 0);
                 own = __shfl_sync(0xFFFFFFFFu, own, 0);
-                if (lane < (int)C) {
-                    const uint32_t laddr = smem_u32(&xch[x_slot * kMaxCluster + crank]);
-                    const uint32_t lbar = smem_u32(&xbar[x_slot]);
-                    st_async_v4(mapa_shared(laddr, lane), mapa_shared(lbar, lane), cm, cs, zy, own);
-                }
+                if (lane < (int)C)
+                    st_async_v2(mapa_shared(smem_u32(&zmsg[z_slot * kMaxCluster + crank]), lane),
+                                mapa_shared(smem_u32(&xbar[z_slot]), lane), zy, own);
                 if (++c_st == S) { c_st = 0; c_ph ^= 1u; }
-                if (++x_slot == NX) { x_slot = 0; x_ph ^= 1u; }
-                if (++arm_slot == NX) arm_slot = 0;
+                if (++z_slot == NX) z_slot = 0;
             }
-            // (c) E(r - D + 1): the row scalars, once every peer's partial is in
+            // (b) E(r - D + 1): the row scalars, once every partial of the row is in
             const int ke = r - D + 1;
             if (ke >= 0 && ke < my_rows) {
                 mbar_wait(&xbar[e_slot], e_ph);
-                float M = -INFINITY, Ssum = 0.0f, zsrc = 0.0f;
-                bool own = false;
-                if (lane < (int)C) {
-                    const XMsg msg = xch[e_slot * kMaxCluster + lane];
-                    M = msg.m;
-                    Ssum = msg.s;
-                    zsrc = msg.zy;
-                    own = msg.owner != 0.0f;
+                const int np = (int)C * kComp;
+                const float2 *ps = part + (size_t)e_slot * kMaxCluster * kComp;
+                float M = -INFINITY, Ssum = 0.0f;
+                for (int q = lane; q < np; q += 32) {
+                    const float2 v2 = ps[q];
+                    lse2_merge(M, Ssum, v2.x, v2.y);
                 }
                 warp_lse2_combine(M, Ssum);
+                float zsrc = 0.0f;
+                bool own = false;
+                if (lane < (int)C) {
+                    const float2 zm = zmsg[e_slot * kMaxCluster + lane];
+                    zsrc = zm.x;
+                    own = zm.y != 0.0f;
+                }
                 const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
                 const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
                 if (lane == 0) {
@@ -238,6 +227,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
                     rowsc[e_slot] = make_float4(lse2, o.s, zyv,
                                                 __int_as_float(y_valid ? ri.target : -1));
+                    // slot consumed: re-arm it for row ke + NX before the compute warps
+                    // can let any peer reach that row
+                    if (ke + NX < my_rows) mbar_arrive_expect_tx(&xbar[e_slot], xbytes);
                     mbar_arrive(&scal_bar[e_slot]);
                     if (crank == 0) {
                         const int64_t row = g + (int64_t)ke * n_cl;
@@ -253,25 +245,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 __syncwarp();
                 if (++e_slot == NX) { e_slot = 0; e_ph ^= 1u; }
             }
-            // (d) refill the stage released by B(r - D - 1) with row r - D - 1 + S
-            const int kd = r - D - 1;
-            if (kd >= 0) {
-                if (kd + S < my_rows) {
-                    mbar_wait(&free_bar[f_st], f_ph);
-                    if (lane == 0) {
-                        mbar_arrive_expect_tx(&full_bar[f_st], my_bytes);
-                        if (my_bytes)
-                            load_slice(stage_base + (size_t)f_st * p.stage_bytes,
-                                       src0 + (int64_t)(kd + S) * row_stride, my_bytes, p.piece,
-                                       &full_bar[f_st], pol);
-                    }
-                    __syncwarp();
-                }
-                if (++f_st == S) { f_st = 0; f_ph ^= 1u; }
-            }
         }
     } else {
         // ================================================================ compute warps
+        const uint64_t pol = policy_evict_first();
         int a_st = 0, a_slot = 0, b_st = 0, b_slot = 0;
         uint32_t a_ph = 0, b_ph = 0;
         for (int it = 0; it < my_rows + D; ++it) {
@@ -306,23 +283,26 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 float s = (s0 + s1) + (s2 + s3);
                 warp_lse2_combine(a, s);
-                if (lane == 0) {
-                    red[a_slot * kComp + warp] = make_float2(a, s);
-                    mbar_arrive(&part_bar[a_slot]);
-                }
+                // the warp partial goes straight to every CTA of the cluster
+                if (lane < (int)C)
+                    st_async_v2(
+                        mapa_shared(smem_u32(&part[((size_t)a_slot * kMaxCluster + crank) * kComp + warp]),
+                                    lane),
+                        mapa_shared(smem_u32(&xbar[a_slot]), lane), a, s);
                 if (++a_st == S) { a_st = 0; a_ph ^= 1u; }
                 if (++a_slot == NX) a_slot = 0;
             }
             if (it >= D) {
                 // ------------------------------------------------------------ B(it - D)
-                const int64_t row = g + (int64_t)(it - D) * n_cl;
+                const int k = it - D;
+                const int64_t row = g + (int64_t)k * n_cl;
                 mbar_wait(&scal_bar[b_slot], b_ph);
                 const float4 sc4 = rowsc[b_slot];
                 const float lse2 = sc4.x, sc = sc4.y, zy = sc4.z;
                 const int32_t y = __float_as_int(sc4.w);
+                const uint32_t sbase = smem_u32(stage_base + (size_t)b_st * p.stage_bytes);
                 if (p.dlogits) {
                     uint16_t *drow = p.dlogits + row * p.ld + col_begin;
-                    const uint32_t sbase = smem_u32(stage_base + (size_t)b_st * p.stage_bytes);
                     const int32_t yv = (y >= col_begin && y < col_end) ? ((y - col_begin) >> 3) : -1;
 #pragma unroll
                     for (int j = 0; j < VPT; ++j) {
@@ -351,8 +331,22 @@ __global__ void __launch_bounds__(kThreads, 2)
                         }
                     }
                 }
+                // the last warp done with this stage refills it with row k + S
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&free_bar[b_st]);   // this warp is done with the stage
+                if (lane == 0) {
+                    __threadfence_block();
+                    if (atomicAdd(&free_cnt[b_st], 1) == kComp - 1) {
+                        free_cnt[b_st] = 0;
+                        __threadfence_block();
+                        if (k + S < my_rows) {
+                            mbar_arrive_expect_tx(&full_bar[b_st], my_bytes);
+                            if (my_bytes)
+                                load_slice(stage_base + (size_t)b_st * p.stage_bytes,
+                                           src0 + (int64_t)(k + S) * row_stride, my_bytes, p.piece,
+                                           &full_bar[b_st], pol);
+                        }
+                    }
+                }
                 if (++b_st == S) b_st = 0;
                 if (++b_slot == NX) { b_slot = 0; b_ph ^= 1u; }
             }
@@ -462,7 +456,7 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
         const size_t fixed = fused_smem_layout(0, fp.stage_bytes).total + 8 * 8;
         const size_t budget = per_sm / ctas_per_sm - 1024 - fixed;
         stages = (int)(budget / fp.stage_bytes);
-        if (stages > 8) stages = 8;
+        if (stages > kMaxStages) stages = kMaxStages;
     }
     if (auto_lag && stages < lag + 2) lag = stages - 2 >= 1 ? stages - 2 : 1;
     fp.lag = lag;
@@ -470,6 +464,10 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
         const char *pc = getenv("GRPO_FUSED_PIECE");
         fp.piece = pc ? (uint32_t)atoi(pc) : 0u;
         fp.piece = fp.piece ? (fp.piece + 15u) / 16u * 16u : fp.stage_bytes;
+    }
+    if (stages > kMaxStages) {
+        if (why) snprintf(why, why_len, "stages %d > %d", stages, kMaxStages);
+        return cudaErrorInvalidValue;
     }
     if (stages < lag + 2) {
         if (why) snprintf(why, why_len, "%d stages < lag + 2 = %d (slice %u B)", stages, lag + 2,
