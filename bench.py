@@ -317,6 +317,7 @@ def main():
     ms = e0.elapsed_time(e1)
     G.grpo_profile_enable(False)
     n_traced, kern_ms = G.grpo_profile_collect()
+    plan = G.grpo_async_last_plan()
     launches = loss.launches - launches0
     clocks = sampler.stop() if sampler else None
     ms_max = max_over_ranks(ms)
@@ -403,8 +404,9 @@ def main():
                                  "chunk buffer (DESIGN.md input recipe)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "fused_cluster_kernel" if (tune is None or tune["kernel"] != 2)
-                         else "rowwise_kernel",
+                         "kernel": {1: "fused_cluster_kernel", 2: "rowwise_kernel"}.get(
+                             plan["kernel"], str(plan["kernel"])),
+                         "plan": plan,
                          "bytes_per_row": bytes_per_row, "launches": n_traced,
                          "avg_launch_ms": avg_launch_ms,
                          "kernel_share_of_step": kern_ms_max / ms_max},

@@ -92,12 +92,14 @@ enum {
 
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
-    int32_t kernel;        /* 0 auto, 1 cluster-resident fused (roofline design), 2 row-wise two-pass */
+    int32_t kernel;        /* 0 auto (= 2 today), 1 cluster-resident fused, 2 row-wise two-pass */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
-    int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1)                                    */
-    int32_t stages;        /* 0 auto, else lag+2..8 shared-memory row stages per CTA (kernel 1) */
-    int32_t lag;           /* 0 auto (1), else 1..2: rows between a row's reduction and its   */
+    int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1); 1,2,4,8 (kernel 2: 1024/512/256/256 threads) */
+    int32_t stages;        /* 0 auto, else lag+2..8 shared-memory row stages per CTA (kernel 1); */
+                           /* kernel 2: 4, 8 or 16 vectors in flight per thread             */
+    int32_t lag;           /* 0 auto, else 1..2: rows between a row's reduction and its       */
                            /* backward, hiding the cluster exchange (kernel 1)               */
+    int32_t prefetch;      /* kernel 2: 1 = TMA-prefetch each CTA's next row into L2         */
 } grpo_tune_t;
 
 /*

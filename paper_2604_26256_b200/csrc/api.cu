@@ -276,8 +276,10 @@ grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int
     const bool traced = n_rows > 0 && prof_on();
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
-    if (kernel == 2) {
-        e = grpo::launch_fused_rowwise(a, s, &launches, &g_last_plan);
+    // kernel 0 (auto) = the row-wise two-pass kernel: the faster of the two on
+    // B200 today (DESIGN.md "Kernel K3" measurements); 1 = cluster-resident.
+    if (kernel == 0 || kernel == 2) {
+        e = grpo::launch_fused_rowwise(a, tune, s, &launches, &g_last_plan);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");
     } else {
         e = grpo::launch_fused_cluster(a, tune, s, &launches, why, sizeof why, &g_last_plan);

@@ -89,6 +89,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return pol;
 }
 
+// Ask the TMA engine to bring [src, src + bytes) into L2 (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // 1-D bulk TMA global -> shared, completion counted on `bar` (bytes % 16 == 0).
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
                                          uint64_t *bar, uint64_t policy) {
@@ -165,6 +170,12 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
                  : "r"(addr)
                  : "memory");
     return v;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -365,8 +376,8 @@ struct LossArgs {
 cudaError_t launch_rowinfo(const LossArgs &a, cudaStream_t s, int *launches);
 cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
                                  int *launches, char *why, size_t why_len, grpo_plan_t *plan);
-cudaError_t launch_fused_rowwise(const LossArgs &a, cudaStream_t s, int *launches,
-                                 grpo_plan_t *plan);
+cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
+                                 int *launches, grpo_plan_t *plan);
 cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches);
 cudaError_t launch_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
                             const int64_t *target_ids, const float *lse, const float *scale,

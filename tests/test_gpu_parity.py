@@ -11,6 +11,8 @@ from tests.gpu_util import compare, run_gpu, run_oracle, to_dev_bits
 pytestmark = pytest.mark.gpu
 
 KERNELS = [{"kernel": 1}, {"kernel": 2}]
+ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u}
+                 for c, u in ((1, 4), (1, 8), (2, 4), (2, 8), (2, 16), (3, 4), (4, 16), (8, 4))]
 
 
 def _case(name, seed, **kw):
@@ -57,6 +59,18 @@ def test_cluster_sizes(dev, C):
         ran += 1
     if (b.V + 7) // 8 <= C * 16 * 256:
         assert ran > 0
+
+
+@pytest.mark.parametrize("plan", ROWWISE_PLANS, ids=lambda d: f"cps{d['ctas_per_sm']}u{d['stages']}")
+def test_rowwise_plans(dev, plan):
+    """Every row-wise kernel instantiation (threads x vectors in flight) matches the oracle."""
+    for name in ("ragged", "mid152k"):
+        b, bits = _case(name, 6)
+        ref = run_oracle(b, bits)
+        gpu = run_gpu(b, bits, dev, tune=plan)
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+    gpu = run_gpu(b, bits, dev, tune=dict(plan, prefetch=1))
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
 
 
 @pytest.mark.parametrize("chunks", [2, 3, 7])
