@@ -256,48 +256,56 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cud
 }
 
 // ------------------------------------------------------------------ segmented reduce
-// One warp per trajectory i: its rows inside this chunk, summed in fp64 in a
-// fixed order (lane-strided sequential sums, then an xor butterfly whose
-// result is identical in every lane).  part[i*5 + {0..4}] =
-// {inv_norm*sum term, inv_norm*sum |term|, sum logp, #clipped, #active}.
-__global__ void segsum_kernel(int64_t row_begin, int64_t n_rows, const int64_t *__restrict__ cu,
-                              int32_t N, const int32_t *__restrict__ traj_index,
-                              const float *__restrict__ inv_norm,
-                              const float *__restrict__ term, const float *__restrict__ logp,
-                              const uint8_t *__restrict__ flags, double *__restrict__ traj_sum,
-                              double *__restrict__ part) {
-    const int lane = threadIdx.x & 31;
-    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (i >= N) return;
+// One CTA per trajectory i: its rows inside this chunk, summed in fp64 in a
+// fixed order (thread-strided sequential sums, an xor butterfly per warp, then
+// the warps in index order), so the result does not depend on scheduling.
+// part[i*5 + {0..4}] = {inv_norm*sum term, inv_norm*sum |term|, sum logp,
+// #clipped, #active}; traj_sum[i] += sum term when the chunk holds rows of i.
+constexpr int kSegThreads = 256;
+
+__global__ void __launch_bounds__(kSegThreads)
+    segsum_kernel(int64_t row_begin, int64_t n_rows, const int64_t *__restrict__ cu, int32_t N,
+                  const int32_t *__restrict__ traj_index, const float *__restrict__ inv_norm,
+                  const float *__restrict__ term, const float *__restrict__ logp,
+                  const uint8_t *__restrict__ flags, double *__restrict__ traj_sum,
+                  double *__restrict__ part) {
+    __shared__ double sh[5][kSegThreads / 32];
+    const int64_t i = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t row_end = row_begin + n_rows;
     const int64_t b = max(cu[i], row_begin), e = min(cu[i + 1], row_end);
-    double st = 0.0, sa = 0.0, sl = 0.0, nc = 0.0, na = 0.0;
-    for (int64_t t = b + lane; t < e; t += 32) {
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t t = b + threadIdx.x; t < e; t += kSegThreads) {
         const int64_t k = t - row_begin;
         const double x = (double)term[k];
-        st += x;
-        sa += fabs(x);
-        sl += (double)logp[k];
+        acc[0] += x;
+        acc[1] += fabs(x);
+        acc[2] += (double)logp[k];
         const uint8_t f = flags[k];
-        nc += (f & kRowClipped) ? 1.0 : 0.0;
-        na += (f & kRowActive) ? 1.0 : 0.0;
+        acc[3] += (f & kRowClipped) ? 1.0 : 0.0;
+        acc[4] += (f & kRowActive) ? 1.0 : 0.0;
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        st += __shfl_xor_sync(0xFFFFFFFFu, st, off);
-        sa += __shfl_xor_sync(0xFFFFFFFFu, sa, off);
-        sl += __shfl_xor_sync(0xFFFFFFFFu, sl, off);
-        nc += __shfl_xor_sync(0xFFFFFFFFu, nc, off);
-        na += __shfl_xor_sync(0xFFFFFFFFu, na, off);
+    for (int q = 0; q < 5; ++q) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xFFFFFFFFu, acc[q], off);
+        if (lane == 0) sh[q][warp] = acc[q];
     }
-    if (lane == 0) {
-        const double w = (double)inv_norm[traj_index ? traj_index[i] : i];
-        if (e > b) traj_sum[i] += st;
-        part[i * 5 + 0] = w * st;
-        part[i * 5 + 1] = w * sa;
-        part[i * 5 + 2] = sl;
-        part[i * 5 + 3] = nc;
-        part[i * 5 + 4] = na;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            tot[q] = 0.0;
+            for (int w = 0; w < kSegThreads / 32; ++w) tot[q] += sh[q][w];
+        }
+        const double wgt = (double)inv_norm[traj_index ? traj_index[i] : i];
+        if (e > b) traj_sum[i] += tot[0];
+        part[i * 5 + 0] = wgt * tot[0];
+        part[i * 5 + 1] = wgt * tot[1];
+        part[i * 5 + 2] = tot[2];
+        part[i * 5 + 3] = tot[3];
+        part[i * 5 + 4] = tot[4];
     }
 }
 
@@ -330,8 +338,7 @@ __global__ void __launch_bounds__(1024) stats_kernel(int32_t N, int64_t n_rows,
 }
 
 cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches) {
-    const int64_t threads = (int64_t)a.N * 32;
-    segsum_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+    segsum_kernel<<<(unsigned)a.N, kSegThreads, 0, s>>>(
         a.row_begin, a.n_rows, a.cu_seqlens, a.N, a.traj_index, a.inv_norm, a.term_ws, a.logp_ws,
         a.flag_ws, a.traj_sum, a.part_ws);
     stats_kernel<<<1, 1024, 0, s>>>(a.N, a.n_rows, a.part_ws, a.stats);
