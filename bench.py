@@ -131,7 +131,9 @@ def oracle_step(O, batch, rows, bits, eps):
 
 
 def load_oracle():
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to its workers)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    os.environ["OMP_NUM_THREADS"] = str(cores or 1)
     import oracle.oracle as O
     return O, int(os.environ["OMP_NUM_THREADS"])
 
