@@ -47,7 +47,7 @@ class ValidateSummary(C.Structure):
 class Tune(C.Structure):
     _fields_ = [("kernel", C.c_int32), ("cluster_size", C.c_int32),
                 ("ctas_per_sm", C.c_int32), ("stages", C.c_int32), ("lag", C.c_int32),
-                ("prefetch", C.c_int32)]
+                ("prefetch", C.c_int32), ("row_cache", C.c_int32)]
 
 
 class Plan(C.Structure):
@@ -210,7 +210,7 @@ def grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav
     tune_p = None
     if tune is not None:
         t = Tune(*[int(tune.get(k, 0)) for k in ("kernel", "cluster_size", "ctas_per_sm", "stages",
-                                                  "lag", "prefetch")])
+                                                  "lag", "prefetch", "row_cache")])
         tune_p = C.byref(t)
     for name, x in (("logits", logits), ("dlogits", dlogits)):
         if x is not None and x.element_size() != 2:

@@ -68,6 +68,7 @@ struct RowwiseParams {
     uint8_t *flag_ws;
     int32_t prefetch;
     int32_t flags;  // bit 0: pass 2 in reverse batch order; bit 1: pass-1 policy evict_normal
+    int32_t cache_batches;  // leading batches of NT*U vectors kept in shared memory
 };
 
 // One CTA per row at a time (persistent, grid-stride over rows).  Pass 1 streams
@@ -90,15 +91,19 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
     const uint64_t pol_stream = policy_evict_first();
     const uint32_t row_bytes = (uint32_t)n_vec * 16u;
     const int n_batch = (n_vec + NT * U - 1) / (NT * U);
+    extern __shared__ uint4 row_cache[];  // [cache_batches][U][NT]
+    const int cache_batches = min(p.cache_batches, n_batch);
     if (p.prefetch && threadIdx.x == 0 && blockIdx.x < p.n_rows)
         bulk_prefetch_l2(p.logits + (int64_t)blockIdx.x * p.ld, row_bytes);
     for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
         const uint16_t *zrow = p.logits + row * p.ld;
         if (p.prefetch && threadIdx.x == 0 && row + gridDim.x < p.n_rows)
             bulk_prefetch_l2(zrow + (int64_t)gridDim.x * p.ld, row_bytes);
-        // ---- pass 1: log2-domain (max, sum exp) of the row
+        // ---- pass 1: log2-domain (max, sum exp) of the row; the first cache_batches
+        //      batches are also kept in shared memory for pass 2
         float a = -INFINITY, s = 0.0f;
-        for (int base = threadIdx.x; base < n_vec; base += NT * U) {
+        for (int bi = 0; bi < n_batch; ++bi) {
+            const int base = threadIdx.x + bi * NT * U;
             uint4 x[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) {
@@ -107,6 +112,11 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
                                   : make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
                                                kBf16NegInfPair);
                 if (vi == tail_vi) x[j] = mask_tail(x[j], tail_valid);
+            }
+            if (bi < cache_batches) {
+#pragma unroll
+                for (int j = 0; j < U; ++j)
+                    row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
             }
             uint32_t mx2 = kBf16NegInfPair;
 #pragma unroll
@@ -163,15 +173,25 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
             const int32_t y = __float_as_int(row_scalars[3]);
             const int yv = y >= 0 ? (y >> 3) : -1;
             uint16_t *drow = p.dlogits + row * p.ld;
-            for (int bi = 0; bi < n_batch; ++bi) {
-                // newest lines first: the end of the row is the part most likely still in L2
-                const int base = threadIdx.x + ((p.flags & 1) ? (n_batch - 1 - bi) : bi) * NT * U;
+            const int n_global = n_batch - cache_batches;
+            for (int q = 0; q < n_batch; ++q) {
+                // batches not cached in shared memory first, newest first (the end of the
+                // row is the part most likely still in L2), then the cached head of the row
+                const int bi = q < n_global ? ((p.flags & 1) ? n_batch - 1 - q : cache_batches + q)
+                                            : q - n_global;
+                const int base = threadIdx.x + bi * NT * U;
                 uint4 x[U];
+                if (bi < cache_batches) {
 #pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int vi = base + j * NT;
-                    x[j] = (vi < n_vec && sc != 0.0f) ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream)
-                                                      : make_uint4(0u, 0u, 0u, 0u);
+                    for (int j = 0; j < U; ++j) x[j] = row_cache[(bi * U + j) * NT + threadIdx.x];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int vi = base + j * NT;
+                        x[j] = (vi < n_vec && sc != 0.0f)
+                                   ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream)
+                                   : make_uint4(0u, 0u, 0u, 0u);
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
@@ -232,14 +252,28 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cud
     if (blocks > a.n_rows) blocks = a.n_rows;
     const int U = (tune && tune->stages > 0) ? tune->stages : 4;
     int nt = 0;
-#define GRPO_RW(NT_, U_)                                                        \
-    if (nt == 0 && cps_nt == NT_ && U == U_) {                                  \
-        nt = NT_;                                                               \
-        rowwise_kernel<NT_, U_><<<(unsigned)blocks, NT_, 0, s>>>(p);            \
+#define GRPO_RW(NT_, U_)                                                                   \
+    if (nt == 0 && cps_nt == NT_ && U == U_) {                                             \
+        nt = NT_;                                                                          \
+        const size_t batch_bytes = (size_t)NT_ * U_ * 16;                                  \
+        const size_t avail = (size_t)(227 * 1024) / cps - 4096;                            \
+        const int rc = tune ? tune->row_cache : 0;                                         \
+        int cb = rc > 0 ? rc : (rc == 0 ? (int)(avail / batch_bytes) : 0);                \
+        const int nb = (n_vec + NT_ * U_ - 1) / (NT_ * U_);                                \
+        if (cb > nb) cb = nb;                                                              \
+        if ((size_t)cb * batch_bytes > avail) return cudaErrorInvalidConfiguration;        \
+        p.cache_batches = cb;                                                              \
+        smem = (size_t)cb * batch_bytes;                                                   \
+        auto kern = rowwise_kernel<NT_, U_>;                                               \
+        cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                              (int)smem);                                  \
+        if (ea != cudaSuccess) return ea;                                                  \
+        kern<<<(unsigned)blocks, NT_, smem, s>>>(p);                                       \
     }
+    size_t smem = 0;
     const int cps_nt = cps == 1 ? 1024 : (cps == 2 ? 512 : (cps == 3 ? 384 : 256));
-    GRPO_RW(1024, 4) GRPO_RW(1024, 8)
-    GRPO_RW(512, 4) GRPO_RW(512, 8) GRPO_RW(512, 16)
+    GRPO_RW(1024, 2) GRPO_RW(1024, 4) GRPO_RW(1024, 8)
+    GRPO_RW(512, 2) GRPO_RW(512, 4) GRPO_RW(512, 8) GRPO_RW(512, 16)
     GRPO_RW(384, 4) GRPO_RW(384, 8) GRPO_RW(384, 16)
     GRPO_RW(256, 4) GRPO_RW(256, 8) GRPO_RW(256, 16)
 #undef GRPO_RW
@@ -250,6 +284,8 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cud
         plan->ctas_per_sm = cps;
         plan->grid = (int32_t)blocks;
         plan->vec_per_thread = nt;
+        plan->stages = p.cache_batches;
+        plan->smem_bytes = (int32_t)smem;
     }
     *launches += 1;
     return cudaGetLastError();

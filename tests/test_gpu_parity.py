@@ -11,8 +11,10 @@ from tests.gpu_util import compare, run_gpu, run_oracle, to_dev_bits
 pytestmark = pytest.mark.gpu
 
 KERNELS = [{"kernel": 1}, {"kernel": 2}]
-ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u}
-                 for c, u in ((1, 4), (1, 8), (2, 4), (2, 8), (2, 16), (3, 4), (4, 16), (8, 4))]
+ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u, "row_cache": rc}
+                 for c, u, rc in ((1, 4, -1), (1, 2, 0), (1, 8, 1), (2, 4, -1), (2, 4, 0), (2, 8, 1),
+                                  (2, 16, -1), (2, 2, 0), (3, 4, 2), (3, 8, 0), (4, 16, 0),
+                                  (8, 4, -1), (8, 4, 0))]
 
 
 def _case(name, seed, **kw):
@@ -61,7 +63,8 @@ def test_cluster_sizes(dev, C):
         assert ran > 0
 
 
-@pytest.mark.parametrize("plan", ROWWISE_PLANS, ids=lambda d: f"cps{d['ctas_per_sm']}u{d['stages']}")
+@pytest.mark.parametrize("plan", ROWWISE_PLANS,
+                         ids=lambda d: f"cps{d['ctas_per_sm']}u{d['stages']}c{d['row_cache']}")
 def test_rowwise_plans(dev, plan):
     """Every row-wise kernel instantiation (threads x vectors in flight) matches the oracle."""
     for name in ("ragged", "mid152k"):
