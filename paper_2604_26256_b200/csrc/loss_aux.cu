@@ -71,68 +71,105 @@ struct RowwiseParams {
     int32_t cache_batches;  // leading batches of NT*U vectors kept in shared memory
 };
 
+template <int NT, int U>
+struct RowwiseBatch {
+    // log2-domain partial of U vectors (already loaded and masked)
+    static __device__ __forceinline__ void reduce(const uint4 (&x)[U], float &a, float &s) {
+        uint32_t mx2 = kBf16NegInfPair;
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+            mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
+        const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
+        if (va == -INFINITY) return;
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            t0 += ex2(fmaf(bf_lo(x[j].x), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].x), kLog2e, -va));
+            t1 += ex2(fmaf(bf_lo(x[j].y), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].y), kLog2e, -va));
+            t2 += ex2(fmaf(bf_lo(x[j].z), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].z), kLog2e, -va));
+            t3 += ex2(fmaf(bf_lo(x[j].w), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].w), kLog2e, -va));
+        }
+        lse2_merge(a, s, va, (t0 + t1) + (t2 + t3));
+    }
+    // s * 2^(z*log2e - lse2) for the 8 elements of one vector, packed to bf16
+    static __device__ __forceinline__ uint4 grad(const uint4 &x, float sc, float lse2) {
+        uint4 d;
+        d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.x), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.x), kLog2e, -lse2)));
+        d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.y), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.y), kLog2e, -lse2)));
+        d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.z), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.z), kLog2e, -lse2)));
+        d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.w), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.w), kLog2e, -lse2)));
+        return d;
+    }
+};
+
 // One CTA per row at a time (persistent, grid-stride over rows).  Pass 1 streams
 // the row from HBM in batches of U vectors per thread (U x 16 B in flight per
 // thread) with an L2 evict_last policy and reduces it to a log2-domain
-// (max, sum) pair; pass 2 re-reads the row -- from L2 when few enough rows are
-// in flight -- and writes dlogits with streaming stores.  Optionally the CTA
-// asks the TMA engine to prefetch its next row into L2 while it works on the
-// current one (cp.async.bulk.prefetch.L2).
+// (max, sum) pair; the first cache_batches batches are also kept in shared
+// memory.  Pass 2 writes dlogits with streaming 128-bit stores: the batches not
+// in shared memory are re-read newest-first (the end of the row is the part most
+// likely still in L2), then the cached head of the row.  Full batches run
+// without bounds checks; only the row's last (partial) batch carries them and
+// the ragged-tail masking.  Optionally the CTA asks the TMA engine to prefetch
+// its next row into L2 (cp.async.bulk.prefetch.L2).
 template <int NT, int U>
 __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
+    using B = RowwiseBatch<NT, U>;
     constexpr int NW = NT / 32;
+    constexpr int BV = NT * U;  // vectors per batch
     __shared__ float2 red[NW];
     __shared__ float row_scalars[4];  // lse2 (log2 domain), s, zy, y
+    extern __shared__ uint4 row_cache[];  // [cache_batches][U][NT]
     const int n_vec = (p.V + 7) / 8;
     const int tail_valid = p.V - (n_vec - 1) * 8;
     const int tail_vi = tail_valid < 8 ? n_vec - 1 : -1;
+    const int n_batch = (n_vec + BV - 1) / BV;
+    // full batches run unchecked; the batch holding the ragged tail vector (if any) and a
+    // short last batch take the checked path
+    const int n_full = tail_vi >= 0 ? tail_vi / BV : n_vec / BV;
+    const int cache_batches = min(p.cache_batches, n_batch);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t pol_keep = (p.flags & 2) ? policy_evict_normal() : policy_evict_last();
+    const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     const uint32_t row_bytes = (uint32_t)n_vec * 16u;
-    const int n_batch = (n_vec + NT * U - 1) / (NT * U);
-    extern __shared__ uint4 row_cache[];  // [cache_batches][U][NT]
-    const int cache_batches = min(p.cache_batches, n_batch);
+    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
+                                     kBf16NegInfPair);
     if (p.prefetch && threadIdx.x == 0 && blockIdx.x < p.n_rows)
         bulk_prefetch_l2(p.logits + (int64_t)blockIdx.x * p.ld, row_bytes);
     for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
         const uint16_t *zrow = p.logits + row * p.ld;
         if (p.prefetch && threadIdx.x == 0 && row + gridDim.x < p.n_rows)
             bulk_prefetch_l2(zrow + (int64_t)gridDim.x * p.ld, row_bytes);
-        // ---- pass 1: log2-domain (max, sum exp) of the row; the first cache_batches
-        //      batches are also kept in shared memory for pass 2
+        // ---- pass 1
         float a = -INFINITY, s = 0.0f;
-        for (int bi = 0; bi < n_batch; ++bi) {
-            const int base = threadIdx.x + bi * NT * U;
+        for (int bi = 0; bi < n_full; ++bi) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + bi * BV + threadIdx.x;
+            uint4 x[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) x[j] = ldg_policy(src + j * NT, pol_keep);
+            if (bi < cache_batches) {
+#pragma unroll
+                for (int j = 0; j < U; ++j) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
+            }
+            B::reduce(x, a, s);
+        }
+        for (int bi = n_full; bi < n_batch; ++bi) {  // the checked last batch
             uint4 x[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-                const int vi = base + j * NT;
-                x[j] = vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_keep)
-                                  : make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
-                                               kBf16NegInfPair);
+                const int vi = bi * BV + j * NT + threadIdx.x;
+                x[j] = vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_keep) : neg_inf;
                 if (vi == tail_vi) x[j] = mask_tail(x[j], tail_valid);
             }
             if (bi < cache_batches) {
 #pragma unroll
-                for (int j = 0; j < U; ++j)
-                    row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
+                for (int j = 0; j < U; ++j) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
             }
-            uint32_t mx2 = kBf16NegInfPair;
-#pragma unroll
-            for (int j = 0; j < U; ++j)
-                mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
-            const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
-            if (va == -INFINITY) continue;
-            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                t0 += ex2(fmaf(bf_lo(x[j].x), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].x), kLog2e, -va));
-                t1 += ex2(fmaf(bf_lo(x[j].y), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].y), kLog2e, -va));
-                t2 += ex2(fmaf(bf_lo(x[j].z), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].z), kLog2e, -va));
-                t3 += ex2(fmaf(bf_lo(x[j].w), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].w), kLog2e, -va));
-            }
-            lse2_merge(a, s, va, (t0 + t1) + (t2 + t3));
+            B::reduce(x, a, s);
         }
         warp_lse2_combine(a, s);
         if (lane == 0) red[warp] = make_float2(a, s);
@@ -173,53 +210,57 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
             const int32_t y = __float_as_int(row_scalars[3]);
             const int yv = y >= 0 ? (y >> 3) : -1;
             uint16_t *drow = p.dlogits + row * p.ld;
-            const int n_global = n_batch - cache_batches;
-            for (int q = 0; q < n_batch; ++q) {
-                // batches not cached in shared memory first, newest first (the end of the
-                // row is the part most likely still in L2), then the cached head of the row
-                const int bi = q < n_global ? ((p.flags & 1) ? n_batch - 1 - q : cache_batches + q)
-                                            : q - n_global;
-                const int base = threadIdx.x + bi * NT * U;
-                uint4 x[U];
-                if (bi < cache_batches) {
-#pragma unroll
-                    for (int j = 0; j < U; ++j) x[j] = row_cache[(bi * U + j) * NT + threadIdx.x];
-                } else {
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const int vi = base + j * NT;
-                        x[j] = (vi < n_vec && sc != 0.0f)
-                                   ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream)
-                                   : make_uint4(0u, 0u, 0u, 0u);
-                    }
+            uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
+            if (sc == 0.0f) {
+                // clipped token or zero advantage: the row of dlogits is exactly zero
+                const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+                for (int vi = threadIdx.x; vi < n_vec; vi += NT) {
+                    if (vi == tail_vi) store_tail(drow + (int64_t)vi * 8, z4, tail_valid);
+                    else stg_stream(dst4 + vi, z4);
                 }
+            } else {
+                const int n_global = n_batch - cache_batches;
+                for (int q = 0; q < n_batch; ++q) {
+                    const int bi = q < n_global ? n_batch - 1 - q : q - n_global;
+                    const int v0 = bi * BV + threadIdx.x;
+                    uint4 x[U];
+                    if (bi < cache_batches) {
 #pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int vi = base + j * NT;
-                    if (vi >= n_vec) break;
-                    uint4 d = make_uint4(0u, 0u, 0u, 0u);
-                    if (sc != 0.0f) {
-                        d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].x), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x[j].x), kLog2e, -lse2)));
-                        d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].y), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x[j].y), kLog2e, -lse2)));
-                        d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].z), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x[j].z), kLog2e, -lse2)));
-                        d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x[j].w), kLog2e, -lse2)),
-                                          sc * ex2(fmaf(bf_hi(x[j].w), kLog2e, -lse2)));
+                        for (int j = 0; j < U; ++j) x[j] = row_cache[(bi * U + j) * NT + threadIdx.x];
+                    } else if (bi < n_full) {
+                        const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + v0;
+#pragma unroll
+                        for (int j = 0; j < U; ++j) x[j] = ldg_policy(src + j * NT, pol_stream);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < U; ++j) {
+                            const int vi = v0 + j * NT;
+                            x[j] = vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream) : neg_inf;
+                        }
                     }
-                    if (vi == tail_vi)
-                        store_tail(drow + (int64_t)vi * 8, d, tail_valid);
-                    else
-                        stg_stream(drow + (int64_t)vi * 8, d);
-                    if (vi == yv) {
-                        const float py = ex2(fmaf(zy, kLog2e, -lse2));
-                        drow[y] = f2bf(sc * (py - 1.0f));
+                    if (bi < n_full) {
+#pragma unroll
+                        for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad(x[j], sc, lse2));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < U; ++j) {
+                            const int vi = v0 + j * NT;
+                            if (vi >= n_vec) break;
+                            const uint4 d = B::grad(x[j], sc, lse2);
+                            if (vi == tail_vi) store_tail(drow + (int64_t)vi * 8, d, tail_valid);
+                            else stg_stream(dst4 + vi, d);
+                        }
                     }
                 }
             }
+            // the target entry: s (p_y - 1) from the unrounded probability (same thread
+            // as the vector store that covered it when sc != 0 -- program order keeps it last)
+            if (sc != 0.0f && yv >= 0 && (yv % NT) == (int)threadIdx.x) {
+                const float py = ex2(fmaf(zy, kLog2e, -lse2));
+                drow[y] = f2bf(sc * (py - 1.0f));
+            }
         }
-        __syncthreads();  // row_scalars / red reused by the next row
+        __syncthreads();  // row_scalars / red / row_cache reused by the next row
     }
 }
 
@@ -250,7 +291,7 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cud
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     int64_t blocks = (int64_t)n_sm * cps;
     if (blocks > a.n_rows) blocks = a.n_rows;
-    const int U = (tune && tune->stages > 0) ? tune->stages : 4;
+    const int U = (tune && tune->stages > 0) ? tune->stages : (cps <= 2 ? 8 : 4);
     int nt = 0;
 #define GRPO_RW(NT_, U_)                                                                   \
     if (nt == 0 && cps_nt == NT_ && U == U_) {                                             \
@@ -434,7 +475,7 @@ __global__ void __launch_bounds__(256)
             } else {
                 stg_stream(drow + (int64_t)vi * 8, d);
             }
-            if (y_mine && yv == vi) drow[y] = f2bf(sc * (ex2(fmaf(zy, kLog2e, -off)) - 1.0f));
+            if (y_mine && yv == vi && sc != 0.0f) drow[y] = f2bf(sc * (ex2(fmaf(zy, kLog2e, -off)) - 1.0f));
         }
     }
 }
