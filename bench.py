@@ -70,13 +70,14 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self):
+    def __init__(self, gpus):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         self.p = None
+        self.gpus = ",".join(str(g) for g in gpus)
 
     def start(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}",
+            self.p = subprocess.Popen(["nvidia-smi", "-i", self.gpus, f"--query-gpu={self.FIELDS}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
@@ -299,7 +300,12 @@ def main():
     barrier()
 
     # ---- timed region (device-resident inputs)
-    sampler = ClockSampler() if rank == 0 else None
+    # the GPUs of this node's ranks (CUDA_VISIBLE_DEVICES, if set, maps them)
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    node_gpus = list(range(int(os.environ.get("LOCAL_WORLD_SIZE", world))))
+    if vis:
+        node_gpus = [vis.split(",")[g] for g in node_gpus]
+    sampler = ClockSampler(node_gpus) if rank == 0 else None
     if sampler:
         sampler.start()
         time.sleep(0.3)
