@@ -100,8 +100,8 @@ typedef struct {
     int32_t lag;           /* 0 auto, else 1..2: rows between a row's reduction and its       */
                            /* backward, hiding the cluster exchange (kernel 1)               */
     int32_t prefetch;      /* kernel 2: 1 = TMA-prefetch each CTA's next row into L2         */
-    int32_t row_cache;     /* kernel 2: leading batches of each row kept in shared memory for */
-                           /* the second pass (0 auto = as many as fit, -1 none, n > 0 n)    */
+    int32_t row_cache;     /* kernel 2: leading vectors per thread of each row kept in shared */
+                           /* memory for the second pass (0 auto = 160 KB per SM, -1 none) */
 } grpo_tune_t;
 
 /*

@@ -68,7 +68,7 @@ struct RowwiseParams {
     uint8_t *flag_ws;
     int32_t prefetch;
     int32_t flags;  // bit 0: pass 2 in reverse batch order; bit 1: pass-1 policy evict_normal
-    int32_t cache_batches;  // leading batches of NT*U vectors kept in shared memory
+    int32_t cache_vecs;  // leading vectors per thread kept in shared memory for pass 2
 };
 
 template <int NT, int U>
@@ -106,44 +106,50 @@ struct RowwiseBatch {
     }
 };
 
-// One CTA per row at a time (persistent, grid-stride over rows).  Pass 1 streams
-// the row from HBM in batches of U vectors per thread (U x 16 B in flight per
-// thread) with an L2 evict_last policy and reduces it to a log2-domain
-// (max, sum) pair; the first cache_batches batches are also kept in shared
-// memory.  Pass 2 writes dlogits with streaming 128-bit stores: the batches not
-// in shared memory are re-read newest-first (the end of the row is the part most
-// likely still in L2), then the cached head of the row.  Full batches run
-// without bounds checks; only the row's last (partial) batch carries them and
-// the ragged-tail masking.  Optionally the CTA asks the TMA engine to prefetch
-// its next row into L2 (cp.async.bulk.prefetch.L2).
-template <int NT, int U>
-__global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
+// Row-wise two-pass kernel.  A row (or, with C > 1, a 1/C slice of it held by one
+// CTA of a C-CTA cluster) is processed by one CTA at a time; the grid is
+// persistent and strides over rows.  Pass 1 streams the slice from HBM in
+// batches of U vectors per thread (U x 16 B in flight per thread, L2
+// evict_last) and reduces it to a log2-domain (max, sum) pair; the first
+// cache_vecs vectors of every thread are also kept in shared memory.  With
+// C > 1 the CTAs of the cluster swap their 16-byte partials through DSMEM
+// around one cluster barrier.  Pass 2 writes dlogits with streaming 128-bit
+// stores: the vectors not in shared memory are re-read newest-first (the end of
+// the slice is the part most likely still in L2), the cached head comes from
+// shared memory.  Full batches run without bounds checks; only the slice's
+// last batch carries them and the ragged-tail masking.
+template <int NT, int U, int C>
+__global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kernel(const RowwiseParams p) {
     using B = RowwiseBatch<NT, U>;
     constexpr int NW = NT / 32;
     constexpr int BV = NT * U;  // vectors per batch
     __shared__ float2 red[NW];
-    __shared__ float row_scalars[4];  // lse2 (log2 domain), s, zy, y
-    extern __shared__ uint4 row_cache[];  // [cache_batches][U][NT]
-    const int n_vec = (p.V + 7) / 8;
-    const int tail_valid = p.V - (n_vec - 1) * 8;
-    const int tail_vi = tail_valid < 8 ? n_vec - 1 : -1;
+    __shared__ float row_scalars[4];          // lse2 (log2 domain), s, zy, y
+    __shared__ float4 xpart[2][C];            // cluster exchange, double-buffered by row parity
+    extern __shared__ uint4 row_cache[];      // [cache_vecs][NT]
+    const uint32_t crank = C > 1 ? cluster_ctarank() : 0;
+    const int64_t grp = C > 1 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
+    const int64_t n_grp = C > 1 ? (int64_t)ncluster_x() : (int64_t)gridDim.x;
+    const int n_vec_row = (p.V + 7) / 8;
+    const int slice = (n_vec_row + C - 1) / C;
+    const int vec_lo = min((int)crank * slice, n_vec_row);
+    const int n_vec = min(slice, n_vec_row - vec_lo);       // vectors of this CTA's slice
+    const int tail_valid = p.V - (n_vec_row - 1) * 8;
+    const int tail_vi = (tail_valid < 8 && n_vec_row - 1 >= vec_lo && n_vec_row - 1 < vec_lo + n_vec)
+                            ? n_vec_row - 1 - vec_lo : -1;  // slice-local index of the ragged vector
     const int n_batch = (n_vec + BV - 1) / BV;
     // full batches run unchecked; the batch holding the ragged tail vector (if any) and a
     // short last batch take the checked path
     const int n_full = tail_vi >= 0 ? tail_vi / BV : n_vec / BV;
-    const int cache_batches = min(p.cache_batches, n_batch);
+    const int cache_vecs = min(p.cache_vecs, n_batch * U);  // per thread
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
-    const uint32_t row_bytes = (uint32_t)n_vec * 16u;
     const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
                                      kBf16NegInfPair);
-    if (p.prefetch && threadIdx.x == 0 && blockIdx.x < p.n_rows)
-        bulk_prefetch_l2(p.logits + (int64_t)blockIdx.x * p.ld, row_bytes);
-    for (int64_t row = blockIdx.x; row < p.n_rows; row += gridDim.x) {
-        const uint16_t *zrow = p.logits + row * p.ld;
-        if (p.prefetch && threadIdx.x == 0 && row + gridDim.x < p.n_rows)
-            bulk_prefetch_l2(zrow + (int64_t)gridDim.x * p.ld, row_bytes);
+    int parity = 0;
+    for (int64_t row = grp; row < p.n_rows; row += n_grp, parity ^= 1) {
+        const uint16_t *zrow = p.logits + row * p.ld + (int64_t)vec_lo * 8;
         // ---- pass 1
         float a = -INFINITY, s = 0.0f;
         for (int bi = 0; bi < n_full; ++bi) {
@@ -151,10 +157,9 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
             uint4 x[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) x[j] = ldg_policy(src + j * NT, pol_keep);
-            if (bi < cache_batches) {
 #pragma unroll
-                for (int j = 0; j < U; ++j) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
-            }
+            for (int j = 0; j < U; ++j)
+                if (bi * U + j < cache_vecs) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
             B::reduce(x, a, s);
         }
         for (int bi = n_full; bi < n_batch; ++bi) {  // the checked last batch
@@ -165,10 +170,9 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
                 x[j] = vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_keep) : neg_inf;
                 if (vi == tail_vi) x[j] = mask_tail(x[j], tail_valid);
             }
-            if (bi < cache_batches) {
 #pragma unroll
-                for (int j = 0; j < U; ++j) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
-            }
+            for (int j = 0; j < U; ++j)
+                if (bi * U + j < cache_vecs) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
             B::reduce(x, a, s);
         }
         warp_lse2_combine(a, s);
@@ -181,14 +185,26 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
                 cs = red[lane].y;
             }
             warp_lse2_combine(cm, cs);
-            if (lane == 0) {
-                const RowInfo ri = p.rowinfo[row];
-                const bool y_valid = ri.target >= 0 && ri.target < p.V;
-                const float zy = y_valid ? __uint_as_float(((uint32_t)zrow[ri.target]) << 16)
-                                         : __int_as_float(0x7FC00000);
+            const RowInfo ri = p.rowinfo[row];  // broadcast load
+            const bool y_valid = ri.target >= 0 && ri.target < p.V;
+            const int y_loc = ri.target - vec_lo * 8;
+            const bool mine = y_valid && y_loc >= 0 && y_loc < n_vec * 8;
+            float zy = mine ? __uint_as_float(((uint32_t)zrow[y_loc]) << 16) : 0.0f;
+            if (C > 1) {
+                // every CTA of the cluster gets this CTA's partial (and z_y if it owns y)
+                if (lane < C) {
+                    const float4 msg = make_float4(cm, cs, zy, mine ? 1.0f : 0.0f);
+                    const uint32_t raddr = mapa_shared(smem_u32(&xpart[parity][crank]), lane);
+                    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(raddr),
+                                 "f"(msg.x), "f"(msg.y), "f"(msg.z), "f"(msg.w)
+                                 : "memory");
+                }
+            }
+            if (C == 1 && lane == 0) {
                 const float l2s = log2f(cs);
                 const float lse2 = cm + l2s;
-                const double logp_d = row_logp(zy, cm, l2s);
+                const float zyv = y_valid ? zy : __int_as_float(0x7FC00000);
+                const double logp_d = row_logp(zyv, cm, l2s);
                 const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
                 const float logp = (float)logp_d;
                 if (p.logp_out) p.logp_out[row] = logp;
@@ -199,8 +215,47 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
                 p.flag_ws[row] = o.flags;
                 row_scalars[0] = lse2;
                 row_scalars[1] = o.s;
-                row_scalars[2] = zy;
+                row_scalars[2] = zyv;
                 row_scalars[3] = __int_as_float(y_valid ? ri.target : -1);
+            }
+        }
+        if (C > 1) {
+            cluster_sync_all();  // the partials of every CTA of the cluster have landed
+            if (warp == 0) {
+                float M = -INFINITY, S = 0.0f, zsrc = 0.0f;
+                bool own = false;
+                if (lane < C) {
+                    const float4 m4 = xpart[parity][lane];
+                    M = m4.x;
+                    S = m4.y;
+                    zsrc = m4.z;
+                    own = m4.w != 0.0f;
+                }
+                warp_lse2_combine(M, S);    // identical bits in every CTA of the cluster
+                const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
+                const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
+                if (lane == 0) {
+                    const RowInfo ri = p.rowinfo[row];
+                    const bool y_valid = own_mask != 0u;
+                    const float zyv = y_valid ? zsh : __int_as_float(0x7FC00000);
+                    const float l2s = log2f(S);
+                    const float lse2 = M + l2s;
+                    const double logp_d = row_logp(zyv, M, l2s);
+                    const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
+                    if (crank == 0) {
+                        const float logp = (float)logp_d;
+                        if (p.logp_out) p.logp_out[row] = logp;
+                        if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
+                        if (p.scale_out) p.scale_out[row] = o.s;
+                        p.term_ws[row] = o.term;
+                        p.logp_ws[row] = logp;
+                        p.flag_ws[row] = o.flags;
+                    }
+                    row_scalars[0] = lse2;
+                    row_scalars[1] = o.s;
+                    row_scalars[2] = zyv;
+                    row_scalars[3] = __int_as_float(y_valid ? ri.target : -1);
+                }
             }
         }
         __syncthreads();
@@ -208,8 +263,9 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
         if (p.dlogits) {
             const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
             const int32_t y = __float_as_int(row_scalars[3]);
-            const int yv = y >= 0 ? (y >> 3) : -1;
-            uint16_t *drow = p.dlogits + row * p.ld;
+            const int y_loc = y >= 0 ? y - vec_lo * 8 : -1;
+            const int yv = (y_loc >= 0 && y_loc < n_vec * 8) ? (y_loc >> 3) : -1;
+            uint16_t *drow = p.dlogits + row * p.ld + (int64_t)vec_lo * 8;
             uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
             if (sc == 0.0f) {
                 // clipped token or zero advantage: the row of dlogits is exactly zero
@@ -219,29 +275,27 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
                     else stg_stream(dst4 + vi, z4);
                 }
             } else {
-                const int n_global = n_batch - cache_batches;
+                // batches newest first: the end of the slice is the part most likely still in
+                // L2; the head of the slice comes from shared memory (cache_vecs per thread)
                 for (int q = 0; q < n_batch; ++q) {
-                    const int bi = q < n_global ? n_batch - 1 - q : q - n_global;
+                    const int bi = n_batch - 1 - q;
                     const int v0 = bi * BV + threadIdx.x;
                     uint4 x[U];
-                    if (bi < cache_batches) {
-#pragma unroll
-                        for (int j = 0; j < U; ++j) x[j] = row_cache[(bi * U + j) * NT + threadIdx.x];
-                    } else if (bi < n_full) {
+                    if (bi < n_full) {
                         const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + v0;
 #pragma unroll
-                        for (int j = 0; j < U; ++j) x[j] = ldg_policy(src + j * NT, pol_stream);
+                        for (int j = 0; j < U; ++j)
+                            x[j] = (bi * U + j < cache_vecs) ? row_cache[(bi * U + j) * NT + threadIdx.x]
+                                                             : ldg_policy(src + j * NT, pol_stream);
+#pragma unroll
+                        for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad(x[j], sc, lse2));
                     } else {
 #pragma unroll
                         for (int j = 0; j < U; ++j) {
                             const int vi = v0 + j * NT;
-                            x[j] = vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream) : neg_inf;
+                            x[j] = (bi * U + j < cache_vecs) ? row_cache[(bi * U + j) * NT + threadIdx.x]
+                                   : (vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream) : neg_inf);
                         }
-                    }
-                    if (bi < n_full) {
-#pragma unroll
-                        for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad(x[j], sc, lse2));
-                    } else {
 #pragma unroll
                         for (int j = 0; j < U; ++j) {
                             const int vi = v0 + j * NT;
@@ -252,16 +306,17 @@ __global__ void __launch_bounds__(NT) rowwise_kernel(const RowwiseParams p) {
                         }
                     }
                 }
-            }
-            // the target entry: s (p_y - 1) from the unrounded probability (same thread
-            // as the vector store that covered it when sc != 0 -- program order keeps it last)
-            if (sc != 0.0f && yv >= 0 && (yv % NT) == (int)threadIdx.x) {
-                const float py = ex2(fmaf(zy, kLog2e, -lse2));
-                drow[y] = f2bf(sc * (py - 1.0f));
+                // the target entry: s (p_y - 1) from the unrounded probability, by the thread
+                // whose vector store covered it (program order keeps this store last)
+                if (yv >= 0 && (yv % NT) == (int)threadIdx.x) {
+                    const float py = ex2(fmaf(zy, kLog2e, -lse2));
+                    drow[y_loc] = f2bf(sc * (py - 1.0f));
+                }
             }
         }
         __syncthreads();  // row_scalars / red / row_cache reused by the next row
     }
+    if (C > 1) cluster_sync_all();  // no CTA leaves while a peer may still address its smem
 }
 
 cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
@@ -289,43 +344,68 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cud
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    int64_t blocks = (int64_t)n_sm * cps;
-    if (blocks > a.n_rows) blocks = a.n_rows;
+    int64_t blocks = 0;
     const int U = (tune && tune->stages > 0) ? tune->stages : (cps <= 2 ? 8 : 4);
     int nt = 0;
-#define GRPO_RW(NT_, U_)                                                                   \
-    if (nt == 0 && cps_nt == NT_ && U == U_) {                                             \
+#define GRPO_RW(NT_, U_, C_)                                                               \
+    if (nt == 0 && cps_nt == NT_ && U == U_ && Cl == C_) {                                 \
         nt = NT_;                                                                          \
-        const size_t batch_bytes = (size_t)NT_ * U_ * 16;                                  \
+        const size_t vec_bytes = (size_t)NT_ * 16;                                         \
         const size_t avail = (size_t)(227 * 1024) / cps - 4096;                            \
         const int rc = tune ? tune->row_cache : 0;                                         \
-        int cb = rc > 0 ? rc : (rc == 0 ? (int)(avail / batch_bytes) : 0);                \
-        const int nb = (n_vec + NT_ * U_ - 1) / (NT_ * U_);                                \
-        if (cb > nb) cb = nb;                                                              \
-        if ((size_t)cb * batch_bytes > avail) return cudaErrorInvalidConfiguration;        \
-        p.cache_batches = cb;                                                              \
-        smem = (size_t)cb * batch_bytes;                                                   \
-        auto kern = rowwise_kernel<NT_, U_>;                                               \
+        /* auto: 160 KB of cache per SM; the rest of the 256 KB L1/smem stays L1, which  \
+           stages the in-flight loads (more cache starves them: measured cliff)  */       \
+        const size_t auto_bytes = (size_t)(160 * 1024) / cps;                              \
+        int cv = rc > 0 ? rc : (rc == 0 ? (int)(auto_bytes / vec_bytes) : 0);             \
+        const int nv = ((n_vec + C_ - 1) / C_ + NT_ - 1) / NT_;                            \
+        if (cv > nv) cv = nv;                                                              \
+        if ((size_t)cv * vec_bytes > avail) return cudaErrorInvalidConfiguration;          \
+        p.cache_vecs = cv;                                                                 \
+        smem = (size_t)cv * vec_bytes;                                                     \
+        auto kern = rowwise_kernel<NT_, U_, C_>;                                           \
         cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                               (int)smem);                                  \
         if (ea != cudaSuccess) return ea;                                                  \
-        kern<<<(unsigned)blocks, NT_, smem, s>>>(p);                                       \
+        cudaLaunchConfig_t cfg = {};                                                       \
+        cudaLaunchAttribute attr[1];                                                       \
+        attr[0].id = cudaLaunchAttributeClusterDimension;                                  \
+        attr[0].val.clusterDim.x = C_;                                                     \
+        attr[0].val.clusterDim.y = 1;                                                      \
+        attr[0].val.clusterDim.z = 1;                                                      \
+        cfg.blockDim = dim3(NT_);                                                          \
+        cfg.dynamicSmemBytes = smem;                                                       \
+        cfg.stream = s;                                                                    \
+        cfg.attrs = attr;                                                                  \
+        cfg.numAttrs = 1;                                                                  \
+        int64_t groups = (int64_t)n_sm * cps / C_;                                         \
+        if (groups > a.n_rows) groups = a.n_rows;                                          \
+        blocks = groups * C_;                                                              \
+        cfg.gridDim = dim3((unsigned)blocks);                                              \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT_, smem);              \
+        ea = cudaLaunchKernelEx(&cfg, kern, p);                                            \
+        if (ea != cudaSuccess) return ea;                                                  \
     }
     size_t smem = 0;
+    int occ = 0;
     const int cps_nt = cps == 1 ? 1024 : (cps == 2 ? 512 : (cps == 3 ? 384 : 256));
-    GRPO_RW(1024, 2) GRPO_RW(1024, 4) GRPO_RW(1024, 8)
-    GRPO_RW(512, 2) GRPO_RW(512, 4) GRPO_RW(512, 8) GRPO_RW(512, 16)
-    GRPO_RW(384, 4) GRPO_RW(384, 8) GRPO_RW(384, 16)
-    GRPO_RW(256, 4) GRPO_RW(256, 8) GRPO_RW(256, 16)
+    const int Cl = (tune && tune->cluster_size > 0) ? tune->cluster_size : 1;
+    GRPO_RW(1024, 2, 1) GRPO_RW(1024, 4, 1) GRPO_RW(1024, 8, 1)
+    GRPO_RW(512, 2, 1) GRPO_RW(512, 4, 1) GRPO_RW(512, 8, 1)
+    GRPO_RW(384, 4, 1) GRPO_RW(384, 8, 1)
+    GRPO_RW(256, 4, 1) GRPO_RW(256, 8, 1)
+    GRPO_RW(1024, 4, 2) GRPO_RW(512, 8, 2) GRPO_RW(512, 4, 2) GRPO_RW(384, 8, 2)
+    GRPO_RW(256, 8, 2) GRPO_RW(512, 8, 4) GRPO_RW(512, 4, 4) GRPO_RW(256, 8, 4)
 #undef GRPO_RW
     if (nt == 0) return cudaErrorInvalidValue;
     if (plan) {
         *plan = grpo_plan_t{};
         plan->kernel = 2;
         plan->ctas_per_sm = cps;
+        plan->cluster_size = Cl;
         plan->grid = (int32_t)blocks;
         plan->vec_per_thread = nt;
-        plan->stages = p.cache_batches;
+        plan->stages = p.cache_vecs;
+        plan->max_clusters = occ;  // kernel 2: resident CTAs per SM the occupancy query allows
         plan->smem_bytes = (int32_t)smem;
     }
     *launches += 1;

@@ -11,10 +11,12 @@ from tests.gpu_util import compare, run_gpu, run_oracle, to_dev_bits
 pytestmark = pytest.mark.gpu
 
 KERNELS = [{"kernel": 1}, {"kernel": 2}]
-ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u, "row_cache": rc}
-                 for c, u, rc in ((1, 4, -1), (1, 2, 0), (1, 8, 1), (2, 4, -1), (2, 4, 0), (2, 8, 1),
-                                  (2, 16, -1), (2, 2, 0), (3, 4, 2), (3, 8, 0), (4, 16, 0),
-                                  (8, 4, -1), (8, 4, 0))]
+ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u, "row_cache": rc, "cluster_size": cl}
+                 for c, u, rc, cl in ((1, 4, -1, 1), (1, 2, 0, 1), (1, 8, 1, 1), (2, 4, -1, 1),
+                                      (2, 4, 0, 1), (2, 8, 1, 1), (2, 8, 0, 1), (2, 2, 0, 1),
+                                      (3, 4, 2, 1), (3, 8, 0, 1), (4, 8, 0, 1), (8, 4, -1, 1),
+                                      (8, 4, 0, 1), (2, 8, 0, 2), (1, 4, 0, 2), (4, 8, 0, 2),
+                                      (2, 8, 0, 4), (2, 4, 3, 4))]
 
 
 def _case(name, seed, **kw):
@@ -64,7 +66,8 @@ def test_cluster_sizes(dev, C):
 
 
 @pytest.mark.parametrize("plan", ROWWISE_PLANS,
-                         ids=lambda d: f"cps{d['ctas_per_sm']}u{d['stages']}c{d['row_cache']}")
+                         ids=lambda d: f"cps{d['ctas_per_sm']}u{d['stages']}c{d['row_cache']}"
+                                       f"C{d['cluster_size']}")
 def test_rowwise_plans(dev, plan):
     """Every row-wise kernel instantiation (threads x vectors in flight) matches the oracle."""
     for name in ("ragged", "mid152k"):
