@@ -69,8 +69,15 @@ def lib():
         _lib.oracle_rows.argtypes = [i64, P, i32, i64, P, P, P, i32, P, P, P, f32, f64,
                                      P, P, P, P, P, P, P]
         _lib.oracle_rows.restype = None
-        _lib.oracle_rows_f64.argtypes = [i64, P, i32, P, P, P, i32, P, P, P, f32, f64,
+        _lib.oracle_rows_f64.argtypes = [i64, P, i32, P, P, P, i32, P, P, P, f32, f32, f64,
                                          P, P, P, P, P, P, P]
+        _lib.oracle_rows2.argtypes = [i64, P, i32, i64, P, P, P, i32, P, P, P, f32, f32, f64,
+                                      P, P, P, P, P, P, P]
+        _lib.oracle_rows2.restype = None
+        _lib.oracle_token_asym.argtypes = [f64, f32, f64, f64, f32, f32, f64, P, P, P, P]
+        _lib.oracle_token_asym.restype = None
+        _lib.oracle_weights.argtypes = [i32, i32, P, P, P, i32, P, P]
+        _lib.oracle_weights.restype = None
         _lib.oracle_rows_f64.restype = None
         _lib.oracle_objective_tokens.argtypes = [i32, P, P, P, P]
         _lib.oracle_objective_tokens.restype = f64
@@ -132,12 +139,29 @@ def log_softmax_row(row_bf16_bits, y):
 
 
 # --------------------------------------------------------------------------- O4
-def token(logp, logp_behav, A, inv_norm, eps, grad_scale=1.0):
+def token(logp, logp_behav, A, inv_norm, eps, grad_scale=1.0, eps_hi=None):
     r, term, s = C.c_double(), C.c_double(), C.c_double()
     clipped = C.c_int32()
-    lib().oracle_token(float(logp), float(logp_behav), float(A), float(inv_norm), float(eps),
-                       float(grad_scale), C.byref(r), C.byref(term), C.byref(clipped), C.byref(s))
+    if eps_hi is None:
+        lib().oracle_token(float(logp), float(logp_behav), float(A), float(inv_norm), float(eps),
+                           float(grad_scale), C.byref(r), C.byref(term), C.byref(clipped),
+                           C.byref(s))
+    else:
+        lib().oracle_token_asym(float(logp), float(logp_behav), float(A), float(inv_norm),
+                                float(eps), float(eps_hi), float(grad_scale), C.byref(r),
+                                C.byref(term), C.byref(clipped), C.byref(s))
     return r.value, term.value, bool(clipped.value), s.value
+
+
+def weights(group_ids, cu_seqlens, group_count, P, norm=0, traj_mask=None):
+    """Token weights w_i under the sequence-mean (0) or token-mean (1) normalisation."""
+    g = _c(group_ids, np.int32)
+    cu = _c(cu_seqlens, np.int64)
+    gc = _c(group_count, np.int32)
+    m = _c(traj_mask, np.uint8)
+    w = np.zeros(len(g), np.float64)
+    lib().oracle_weights(len(g), P, _p(g), _p(cu), _p(gc), int(norm), _p(m), _p(w))
+    return w
 
 
 # --------------------------------------------------------------------------- O5
@@ -160,8 +184,9 @@ class RowsResult:
 
 
 def rows(row_ids, logits_bits, V, target_ids, logp_behav, cu_seqlens, adv, inv_norm,
-         eps, grad_scale=1.0, want_dlogits=True):
-    """O3-O5 on a set of global rows.  logits_bits: uint16 [n_rows, ld] (ld >= V)."""
+         eps, grad_scale=1.0, want_dlogits=True, eps_hi=None):
+    """O3-O5 on a set of global rows.  logits_bits: uint16 [n_rows, ld] (ld >= V).
+    eps is the lower clip range; eps_hi (default eps) the upper one."""
     row_ids = _c(row_ids, np.int64)
     lg = np.ascontiguousarray(logits_bits, dtype=np.uint16)
     n = len(row_ids)
@@ -174,8 +199,9 @@ def rows(row_ids, logits_bits, V, target_ids, logp_behav, cu_seqlens, adv, inv_n
     out = {k: np.zeros(n, np.float64) for k in ("lse", "logp", "r", "term", "s")}
     clipped = np.zeros(n, np.int32)
     dl = np.zeros((n, V), np.float64) if want_dlogits else None
-    lib().oracle_rows(n, _p(row_ids), V, ld, _p(lg), _p(tgt), _p(lw), len(adv), _p(cu),
-                      _p(adv), _p(inv), float(eps), float(grad_scale), _p(out["lse"]),
+    lib().oracle_rows2(n, _p(row_ids), V, ld, _p(lg), _p(tgt), _p(lw), len(adv), _p(cu),
+                       _p(adv), _p(inv), float(eps), float(eps if eps_hi is None else eps_hi),
+                       float(grad_scale), _p(out["lse"]),
                       _p(out["logp"]), _p(out["r"]), _p(out["term"]), _p(clipped),
                       _p(out["s"]), _p(dl))
     return RowsResult(out["lse"], out["logp"], out["r"], out["term"], clipped.astype(bool),
@@ -183,7 +209,7 @@ def rows(row_ids, logits_bits, V, target_ids, logp_behav, cu_seqlens, adv, inv_n
 
 
 def rows_f64(row_ids, logits_f64, target_ids, logp_behav, cu_seqlens, adv, inv_norm, eps,
-             grad_scale=1.0, want_dlogits=True):
+             grad_scale=1.0, want_dlogits=True, eps_hi=None):
     """O3-O5 on fp64 logits [n_rows, V] (finite-difference pins)."""
     row_ids = _c(row_ids, np.int64)
     lg = np.ascontiguousarray(logits_f64, dtype=np.float64)
@@ -197,7 +223,8 @@ def rows_f64(row_ids, logits_f64, target_ids, logp_behav, cu_seqlens, adv, inv_n
     clipped = np.zeros(n, np.int32)
     dl = np.zeros((n, V), np.float64) if want_dlogits else None
     lib().oracle_rows_f64(n, _p(row_ids), V, _p(lg), _p(tgt), _p(lw), len(adv), _p(cu),
-                          _p(adv), _p(inv), float(eps), float(grad_scale), _p(out["lse"]),
+                          _p(adv), _p(inv), float(eps), float(eps if eps_hi is None else eps_hi),
+                          float(grad_scale), _p(out["lse"]),
                           _p(out["logp"]), _p(out["r"]), _p(out["term"]), _p(clipped),
                           _p(out["s"]), _p(dl))
     return RowsResult(out["lse"], out["logp"], out["r"], out["term"], clipped.astype(bool),
@@ -223,7 +250,8 @@ def objective_nested(cu_seqlens, group_ids, version_ids, term, P):
 
 
 # --------------------------------------------------------------------- full path
-def run_batch(batch, logits_bits, eps=0.2, grad_scale=1.0, std_floor=1e-8, want_dlogits=True):
+def run_batch(batch, logits_bits, eps=0.2, grad_scale=1.0, std_floor=1e-8, want_dlogits=True,
+              eps_hi=None, norm=0, traj_mask=None):
     """Whole hot path on a small batch: validate, advantage, rows, J.
 
     ``batch`` is a synth.gen.Batch (or anything with the same fields);
@@ -233,14 +261,18 @@ def run_batch(batch, logits_bits, eps=0.2, grad_scale=1.0, std_floor=1e-8, want_
                    P=batch.P, V=batch.V, G=batch.G, tbs=batch.tbs, v_theta=batch.v_theta,
                    K=batch.K, token_version=batch.token_version, logp_behav=batch.logp_behav)
     adv, inv, gc = advantage(batch.rewards, batch.group_ids, batch.cu_seqlens, batch.P, std_floor)
+    if norm != 0 or traj_mask is not None:
+        inv = weights(batch.group_ids, batch.cu_seqlens, gc, batch.P, norm, traj_mask)
     T = int(batch.cu_seqlens[-1])
     rr = rows(np.arange(T, dtype=np.int64), logits_bits, batch.V, batch.target_ids,
-              batch.logp_behav, batch.cu_seqlens, adv, inv, eps, grad_scale, want_dlogits)
+              batch.logp_behav, batch.cu_seqlens, adv, inv, eps, grad_scale, want_dlogits,
+              eps_hi=eps_hi)
     J, traj_sum = objective_tokens(batch.cu_seqlens, inv, rr.term)
     return dict(validate=val, adv=adv, inv_norm=inv, group_count=gc, rows=rr, J=J,
                 loss=-J, traj_sum=traj_sum,
                 n_clipped=int(rr.clipped.sum()),
-                n_active=int(((~rr.clipped) & (adv[_traj_index(batch.cu_seqlens)] != 0)).sum()))
+                n_active=int(((~rr.clipped) & (adv[_traj_index(batch.cu_seqlens)] != 0)
+                              & (inv[_traj_index(batch.cu_seqlens)] != 0)).sum()))
 
 
 def _traj_index(cu_seqlens):

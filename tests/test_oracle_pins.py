@@ -432,3 +432,105 @@ def test_validate_group_size_brute_force():
             assert bool(v["traj_flags"][i] & (1 << 4)) == (g[i] == 0)
         assert v["summary"]["n_groups_wrong_size"] == 1
         assert v["summary"]["c2_dropped"] == (1 if delta < 0 else 0)
+
+
+# ----------------------------------------------------------------- NEXT(1): DAPO options
+def _const_ratio_batch(r_const, V=8, L=(3, 1, 2, 5)):
+    T = sum(L)
+    lw = np.full(T, -math.log(V) - math.log(r_const), np.float32)
+    return make_manual(1, 4, 1, V, L, [0] * 4, [1, 0, 0, 1], [1000] * 4, [3] * T, lw), T, V
+
+
+def test_clip_higher_closed_form():
+    """Asymmetric clip [1-eps_lo, 1+eps_hi] (DAPO clip-higher): constant ratio r on every
+    token of R = [1,0,0,1] gives per-trajectory means min(rA, clip(r)A) in closed form:
+      r = 1.5:  A>0 -> 1+eps_hi, A<0 -> -r          J = (2(1+eps_hi) - 2r)/4
+      r = 1.25, eps_hi = 0.28: inside the range -> J = 0 (symmetric eps = 0.2 gives -0.025)
+      r = 0.5:  A>0 -> r, A<0 -> -(1-eps_lo)         J = (2r - 2(1-eps_lo))/4"""
+    hi = float(np.float32(0.28))
+    lo = float(np.float32(0.2))
+    for r_const, eps_hi, expect in ((1.5, 0.28, (2 * (1 + hi) - 3.0) / 4), (1.25, 0.28, 0.0),
+                                    (1.25, 0.2, (2 * (1 + lo) - 2.5) / 4),
+                                    (0.5, 0.28, (1.0 - 2 * (1 - lo)) / 4)):
+        b, T, V = _const_ratio_batch(r_const)
+        res = O.run_batch(b, np.zeros((T, V), np.uint16), eps=0.2, eps_hi=eps_hi, want_dlogits=False)
+        assert abs(res["J"] - expect) < 1e-6, (r_const, eps_hi, res["J"], expect)
+
+
+def test_token_mean_weights():
+    """Token-mean normalisation (DAPO): w_i = 1/sum of kept L; with equal lengths it coincides with
+    the paper's sequence mean 1/(P G L); kept weights always satisfy sum_i w_i L_i = 1."""
+    rng = np.random.default_rng(11)
+    P, G = 3, 4
+    g = rng.permutation(np.repeat(np.arange(P), G)).astype(np.int32)
+    cu = np.arange(P * G + 1) * 7
+    _, inv, gc = O.advantage(np.zeros(P * G, np.float32), g, cu, P)
+    w_tok = O.weights(g, cu, gc, P, norm=1)
+    np.testing.assert_allclose(w_tok, inv, rtol=1e-15)
+    np.testing.assert_allclose(w_tok, 1.0 / cu[-1], rtol=1e-15)
+    L = rng.integers(1, 20, size=P * G)
+    cu = np.concatenate([[0], np.cumsum(L)])
+    mask = (rng.random(P * G) < 0.7).astype(np.uint8)
+    _, _, gc = O.advantage(np.zeros(P * G, np.float32), g, cu, P)
+    w = O.weights(g, cu, gc, P, norm=1, traj_mask=mask)
+    assert abs(np.sum(w * L) - 1.0) < 1e-12
+    assert np.all(w[mask == 0] == 0.0)
+    ws = O.weights(g, cu, gc, P, norm=0, traj_mask=mask)
+    _, inv, _ = O.advantage(np.zeros(P * G, np.float32), g, cu, P)
+    np.testing.assert_allclose(ws, np.where(mask == 1, inv, 0.0), rtol=1e-15)
+
+
+def test_mask_equals_sub_batch():
+    """Masking every trajectory outside one prompt group equals running that group as its own
+    batch (groups are independent, eq:group_advantage; token mean over the kept tokens)."""
+    b = make_batch("mid32k", 4)
+    bits = b.logits_bits()
+    p0 = 2
+    mask = (b.group_ids == p0).astype(np.uint8)
+    full = O.run_batch(b, bits, norm=1, traj_mask=mask, want_dlogits=False)
+    idx = np.nonzero(mask)[0]
+    rows = np.concatenate([np.arange(b.cu_seqlens[i], b.cu_seqlens[i + 1]) for i in idx])
+    sub = make_manual(1, b.G, b.K, b.V, b.lengths[idx], np.zeros(len(idx), np.int32),
+                      b.rewards[idx], b.version_ids[idx], b.target_ids[rows], b.logp_behav[rows])
+    ref = O.run_batch(sub, bits[rows], norm=1, want_dlogits=False)
+    assert abs(full["J"] - ref["J"]) < 1e-12 * max(1.0, abs(ref["J"]))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_gradient_finite_differences_dapo(seed):
+    """O5 under clip-higher + token-mean weights + a trajectory mask vs central differences;
+    masked trajectories get exactly zero gradient."""
+    rng = np.random.default_rng(300 + seed)
+    V = int(rng.integers(2, 12))
+    L, g, R, ver, T, tgt = _tiny_batch(rng, V=V)
+    z = rng.normal(size=(T, V)) * 1.5
+    lsm = z - np.log(np.exp(z).sum(1, keepdims=True))
+    cur = lsm[np.arange(T), tgt]
+    hi = float(np.float32(0.28))
+    for _ in range(100):
+        lw = (cur - rng.normal(size=T) * 0.25).astype(np.float32)
+        r = np.exp(cur - lw.astype(np.float64))
+        if np.all(np.abs(r - (1 + hi)) > 1e-3) and np.all(np.abs(r - (1 - EPS32)) > 1e-3):
+            break
+    b = make_manual(2, 4, 3, V, L, g, R, ver, tgt, lw)
+    adv, _, gc = O.advantage(b.rewards, b.group_ids, b.cu_seqlens, b.P)
+    mask = np.ones(len(L), np.uint8)
+    mask[int(rng.integers(0, len(L)))] = 0
+    w = O.weights(b.group_ids, b.cu_seqlens, gc, b.P, norm=1, traj_mask=mask)
+    rr = O.rows_f64(np.arange(T), z, tgt, lw, b.cu_seqlens, adv, w, 0.2, eps_hi=0.28)
+
+    def J_of(zz):
+        q = O.rows_f64(np.arange(T), zz, tgt, lw, b.cu_seqlens, adv, w, 0.2, eps_hi=0.28,
+                       want_dlogits=False)
+        return O.objective_tokens(b.cu_seqlens, w, q.term)[0]
+    h = 1e-5
+    num = np.zeros_like(z)
+    for t in range(T):
+        for v in range(V):
+            zp = z.copy(); zp[t, v] += h
+            zm = z.copy(); zm[t, v] -= h
+            num[t, v] = -(J_of(zp) - J_of(zm)) / (2 * h)
+    err = np.abs(num - rr.dlogits).max() / max(np.abs(rr.dlogits).max(), 1e-12)
+    assert err < 1e-6, err
+    masked_rows = np.repeat(mask == 0, L)
+    assert np.all(rr.dlogits[masked_rows] == 0.0)
