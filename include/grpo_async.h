@@ -90,6 +90,23 @@ enum {
     GRPO_NUM_STATS = 6
 };
 
+/* Loss options of the DAPO setting the paper trains with ("we follow the
+ * setting of DAPO").  grpo_async_loss_fwd / grpo_async_advantage
+ * are the paper's equation as written (eps_lo = eps_hi = eps, GRPO_NORM_SEQ, no mask). */
+enum {
+    GRPO_NORM_SEQ = 0,   /* eq:grpo_async: 1/L_i per trajectory, 1/G_p per group, 1/P per prompt */
+    GRPO_NORM_TOKEN = 1  /* DAPO token-level: 1 / (sum of L_i over kept trajectories)            */
+};
+typedef struct {
+    float eps_lo;              /* clip below at 1 - eps_lo, in (0, 1)                             */
+    float eps_hi;              /* clip above at 1 + eps_hi, > 0 ("clip-higher": eps_hi > eps_lo)  */
+    int32_t norm;              /* GRPO_NORM_SEQ or GRPO_NORM_TOKEN                                */
+    const uint8_t *traj_mask;  /* device uint8[N] or NULL: 0 drops trajectory i from the loss and */
+                               /* from the token-mean denominator (overlong filtering, masking of */
+                               /* C1-violating partial rollouts); group statistics keep    */
+                               /* every member                                                    */
+} grpo_loss_opts_t;
+
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
     int32_t kernel;        /* 0 auto (= 2 today), 1 cluster-resident fused, 2 row-wise two-pass */
@@ -159,6 +176,18 @@ grpo_status_t grpo_async_advantage(const float *rewards, const int32_t *group_id
                                    int32_t *group_count, grpo_stream_t stream);
 
 /*
+ * grpo_async_advantage_ex -- grpo_async_advantage with grpo_loss_opts_t:
+ *   inv_norm_i = 1/(P * count_p * L_i) (GRPO_NORM_SEQ) or 1/sum_kept L (GRPO_NORM_TOKEN),
+ *   and 0 for trajectories the mask drops.  opts->eps_* are not used here.
+ * Errors: as grpo_async_advantage, plus GRPO_ERR_INVALID_ARG for NULL opts or a bad norm.
+ */
+grpo_status_t grpo_async_advantage_ex(const float *rewards, const int32_t *group_ids,
+                                      const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                      float std_floor, const grpo_loss_opts_t *opts, float *adv,
+                                      float *inv_norm, int32_t *group_count,
+                                      grpo_stream_t stream);
+
+/*
  * grpo_async_loss_fwd -- fused log-softmax + target gather + ratio + clip +
  * min + segmented mean, and (if dlogits != NULL) the backward in the same pass.
  * The chunk is rows [row_begin, row_begin + n_rows) of this rank's packing.
@@ -194,6 +223,23 @@ grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int
                                   double *traj_sum, double *stats, uint16_t *dlogits,
                                   void *workspace, size_t workspace_bytes,
                                   const grpo_tune_t *tune, grpo_stream_t stream);
+
+/*
+ * grpo_async_loss_fwd_ex -- grpo_async_loss_fwd with the clip range [1 - opts->eps_lo,
+ * 1 + opts->eps_hi] (the weights come from grpo_async_advantage_ex).  Same arguments
+ * otherwise; eps is replaced by opts.
+ * Errors: as grpo_async_loss_fwd, plus GRPO_ERR_INVALID_ARG for NULL opts, eps_lo not in
+ * (0,1) or eps_hi <= 0.
+ */
+grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, int64_t n_rows,
+                                     int32_t V, int64_t ld, const int64_t *target_ids,
+                                     const float *logp_behav, const int64_t *cu_seqlens,
+                                     int32_t N, const int32_t *traj_index, const float *adv,
+                                     const float *inv_norm, const grpo_loss_opts_t *opts,
+                                     float grad_scale, float *logp_out, float *lse_out,
+                                     float *token_scale_out, double *traj_sum, double *stats,
+                                     uint16_t *dlogits, void *workspace, size_t workspace_bytes,
+                                     const grpo_tune_t *tune, grpo_stream_t stream);
 
 /*
  * grpo_async_loss_bwd -- unfused backward: one streaming pass that re-reads

@@ -31,7 +31,8 @@ SUMMARY_FIELDS = ("n_traj", "n_tokens", "n_stale", "n_future", "n_zero_len", "n_
                   "cu_ok", "tbs_ok", "c1_ok", "c2_ok", "c3_ok", "valid")
 
 EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advantage",
-            "grpo_async_loss_fwd", "grpo_async_loss_bwd", "grpo_async_workspace_size",
+            "grpo_async_advantage_ex", "grpo_async_loss_fwd", "grpo_async_loss_fwd_ex",
+            "grpo_async_loss_bwd", "grpo_async_workspace_size",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -48,6 +49,14 @@ class Tune(C.Structure):
     _fields_ = [("kernel", C.c_int32), ("cluster_size", C.c_int32),
                 ("ctas_per_sm", C.c_int32), ("stages", C.c_int32), ("lag", C.c_int32),
                 ("prefetch", C.c_int32), ("row_cache", C.c_int32)]
+
+
+NORM_SEQ, NORM_TOKEN = 0, 1
+
+
+class LossOpts(C.Structure):
+    _fields_ = [("eps_lo", C.c_float), ("eps_hi", C.c_float), ("norm", C.c_int32),
+                ("traj_mask", C.c_void_p)]
 
 
 class Plan(C.Structure):
@@ -82,6 +91,11 @@ def _load():
     lib.grpo_async_loss_fwd.argtypes = [P, i64, i64, i32, i64, P, P, P, i32, P, P, P, f32, f32,
                                         P, P, P, P, P, P, P, sz, P, P]
     lib.grpo_async_loss_fwd.restype = st
+    lib.grpo_async_advantage_ex.argtypes = [P, P, P, i32, i32, f32, P, P, P, P, P]
+    lib.grpo_async_advantage_ex.restype = st
+    lib.grpo_async_loss_fwd_ex.argtypes = [P, i64, i64, i32, i64, P, P, P, i32, P, P, P, P, f32,
+                                           P, P, P, P, P, P, P, sz, P, P]
+    lib.grpo_async_loss_fwd_ex.restype = st
     lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
     lib.grpo_async_loss_bwd.restype = st
     lib.grpo_async_workspace_size.argtypes = [i64, i32, i32]
@@ -200,6 +214,49 @@ def grpo_async_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor, adv, i
         _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, P, float(std_floor),
         _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"),
         _ptr(group_count, torch.int32, "group_count"), _stream(stream)))
+
+
+def _opts(eps_lo, eps_hi, norm, traj_mask):
+    return LossOpts(float(eps_lo), float(eps_hi), int(norm),
+                    _ptr(traj_mask, torch.uint8, "traj_mask"))
+
+
+def grpo_async_advantage_ex(rewards, group_ids, cu_seqlens, N, P, std_floor, eps_lo, eps_hi, norm,
+                            traj_mask, adv, inv_norm, group_count=None, stream=None):
+    o = _opts(eps_lo, eps_hi, norm, traj_mask)
+    _check(LIB.grpo_async_advantage_ex(
+        _ptr(rewards, torch.float32, "rewards"), _ptr(group_ids, torch.int32, "group_ids"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, P, float(std_floor), C.byref(o),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"),
+        _ptr(group_count, torch.int32, "group_count"), _stream(stream)))
+
+
+def _tune(tune):
+    if tune is None:
+        return None
+    return C.byref(Tune(*[int(tune.get(k, 0)) for k in ("kernel", "cluster_size", "ctas_per_sm",
+                                                       "stages", "lag", "prefetch", "row_cache")]))
+
+
+def grpo_async_loss_fwd_ex(logits, row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens,
+                           N, traj_index, adv, inv_norm, eps_lo, eps_hi, norm, traj_mask,
+                           grad_scale, logp_out, lse_out, token_scale_out, traj_sum, stats,
+                           dlogits, workspace, tune=None, stream=None):
+    for name, x in (("logits", logits), ("dlogits", dlogits)):
+        if x is not None and x.element_size() != 2:
+            raise TypeError(f"{name}: expected a 16-bit (bf16) tensor")
+    o = _opts(eps_lo, eps_hi, norm, traj_mask)
+    tp = _tune(tune)
+    _check(LIB.grpo_async_loss_fwd_ex(
+        _ptr(logits, None, "logits"), row_begin, n_rows, V, ld,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(logp_behav, torch.float32, "logp_behav"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, _ptr(traj_index, torch.int32, "traj_index"),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"), C.byref(o),
+        float(grad_scale), _ptr(logp_out, torch.float32, "logp_out"),
+        _ptr(lse_out, torch.float32, "lse_out"), _ptr(token_scale_out, torch.float32, "token_scale_out"),
+        _ptr(traj_sum, torch.float64, "traj_sum"), _ptr(stats, torch.float64, "stats"),
+        _ptr(dlogits, None, "dlogits"), _ptr(workspace, torch.uint8, "workspace"),
+        workspace.numel() if workspace is not None else 0, tp, _stream(stream)))
 
 
 def grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens, N,

@@ -73,11 +73,18 @@ class GrpoAsyncLoss:
     """One step of the hot path over a DeviceBatch.
 
     eps: clip range; grad_scale multiplies dlogits; std_floor: Z2.
-    tune: optional dict for grpo_tune_t (kernel / cluster_size / ctas_per_sm / stages).
+    DAPO options: eps_hi (clip-higher upper range, default eps),
+    norm ("seq" = eq:grpo_async as written, "token" = DAPO token mean) and traj_mask
+    (uint8 device tensor [N], 0 drops a trajectory from the loss).
+    tune: optional dict for grpo_tune_t (kernel / cluster_size / ctas_per_sm / stages / ...).
     """
 
-    def __init__(self, eps=0.2, std_floor=1e-8, grad_scale=1.0, tune=None):
+    def __init__(self, eps=0.2, std_floor=1e-8, grad_scale=1.0, tune=None, eps_hi=None,
+                 norm="seq", traj_mask=None):
         self.eps = float(eps)
+        self.eps_hi = float(eps if eps_hi is None else eps_hi)
+        self.norm = {"seq": L.NORM_SEQ, "token": L.NORM_TOKEN}[norm]
+        self.traj_mask = traj_mask
         self.std_floor = float(std_floor)
         self.grad_scale = float(grad_scale)
         self.tune = tune
@@ -99,10 +106,18 @@ class GrpoAsyncLoss:
         dev = db.rewards.device
         adv = adv if adv is not None else torch.empty(db.N, dtype=torch.float32, device=dev)
         inv = inv_norm if inv_norm is not None else torch.empty(db.N, dtype=torch.float32, device=dev)
-        L.grpo_async_advantage(db.rewards, db.group_ids, db.cu_seqlens, db.N, db.P, self.std_floor,
-                               adv, inv, None, stream)
+        if self._default_opts():
+            L.grpo_async_advantage(db.rewards, db.group_ids, db.cu_seqlens, db.N, db.P,
+                                   self.std_floor, adv, inv, None, stream)
+        else:
+            L.grpo_async_advantage_ex(db.rewards, db.group_ids, db.cu_seqlens, db.N, db.P,
+                                      self.std_floor, self.eps, self.eps_hi, self.norm,
+                                      self.traj_mask, adv, inv, None, stream)
         self.launches += L.grpo_last_launch_count()
         return adv, inv
+
+    def _default_opts(self):
+        return self.eps_hi == self.eps and self.norm == L.NORM_SEQ and self.traj_mask is None
 
     def workspace(self, n_rows, V, N, device):
         need = L.grpo_async_workspace_size(n_rows, V, N)
@@ -118,10 +133,17 @@ class GrpoAsyncLoss:
         ld = logits.shape[1]
         N = cu_seqlens.numel() - 1
         ws = self.workspace(n_rows, V, N, logits.device)
-        L.grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav,
-                              cu_seqlens, N, traj_index, adv, inv_norm, self.eps, self.grad_scale,
-                              logp_out, lse_out, scale_out, traj_sum, stats, dlogits, ws,
-                              self.tune, stream)
+        if self._default_opts():
+            L.grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav,
+                                  cu_seqlens, N, traj_index, adv, inv_norm, self.eps,
+                                  self.grad_scale, logp_out, lse_out, scale_out, traj_sum, stats,
+                                  dlogits, ws, self.tune, stream)
+        else:
+            L.grpo_async_loss_fwd_ex(logits, row_begin, n_rows, V, ld, target_ids, logp_behav,
+                                     cu_seqlens, N, traj_index, adv, inv_norm, self.eps,
+                                     self.eps_hi, self.norm, self.traj_mask, self.grad_scale,
+                                     logp_out, lse_out, scale_out, traj_sum, stats, dlogits, ws,
+                                     self.tune, stream)
         self.launches += L.grpo_last_launch_count()
 
     def loss_bwd(self, logits, n_rows, V, target_ids, lse, token_scale, dlogits, mult=1.0,

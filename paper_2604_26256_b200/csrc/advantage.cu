@@ -1,4 +1,5 @@
 // advantage.cu -- group-relative advantages, eq:group_advantage:
+// (with grpo_async_advantage_ex: DAPO token-mean weights and trajectory masks)
 //   A_i = (R_i - mean_p) / std_p  over the members of prompt group p,
 // population std (Z1), A = 0 exactly for a group whose rewards are
 // bitwise equal, else denominator max(std, floor) (Z2), and the token weight
@@ -12,14 +13,30 @@
 
 namespace grpo {
 
+// A trajectory is kept in the loss when its group id is valid, L_i > 0 and the
+// optional mask allows it.
+__device__ __forceinline__ bool kept(const int32_t *group_ids, const int64_t *cu,
+                                     const uint8_t *traj_mask, int32_t P, int32_t i) {
+    const int32_t g = group_ids[i];
+    return g >= 0 && g < P && cu[i + 1] > cu[i] && (!traj_mask || traj_mask[i]);
+}
+
 __global__ void __launch_bounds__(256)
     advantage_kernel(const float *__restrict__ rewards, const int32_t *__restrict__ group_ids,
                      const int64_t *__restrict__ cu, int32_t N, int32_t P, float std_floor,
+                     int32_t norm, const uint8_t *__restrict__ traj_mask,
                      float *__restrict__ adv, float *__restrict__ inv_norm,
                      int32_t *__restrict__ group_count) {
     const int lane = threadIdx.x & 31;
     const int32_t p = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     if (p >= P) return;
+    // token-mean normalisation (DAPO): the kept tokens of the whole batch
+    int64_t T_kept = 0;
+    if (norm == GRPO_NORM_TOKEN) {
+        for (int32_t i = lane; i < N; i += 32)
+            if (kept(group_ids, cu, traj_mask, P, i)) T_kept += cu[i + 1] - cu[i];
+        for (int off = 16; off > 0; off >>= 1) T_kept += __shfl_xor_sync(0xFFFFFFFFu, T_kept, off);
+    }
     // pass 1: count, sum, bitwise equality
     int32_t n = 0;
     double sum = 0.0;
@@ -67,8 +84,12 @@ __global__ void __launch_bounds__(256)
             const double a = all_equal ? 0.0 : ((double)rewards[i] - mean) / den;
             const int64_t L = cu[i + 1] - cu[i];
             adv[i] = (float)a;
-            inv_norm[i] = L > 0 ? (float)(1.0 / __dmul_rn(__dmul_rn((double)P, (double)n), (double)L))
-                                : 0.0f;
+            if (!kept(group_ids, cu, traj_mask, P, i))
+                inv_norm[i] = 0.0f;
+            else if (norm == GRPO_NORM_TOKEN)
+                inv_norm[i] = (float)(1.0 / (double)T_kept);
+            else
+                inv_norm[i] = (float)(1.0 / __dmul_rn(__dmul_rn((double)P, (double)n), (double)L));
         }
     }
 }
@@ -87,7 +108,8 @@ __global__ void advantage_invalid_kernel(const int32_t *__restrict__ group_ids, 
 }
 
 cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, const int64_t *cu,
-                             int32_t N, int32_t P, float std_floor, float *adv, float *inv_norm,
+                             int32_t N, int32_t P, float std_floor, int32_t norm,
+                             const uint8_t *traj_mask, float *adv, float *inv_norm,
                              int32_t *group_count, cudaStream_t s, int *launches) {
     if (N > 0) {
         advantage_invalid_kernel<<<(N + 255) / 256, 256, 0, s>>>(group_ids, N, P, adv, inv_norm);
@@ -95,7 +117,7 @@ cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, con
     }
     const int64_t threads = (int64_t)P * 32;
     advantage_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-        rewards, group_ids, cu, N, P, std_floor, adv, inv_norm, group_count);
+        rewards, group_ids, cu, N, P, std_floor, norm, traj_mask, adv, inv_norm, group_count);
     *launches += 1;
     return cudaGetLastError();
 }

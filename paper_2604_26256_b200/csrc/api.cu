@@ -199,9 +199,30 @@ grpo_status_t grpo_async_advantage(const float *rewards, const int32_t *group_id
     if (N > 0 && (!rewards || !group_ids || !cu_seqlens || !adv || !inv_norm))
         return fail(GRPO_ERR_INVALID_ARG, "advantage: NULL pointer");
     int launches = 0;
-    cudaError_t e = grpo::launch_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor, adv,
-                                           inv_norm, group_count, (cudaStream_t)stream, &launches);
+    cudaError_t e = grpo::launch_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor,
+                                           GRPO_NORM_SEQ, nullptr, adv, inv_norm, group_count,
+                                           (cudaStream_t)stream, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "advantage");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_advantage_ex(const float *rewards, const int32_t *group_ids,
+                                      const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                      float std_floor, const grpo_loss_opts_t *opts, float *adv,
+                                      float *inv_norm, int32_t *group_count,
+                                      grpo_stream_t stream) {
+    if (!opts) return fail(GRPO_ERR_INVALID_ARG, "advantage_ex: NULL opts");
+    if (opts->norm != GRPO_NORM_SEQ && opts->norm != GRPO_NORM_TOKEN)
+        return fail(GRPO_ERR_INVALID_ARG, "advantage_ex: norm %d", opts->norm);
+    if (N < 0 || P <= 0) return fail(GRPO_ERR_INVALID_ARG, "advantage_ex: N=%d P=%d", N, P);
+    if (!(std_floor > 0.0f)) return fail(GRPO_ERR_INVALID_ARG, "advantage_ex: std_floor must be > 0");
+    if (N > 0 && (!rewards || !group_ids || !cu_seqlens || !adv || !inv_norm))
+        return fail(GRPO_ERR_INVALID_ARG, "advantage_ex: NULL pointer");
+    int launches = 0;
+    cudaError_t e = grpo::launch_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor,
+                                           opts->norm, opts->traj_mask, adv, inv_norm,
+                                           group_count, (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "advantage_ex");
     return ok(launches);
 }
 
@@ -214,10 +235,29 @@ grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int
                                   double *traj_sum, double *stats, uint16_t *dlogits,
                                   void *workspace, size_t workspace_bytes,
                                   const grpo_tune_t *tune, grpo_stream_t stream) {
+    if (!(eps > 0.0f && eps < 1.0f)) return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: eps not in (0,1)");
+    const grpo_loss_opts_t opts = {eps, eps, GRPO_NORM_SEQ, nullptr};
+    return grpo_async_loss_fwd_ex(logits, row_begin, n_rows, V, ld, target_ids, logp_behav,
+                                  cu_seqlens, N, traj_index, adv, inv_norm, &opts, grad_scale,
+                                  logp_out, lse_out, token_scale_out, traj_sum, stats, dlogits,
+                                  workspace, workspace_bytes, tune, stream);
+}
+
+grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, int64_t n_rows,
+                                     int32_t V, int64_t ld, const int64_t *target_ids,
+                                     const float *logp_behav, const int64_t *cu_seqlens,
+                                     int32_t N, const int32_t *traj_index, const float *adv,
+                                     const float *inv_norm, const grpo_loss_opts_t *opts,
+                                     float grad_scale, float *logp_out, float *lse_out,
+                                     float *token_scale_out, double *traj_sum, double *stats,
+                                     uint16_t *dlogits, void *workspace, size_t workspace_bytes,
+                                     const grpo_tune_t *tune, grpo_stream_t stream) {
+    if (!opts) return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: NULL opts");
     if (n_rows < 0 || N <= 0 || V <= 0 || row_begin < 0)
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: n_rows=%lld N=%d V=%d row_begin=%lld",
                     (long long)n_rows, N, V, (long long)row_begin);
-    if (!(eps > 0.0f && eps < 1.0f)) return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: eps not in (0,1)");
+    if (!(opts->eps_lo > 0.0f && opts->eps_lo < 1.0f) || !(opts->eps_hi > 0.0f))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: eps_lo not in (0,1) or eps_hi <= 0");
     if (!cu_seqlens || !adv || !inv_norm || !traj_sum || !stats)
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: NULL cu_seqlens/adv/inv_norm/traj_sum/stats");
     if (n_rows > 0 && (!logits || !target_ids || !logp_behav))
@@ -248,7 +288,8 @@ grpo_status_t grpo_async_loss_fwd(const uint16_t *logits, int64_t row_begin, int
     a.traj_index = traj_index;
     a.adv = adv;
     a.inv_norm = inv_norm;
-    a.eps = eps;
+    a.eps_lo = opts->eps_lo;
+    a.eps_hi = opts->eps_hi;
     a.grad_scale = grad_scale;
     a.logp_out = logp_out;
     a.lse_out = lse_out;

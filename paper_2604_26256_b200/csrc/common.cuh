@@ -340,18 +340,19 @@ __device__ __forceinline__ double row_logp(float zy, float M, float l2s) {
     return (fma((double)zy, kLog2eD, -(double)M) - (double)l2s) * kLn2D;
 }
 
-__device__ __forceinline__ RowOut row_epilogue(double logp, const RowInfo &ri, float eps,
-                                               float grad_scale) {
+__device__ __forceinline__ RowOut row_epilogue(double logp, const RowInfo &ri, float eps_lo,
+                                               float eps_hi, float grad_scale) {
     RowOut o;
     const float r = expf((float)(logp - (double)ri.logp_w));
-    const float lo = 1.0f - eps, hi = 1.0f + eps;
+    const float lo = 1.0f - eps_lo, hi = 1.0f + eps_hi;
     const float c = fminf(fmaxf(r, lo), hi);
     const float A = ri.adv;
     o.r = r;
     o.term = fminf(r * A, c * A);
     const bool clipped = (A > 0.0f && r > hi) || (A < 0.0f && r < lo);
     o.s = clipped ? 0.0f : grad_scale * ri.inv_norm * A * r;
-    o.flags = (clipped ? kRowClipped : 0) | ((!clipped && A != 0.0f) ? kRowActive : 0);
+    o.flags = (clipped ? kRowClipped : 0) |
+              ((!clipped && A != 0.0f && ri.inv_norm != 0.0f) ? kRowActive : 0);
     return o;
 }
 
@@ -371,7 +372,7 @@ struct LossArgs {
     const int32_t *traj_index;
     const float *adv;
     const float *inv_norm;
-    float eps;
+    float eps_lo, eps_hi;   // clip range [1 - eps_lo, 1 + eps_hi]
     float grad_scale;
     float *logp_out;
     float *lse_out;
@@ -402,7 +403,8 @@ cudaError_t launch_validate(const int64_t *version_ids, const int64_t *token_ver
                             int32_t *group_count, int32_t *stale_hist,
                             grpo_validate_summary_t *summary, cudaStream_t s, int *launches);
 cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, const int64_t *cu,
-                             int32_t N, int32_t P, float std_floor, float *adv, float *inv_norm,
+                             int32_t N, int32_t P, float std_floor, int32_t norm,
+                             const uint8_t *traj_mask, float *adv, float *inv_norm,
                              int32_t *group_count, cudaStream_t s, int *launches);
 
 }  // namespace grpo

@@ -63,7 +63,7 @@ struct RowwiseParams {
     int32_t V;
     int64_t n_rows;
     const RowInfo *rowinfo;
-    float eps, grad_scale;
+    float eps_lo, eps_hi, grad_scale;
     float *logp_out, *lse_out, *scale_out, *term_ws, *logp_ws;
     uint8_t *flag_ws;
     int32_t prefetch;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                 const float lse2 = cm + l2s;
                 const float zyv = y_valid ? zy : __int_as_float(0x7FC00000);
                 const double logp_d = row_logp(zyv, cm, l2s);
-                const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
+                const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                 const float logp = (float)logp_d;
                 if (p.logp_out) p.logp_out[row] = logp;
                 if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                     const float l2s = log2f(S);
                     const float lse2 = M + l2s;
                     const double logp_d = row_logp(zyv, M, l2s);
-                    const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
+                    const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                     if (crank == 0) {
                         const float logp = (float)logp_d;
                         if (p.logp_out) p.logp_out[row] = logp;
@@ -329,7 +329,8 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cud
     p.V = a.V;
     p.n_rows = a.n_rows;
     p.rowinfo = a.rowinfo;
-    p.eps = a.eps;
+    p.eps_lo = a.eps_lo;
+    p.eps_hi = a.eps_hi;
     p.grad_scale = a.grad_scale;
     p.logp_out = a.logp_out;
     p.lse_out = a.lse_out;

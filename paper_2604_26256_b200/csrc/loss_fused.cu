@@ -53,7 +53,7 @@ struct FusedParams {
     int32_t V;
     int64_t n_rows;
     const RowInfo *rowinfo;
-    float eps, grad_scale;
+    float eps_lo, eps_hi, grad_scale;
     float *logp_out, *lse_out, *scale_out, *term_ws, *logp_ws;
     uint8_t *flag_ws;
     int32_t n_vec_row;  // ceil(V / 8)
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const float l2s = log2f(Ssum);
                     const float lse2 = M + l2s;           // log2-domain logsumexp of the row
                     const double logp_d = row_logp(zyv, M, l2s);
-                    const RowOut o = row_epilogue(logp_d, ri, p.eps, p.grad_scale);
+                    const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                     rowsc[e_slot] = make_float4(lse2, o.s, zyv,
                                                 __int_as_float(y_valid ? ri.target : -1));
                     // slot consumed: re-arm it for row ke + NX before the compute warps
@@ -429,7 +429,8 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
     fp.V = a.V;
     fp.n_rows = a.n_rows;
     fp.rowinfo = a.rowinfo;
-    fp.eps = a.eps;
+    fp.eps_lo = a.eps_lo;
+    fp.eps_hi = a.eps_hi;
     fp.grad_scale = a.grad_scale;
     fp.logp_out = a.logp_out;
     fp.lse_out = a.lse_out;

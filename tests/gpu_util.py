@@ -24,10 +24,13 @@ def dev_bits_to_f64(t: torch.Tensor, V: int) -> np.ndarray:
 
 
 def run_gpu(batch, logits_bits, device, tune=None, chunks=1, inplace=False, want_dlogits=True,
-            grad_scale=1.0, eps=0.2):
+            grad_scale=1.0, eps=0.2, eps_hi=None, norm="seq", traj_mask=None):
     """Whole path on the GPU: validate, advantage, fused loss over `chunks` row chunks."""
     db = G.DeviceBatch.from_host(batch, device)
-    loss = G.GrpoAsyncLoss(eps=eps, grad_scale=grad_scale, tune=tune)
+    mask_d = None if traj_mask is None else torch.from_numpy(
+        np.ascontiguousarray(traj_mask, np.uint8)).to(device)
+    loss = G.GrpoAsyncLoss(eps=eps, grad_scale=grad_scale, tune=tune, eps_hi=eps_hi, norm=norm,
+                           traj_mask=mask_d)
     vo = loss.validate(db)
     adv, inv = loss.advantage(db)
     T, ld, V = batch.T, batch.ld, batch.V
@@ -65,17 +68,20 @@ def run_gpu(batch, logits_bits, device, tune=None, chunks=1, inplace=False, want
     return out
 
 
-def run_oracle(batch, logits_bits, want_dlogits=True, eps=0.2, grad_scale=1.0):
+def run_oracle(batch, logits_bits, want_dlogits=True, eps=0.2, grad_scale=1.0, eps_hi=None,
+               norm="seq", traj_mask=None):
     return O.run_batch(batch, logits_bits, eps=eps, grad_scale=grad_scale,
-                       std_floor=float(np.float32(1e-8)), want_dlogits=want_dlogits)
+                       std_floor=float(np.float32(1e-8)), want_dlogits=want_dlogits,
+                       eps_hi=eps_hi, norm={"seq": 0, "token": 1}[norm], traj_mask=traj_mask)
 
 
-def near_boundary(r, eps=EPS32, tol=1e-5):
-    return (np.abs(r - (1 + eps)) <= tol) | (np.abs(r - (1 - eps)) <= tol)
+def near_boundary(r, eps=EPS32, tol=1e-5, eps_hi=None):
+    hi = eps if eps_hi is None else float(np.float32(eps_hi))
+    return (np.abs(r - (1 + hi)) <= tol) | (np.abs(r - (1 - eps)) <= tol)
 
 
 def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5, dl_rel=1e-2,
-            logits_pad=None):
+            logits_pad=None, eps_hi=None):
     """Assert the north_star criteria; returns a dict of measured errors."""
     rr = ref["rows"]
     errs = {}
@@ -106,7 +112,7 @@ def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5,
     ts_scale = np.maximum(np.abs(ref["traj_sum"]), 1e-3 * batch.lengths)
     assert np.all(np.abs(gpu["traj_sum"] - ref["traj_sum"]) <= 1e-5 * ts_scale + 1e-6), "traj_sum"
     # clip decisions: fp32 vs fp64 may differ only within 1e-5 of a clip boundary
-    nb = near_boundary(rr.r)
+    nb = near_boundary(rr.r, eps_hi=eps_hi)
     clipped_gpu_s = gpu["scale"] == 0.0
     oracle_zero_s = rr.s == 0.0
     mism = (clipped_gpu_s != oracle_zero_s) & ~nb
