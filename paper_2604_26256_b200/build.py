@@ -36,7 +36,7 @@ def _stale(target, deps):
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(INCLUDE, "grpo_async.h")]
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     if not force and not _stale(LIB, deps):
         return LIB
     os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)

@@ -77,6 +77,9 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 }  // namespace
 
+// shared with the host control plane (transfer_queue.cu)
+grpo_status_t grpo_internal_fail(grpo_status_t st, const char *msg) { return fail(st, "%s", msg); }
+
 extern "C" {
 
 const char *grpo_last_error(void) { return g_last_error.c_str(); }

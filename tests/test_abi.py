@@ -8,11 +8,11 @@ import re
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "grpo_async.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("grpo_async.h", "grpo_transfer_queue.h")]
 
 
 def declared_functions():
-    src = open(HEADER).read()
+    src = "\n".join(open(h).read() for h in HEADERS)
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(grpo_\w+)\s*\(", src)))
 
@@ -29,13 +29,15 @@ def test_library_exports_every_declared_symbol():
     lib = C.CDLL(L.LIB_PATH)
     missing = [n for n in declared_functions() if not hasattr(lib, n)]
     assert not missing, missing
-    assert set(L.EXPORTED) == set(declared_functions())
+    import paper_2604_26256_b200.transfer_queue as TQ
+    assert set(L.EXPORTED) | set(TQ.EXPORTED) == set(declared_functions())
 
 
 def test_binding_names_match_c_entry_points():
     import paper_2604_26256_b200 as G
     for n in declared_functions():
-        assert hasattr(G._lib, n), n
+        if not n.startswith("grpo_tq_"):
+            assert hasattr(G._lib, n), n
 
 
 def test_host_side_errors_without_gpu():
