@@ -156,7 +156,9 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
             const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + bi * BV + threadIdx.x;
             uint4 x[U];
 #pragma unroll
-            for (int j = 0; j < U; ++j) x[j] = ldg_policy(src + j * NT, pol_keep);
+            for (int j = 0; j < U; ++j)
+                // vectors kept in shared memory are not re-read: let L2 evict them first
+                x[j] = ldg_policy(src + j * NT, bi * U + j < cache_vecs ? pol_stream : pol_keep);
 #pragma unroll
             for (int j = 0; j < U; ++j)
                 if (bi * U + j < cache_vecs) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
@@ -167,7 +169,9 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 const int vi = bi * BV + j * NT + threadIdx.x;
-                x[j] = vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_keep) : neg_inf;
+                x[j] = vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8,
+                                               bi * U + j < cache_vecs ? pol_stream : pol_keep)
+                                  : neg_inf;
                 if (vi == tail_vi) x[j] = mask_tail(x[j], tail_valid);
             }
 #pragma unroll
