@@ -242,6 +242,51 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
                                      const grpo_tune_t *tune, grpo_stream_t stream);
 
 /*
+ * grpo_async_loss_fwd_vp -- the fused loss for vocabulary-parallel logits (
+ * Megatron-style tensor parallelism of the LM head): rank q of a group of R
+ * GPUs holds the columns [q*shard_cols, (q+1)*shard_cols) of every row of the chunk.
+ * The per-row logsumexp needs all R shards: the kernel exchanges one 16-byte partial
+ * per row and rank through peer memory (NVLink P2P stores + system-scope arrival
+ * counters) inside the loss kernel, then writes this rank's slice of dlogits.  Every
+ * rank computes identical per-row outputs, traj_sum and stats (no further reduction).
+ * comm describes the group (host struct of device pointers):
+ *   world R <= GRPO_VP_MAX_RANKS; the call computes ranks [rank_begin, rank_begin+n_local)
+ *   (n_local = 1 on a multi-GPU run; n_local = R when one GPU runs the whole group as a
+ *   cooperative grid); shard_cols % 8 == 0; logits[i] / dlogits[i] bf16 [n_rows, ld] of
+ *   local rank i (ld >= shard_cols, 16-byte aligned; dlogits may be NULL = forward only);
+ *   xbuf[q] >= n_rows*world*16 bytes and flags[q] uint32[n_rows] of EVERY rank q, mapped
+ *   into this process (peer pointers); flags zero-initialised once; epoch = number of
+ *   earlier calls on these buffers (the same on every rank).  All ranks must call with the
+ *   same arguments except the pointers they own; a rank whose peers never arrive traps.
+ * Other arguments as grpo_async_loss_fwd_ex (per-row outputs written by local rank 0).
+ * Errors: GRPO_ERR_INVALID_ARG (bad comm, NULL pointers), GRPO_ERR_ALIGNMENT,
+ *   GRPO_ERR_WORKSPACE, GRPO_ERR_CUDA.
+ */
+#define GRPO_VP_MAX_RANKS 8
+typedef struct {
+    int32_t world;
+    int32_t rank_begin;
+    int32_t n_local;
+    int32_t shard_cols;
+    const uint16_t *logits[GRPO_VP_MAX_RANKS];
+    uint16_t *dlogits[GRPO_VP_MAX_RANKS];
+    void *xbuf[GRPO_VP_MAX_RANKS];
+    uint32_t *flags[GRPO_VP_MAX_RANKS];
+    uint32_t epoch;
+} grpo_vp_comm_t;
+
+grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_begin,
+                                     int64_t n_rows, int32_t V, int64_t ld,
+                                     const int64_t *target_ids, const float *logp_behav,
+                                     const int64_t *cu_seqlens, int32_t N,
+                                     const int32_t *traj_index, const float *adv,
+                                     const float *inv_norm, const grpo_loss_opts_t *opts,
+                                     float grad_scale, float *logp_out, float *lse_out,
+                                     float *token_scale_out, double *traj_sum, double *stats,
+                                     void *workspace, size_t workspace_bytes,
+                                     grpo_stream_t stream);
+
+/*
  * grpo_async_loss_bwd -- unfused backward: one streaming pass that re-reads
  * the logits and writes dlogits = grad_scale_mult * s_t * (exp(z - lse_t) - onehot(y_t))
  * from the lse and token_scale saved by grpo_async_loss_fwd.

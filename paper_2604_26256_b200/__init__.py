@@ -12,6 +12,7 @@ from ._lib import (  # noqa: F401
     grpo_async_validate_sync, grpo_async_workspace_size, grpo_last_error,
     grpo_last_launch_count, grpo_version, grpo_profile_enable, grpo_profile_collect, grpo_async_last_plan, GrpoError, FLAG_NAMES, SUMMARY_FIELDS, NUM_STATS,
     STAT_J, STAT_ROWS, STAT_CLIPPED, STAT_ACTIVE, STAT_ABS, STAT_LOGP, LIB_PATH)
-from .api import DeviceBatch, GrpoAsyncLoss, ValidateOut, lpt_partition, shard_rows  # noqa: F401
+from .api import (DeviceBatch, GrpoAsyncLoss, ValidateOut, VpGroup, lpt_partition,  # noqa: F401
+                  shard_rows)
 
 __version__ = "0.1.0"

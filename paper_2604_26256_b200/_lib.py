@@ -32,7 +32,7 @@ SUMMARY_FIELDS = ("n_traj", "n_tokens", "n_stale", "n_future", "n_zero_len", "n_
 
 EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advantage",
             "grpo_async_advantage_ex", "grpo_async_loss_fwd", "grpo_async_loss_fwd_ex",
-            "grpo_async_loss_bwd", "grpo_async_workspace_size",
+            "grpo_async_loss_fwd_vp", "grpo_async_loss_bwd", "grpo_async_workspace_size",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -67,6 +67,17 @@ class Plan(C.Structure):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
+VP_MAX_RANKS = 8
+
+
+class VpComm(C.Structure):
+    """grpo_vp_comm_t: the vocabulary-parallel group (device pointers as integers)."""
+    _fields_ = [("world", C.c_int32), ("rank_begin", C.c_int32), ("n_local", C.c_int32),
+                ("shard_cols", C.c_int32), ("logits", C.c_void_p * VP_MAX_RANKS),
+                ("dlogits", C.c_void_p * VP_MAX_RANKS), ("xbuf", C.c_void_p * VP_MAX_RANKS),
+                ("flags", C.c_void_p * VP_MAX_RANKS), ("epoch", C.c_uint32)]
+
+
 class GrpoError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 6 else status}: {msg}")
@@ -96,6 +107,9 @@ def _load():
     lib.grpo_async_loss_fwd_ex.argtypes = [P, i64, i64, i32, i64, P, P, P, i32, P, P, P, P, f32,
                                            P, P, P, P, P, P, P, sz, P, P]
     lib.grpo_async_loss_fwd_ex.restype = st
+    lib.grpo_async_loss_fwd_vp.argtypes = [P, i64, i64, i32, i64, P, P, P, i32, P, P, P, P, f32,
+                                           P, P, P, P, P, P, sz, P]
+    lib.grpo_async_loss_fwd_vp.restype = st
     lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
     lib.grpo_async_loss_bwd.restype = st
     lib.grpo_async_workspace_size.argtypes = [i64, i32, i32]
@@ -282,6 +296,47 @@ def grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav
         _ptr(traj_sum, torch.float64, "traj_sum"), _ptr(stats, torch.float64, "stats"),
         _ptr(dlogits, None, "dlogits"), _ptr(workspace, torch.uint8, "workspace"),
         workspace.numel() if workspace is not None else 0, tune_p, _stream(stream)))
+
+
+def _addr(x, name):
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        return _ptr(x, None, name)
+    return int(x)
+
+
+def grpo_async_loss_fwd_vp(world, rank_begin, shard_cols, logits, dlogits, xbuf, flags, epoch,
+                           row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens, N,
+                           traj_index, adv, inv_norm, eps_lo, eps_hi, norm, traj_mask, grad_scale,
+                           logp_out, lse_out, token_scale_out, traj_sum, stats, workspace,
+                           stream=None):
+    """logits / dlogits: the n_local local shards (bf16 tensors or raw device addresses);
+    xbuf / flags: all `world` exchange buffers as seen from this process (peer addresses)."""
+    n_local = len(logits)
+    if len(xbuf) != world or len(flags) != world or world > VP_MAX_RANKS:
+        raise ValueError("xbuf/flags need one entry per rank, world <= 8")
+    dl = list(dlogits) if dlogits is not None else [None] * n_local
+    c = VpComm()
+    c.world, c.rank_begin, c.n_local, c.shard_cols, c.epoch = world, rank_begin, n_local, \
+        shard_cols, epoch
+    for i in range(n_local):
+        c.logits[i] = _addr(logits[i], "logits")
+        c.dlogits[i] = _addr(dl[i], "dlogits")
+    for q in range(world):
+        c.xbuf[q] = _addr(xbuf[q], "xbuf")
+        c.flags[q] = _addr(flags[q], "flags")
+    o = _opts(eps_lo, eps_hi, norm, traj_mask)
+    _check(LIB.grpo_async_loss_fwd_vp(
+        C.byref(c), row_begin, n_rows, V, ld,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(logp_behav, torch.float32, "logp_behav"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, _ptr(traj_index, torch.int32, "traj_index"),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"), C.byref(o),
+        float(grad_scale), _ptr(logp_out, torch.float32, "logp_out"),
+        _ptr(lse_out, torch.float32, "lse_out"), _ptr(token_scale_out, torch.float32, "token_scale_out"),
+        _ptr(traj_sum, torch.float64, "traj_sum"), _ptr(stats, torch.float64, "stats"),
+        _ptr(workspace, torch.uint8, "workspace"),
+        workspace.numel() if workspace is not None else 0, _stream(stream)))
 
 
 def grpo_async_loss_bwd(logits, n_rows, V, ld, target_ids, lse, token_scale, grad_scale_mult,

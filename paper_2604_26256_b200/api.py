@@ -146,11 +146,77 @@ class GrpoAsyncLoss:
                                      self.tune, stream)
         self.launches += L.grpo_last_launch_count()
 
+    # ---- fused loss over vocabulary-parallel logits
+    def loss_chunk_vp(self, comm, shards, row_begin, n_rows, target_ids, logp_behav, cu_seqlens,
+                      adv, inv_norm, traj_sum, stats, dshards=None, traj_index=None,
+                      logp_out=None, lse_out=None, scale_out=None, V=None, stream=None):
+        """comm: VpGroup; shards / dshards: this process's local shard tensors [n_rows, ld]."""
+        ld = shards[0].shape[1]
+        N = cu_seqlens.numel() - 1
+        V = V if V is not None else comm.world * comm.shard_cols
+        ws = self.workspace(n_rows, V, N, shards[0].device)
+        L.grpo_async_loss_fwd_vp(comm.world, comm.rank_begin, comm.shard_cols, shards, dshards,
+                                 comm.xbuf, comm.flags, comm.epoch, row_begin, n_rows, V, ld,
+                                 target_ids, logp_behav, cu_seqlens, N, traj_index, adv, inv_norm,
+                                 self.eps, self.eps_hi, self.norm, self.traj_mask, self.grad_scale,
+                                 logp_out, lse_out, scale_out, traj_sum, stats, ws, stream)
+        comm.epoch += 1
+        self.launches += L.grpo_last_launch_count()
+
     def loss_bwd(self, logits, n_rows, V, target_ids, lse, token_scale, dlogits, mult=1.0,
                  stream=None):
         L.grpo_async_loss_bwd(logits, n_rows, V, logits.shape[1], target_ids, lse, token_scale,
                               mult, dlogits, stream)
         self.launches += L.grpo_last_launch_count()
+
+
+class VpGroup:
+    """Exchange buffers of a vocabulary-parallel group (grpo_vp_comm_t without the logits).
+
+    xbuf[q] (>= max_rows * world * 16 B) and flags[q] (uint32 [max_rows], zeroed once)
+    belong to rank q; every process holds all `world` addresses (its own plus peer
+    mappings).  `local(...)` builds the single-GPU group in which one process runs all
+    ranks; `from_symmetric(...)` maps the buffers of a torch.distributed group through
+    torch symmetric memory (NVLink peer pointers).  epoch counts the calls made.
+    """
+
+    def __init__(self, world, rank_begin, shard_cols, xbuf, flags, keep=()):
+        self.world, self.rank_begin, self.shard_cols = world, rank_begin, shard_cols
+        self.xbuf, self.flags = list(xbuf), list(flags)
+        self.epoch = 0
+        self._keep = keep
+
+    @staticmethod
+    def shard_cols_for(V, world):
+        return -(-V // (world * 8)) * 8
+
+    @staticmethod
+    def local(world, V, max_rows, device, shard_cols=None):
+        sc = shard_cols or VpGroup.shard_cols_for(V, world)
+        xb = [torch.empty(max(max_rows, 1) * world * 4, dtype=torch.float32, device=device)
+              for _ in range(world)]
+        fl = [torch.zeros(max(max_rows, 1), dtype=torch.int32, device=device) for _ in range(world)]
+        return VpGroup(world, 0, sc, [x.data_ptr() for x in xb], [f.data_ptr() for f in fl],
+                       keep=(xb, fl))
+
+    @staticmethod
+    def from_symmetric(V, max_rows, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        sc = VpGroup.shard_cols_for(V, world)
+        n_x = max(max_rows, 1) * world * 4
+        buf = symm.empty(n_x + max(max_rows, 1) + 64, dtype=torch.float32, device=device)
+        buf[n_x:].view(torch.int32).zero_()
+        h = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+        xb, fl = [], []
+        for q in range(world):
+            peer = h.get_buffer(q, (n_x + max(max_rows, 1),), torch.float32)
+            xb.append(peer.data_ptr())
+            fl.append(peer.data_ptr() + n_x * 4)
+        torch.cuda.synchronize(device)
+        dist.barrier(group)
+        return VpGroup(world, rank, sc, xb, fl, keep=(buf, h))
 
 
 def lpt_partition(lengths, world_size):

@@ -335,6 +335,94 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     return ok(launches);
 }
 
+grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_begin,
+                                     int64_t n_rows, int32_t V, int64_t ld,
+                                     const int64_t *target_ids, const float *logp_behav,
+                                     const int64_t *cu_seqlens, int32_t N,
+                                     const int32_t *traj_index, const float *adv,
+                                     const float *inv_norm, const grpo_loss_opts_t *opts,
+                                     float grad_scale, float *logp_out, float *lse_out,
+                                     float *token_scale_out, double *traj_sum, double *stats,
+                                     void *workspace, size_t workspace_bytes,
+                                     grpo_stream_t stream) {
+    if (!comm || !opts) return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: NULL comm/opts");
+    if (comm->world < 1 || comm->world > GRPO_VP_MAX_RANKS || comm->n_local < 1 ||
+        comm->rank_begin < 0 || comm->rank_begin + comm->n_local > comm->world)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: world=%d rank_begin=%d n_local=%d",
+                    comm->world, comm->rank_begin, comm->n_local);
+    if (comm->shard_cols <= 0 || comm->shard_cols % 8 != 0 ||
+        (int64_t)comm->shard_cols * comm->world < V)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: shard_cols=%d (multiple of 8, world*shard_cols >= V=%d)",
+                    comm->shard_cols, V);
+    if (n_rows < 0 || N <= 0 || V <= 0 || row_begin < 0)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: n_rows/N/V/row_begin");
+    if (!(opts->eps_lo > 0.0f && opts->eps_lo < 1.0f) || !(opts->eps_hi > 0.0f))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: eps_lo not in (0,1) or eps_hi <= 0");
+    if (!cu_seqlens || !adv || !inv_norm || !traj_sum || !stats)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: NULL cu_seqlens/adv/inv_norm/traj_sum/stats");
+    if (n_rows > 0 && (!target_ids || !logp_behav))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: NULL target_ids/logp_behav");
+    if (ld < comm->shard_cols || ld % 8 != 0)
+        return fail(GRPO_ERR_ALIGNMENT, "loss_fwd_vp: ld=%lld < shard_cols or not a multiple of 8",
+                    (long long)ld);
+    for (int q = 0; q < comm->n_local; ++q) {
+        if (!comm->logits[q]) return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: NULL logits[%d]", q);
+        if (!aligned16(comm->logits[q]) || (comm->dlogits[q] && !aligned16(comm->dlogits[q])))
+            return fail(GRPO_ERR_ALIGNMENT, "loss_fwd_vp: logits/dlogits[%d] not 16-byte aligned", q);
+    }
+    for (int q = 0; q < comm->world; ++q)
+        if (!comm->xbuf[q] || !comm->flags[q] || !aligned16(comm->xbuf[q]))
+            return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: xbuf/flags[%d] NULL or misaligned", q);
+    const size_t need = grpo_async_workspace_size(n_rows, V, N);
+    if (!workspace || workspace_bytes < need)
+        return fail(GRPO_ERR_WORKSPACE, "loss_fwd_vp: workspace %zu B < required %zu B",
+                    workspace_bytes, need);
+    grpo::LossArgs a{};
+    a.ld = ld;
+    a.V = V;
+    a.row_begin = row_begin;
+    a.n_rows = n_rows;
+    a.target_ids = target_ids;
+    a.logp_behav = logp_behav;
+    a.cu_seqlens = cu_seqlens;
+    a.N = N;
+    a.traj_index = traj_index;
+    a.adv = adv;
+    a.inv_norm = inv_norm;
+    a.eps_lo = opts->eps_lo;
+    a.eps_hi = opts->eps_hi;
+    a.grad_scale = grad_scale;
+    a.logp_out = logp_out;
+    a.lse_out = lse_out;
+    a.scale_out = token_scale_out;
+    a.traj_sum = traj_sum;
+    a.stats = stats;
+    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
+    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
+    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
+    a.term_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.logp_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.flag_ws = w;
+    w += align256((size_t)n_rows);
+    a.part_ws = reinterpret_cast<double *>(w);
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_rowinfo(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/rowinfo");
+    const bool traced = n_rows > 0 && prof_on();
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/profile");
+    e = grpo::launch_vp(a, comm, s, &launches, &g_last_plan, why, sizeof why);
+    if (e != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/vp_kernel", why);
+    if (traced && (e = prof_end(s, ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/profile");
+    e = grpo::launch_segment_reduce(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/segment_reduce");
+    return ok(launches);
+}
+
 grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
                                   const int64_t *target_ids, const float *lse,
                                   const float *token_scale, float grad_scale_mult,

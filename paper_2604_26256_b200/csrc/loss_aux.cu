@@ -9,6 +9,7 @@
 //                       J's chunk contribution  sum_i inv_norm_i * sum_t term_t
 //   bwd_kernel          unfused backward: dlogits = s (exp(z - lse) - onehot)
 #include "common.cuh"
+#include "rowwise.cuh"
 
 namespace grpo {
 
@@ -71,40 +72,6 @@ struct RowwiseParams {
     int32_t cache_vecs;  // leading vectors per thread kept in shared memory for pass 2
 };
 
-template <int NT, int U>
-struct RowwiseBatch {
-    // log2-domain partial of U vectors (already loaded and masked)
-    static __device__ __forceinline__ void reduce(const uint4 (&x)[U], float &a, float &s) {
-        uint32_t mx2 = kBf16NegInfPair;
-#pragma unroll
-        for (int j = 0; j < U; ++j)
-            mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
-        const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
-        if (va == -INFINITY) return;
-        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
-#pragma unroll
-        for (int j = 0; j < U; ++j) {
-            t0 += ex2(fmaf(bf_lo(x[j].x), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].x), kLog2e, -va));
-            t1 += ex2(fmaf(bf_lo(x[j].y), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].y), kLog2e, -va));
-            t2 += ex2(fmaf(bf_lo(x[j].z), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].z), kLog2e, -va));
-            t3 += ex2(fmaf(bf_lo(x[j].w), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].w), kLog2e, -va));
-        }
-        lse2_merge(a, s, va, (t0 + t1) + (t2 + t3));
-    }
-    // s * 2^(z*log2e - lse2) for the 8 elements of one vector, packed to bf16
-    static __device__ __forceinline__ uint4 grad(const uint4 &x, float sc, float lse2) {
-        uint4 d;
-        d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.x), kLog2e, -lse2)),
-                          sc * ex2(fmaf(bf_hi(x.x), kLog2e, -lse2)));
-        d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.y), kLog2e, -lse2)),
-                          sc * ex2(fmaf(bf_hi(x.y), kLog2e, -lse2)));
-        d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.z), kLog2e, -lse2)),
-                          sc * ex2(fmaf(bf_hi(x.z), kLog2e, -lse2)));
-        d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.w), kLog2e, -lse2)),
-                          sc * ex2(fmaf(bf_hi(x.w), kLog2e, -lse2)));
-        return d;
-    }
-};
 
 // Row-wise two-pass kernel.  A row (or, with C > 1, a 1/C slice of it held by one
 // CTA of a C-CTA cluster) is processed by one CTA at a time; the grid is

@@ -1,0 +1,45 @@
+// rowwise.cuh -- per-batch math shared by the row-wise loss kernels (loss_aux.cu,
+// loss_vp.cu): the log2-domain softmax partial of U 8-element vectors and the
+// gradient s * 2^(z*log2e - lse2) of one vector packed to bf16.
+#pragma once
+
+#include "common.cuh"
+
+namespace grpo {
+
+template <int NT, int U>
+struct RowwiseBatch {
+    // log2-domain partial of U vectors (already loaded and masked)
+    static __device__ __forceinline__ void reduce(const uint4 (&x)[U], float &a, float &s) {
+        uint32_t mx2 = kBf16NegInfPair;
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+            mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
+        const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
+        if (va == -INFINITY) return;
+        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            t0 += ex2(fmaf(bf_lo(x[j].x), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].x), kLog2e, -va));
+            t1 += ex2(fmaf(bf_lo(x[j].y), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].y), kLog2e, -va));
+            t2 += ex2(fmaf(bf_lo(x[j].z), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].z), kLog2e, -va));
+            t3 += ex2(fmaf(bf_lo(x[j].w), kLog2e, -va)) + ex2(fmaf(bf_hi(x[j].w), kLog2e, -va));
+        }
+        lse2_merge(a, s, va, (t0 + t1) + (t2 + t3));
+    }
+    // s * 2^(z*log2e - lse2) for the 8 elements of one vector, packed to bf16
+    static __device__ __forceinline__ uint4 grad(const uint4 &x, float sc, float lse2) {
+        uint4 d;
+        d.x = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.x), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.x), kLog2e, -lse2)));
+        d.y = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.y), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.y), kLog2e, -lse2)));
+        d.z = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.z), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.z), kLog2e, -lse2)));
+        d.w = pack_bf16x2(sc * ex2(fmaf(bf_lo(x.w), kLog2e, -lse2)),
+                          sc * ex2(fmaf(bf_hi(x.w), kLog2e, -lse2)));
+        return d;
+    }
+};
+
+}  // namespace grpo

@@ -142,3 +142,62 @@ def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5,
             expect = logits_pad if gpu["inplace"] else np.uint16(0x7FC3)
             assert np.all(pad == expect), "padding columns of dlogits were written"
     return errs
+
+
+def run_gpu_vp(batch, logits_bits, device, world, chunks=1, grad_scale=1.0, eps=0.2,
+               eps_hi=None, norm="seq", traj_mask=None, want_dlogits=True, calls=1,
+               shard_cols=None):
+    """The vocabulary-parallel path (NEXT(3)) with all `world` ranks in one cooperative
+    launch on one GPU: the logits are cut into world column shards of shard_cols columns,
+    the per-rank dlogits shards are re-assembled into [T, ld] (padding left 0x7FC3).
+    `calls` > 1 repeats the whole loss on the same exchange buffers (epoch counting)."""
+    db = G.DeviceBatch.from_host(batch, device)
+    mask_d = None if traj_mask is None else torch.from_numpy(
+        np.ascontiguousarray(traj_mask, np.uint8)).to(device)
+    loss = G.GrpoAsyncLoss(eps=eps, grad_scale=grad_scale, eps_hi=eps_hi, norm=norm,
+                           traj_mask=mask_d)
+    vo = loss.validate(db)
+    adv, inv = loss.advantage(db)
+    T, ld, V = batch.T, batch.ld, batch.V
+    comm = G.VpGroup.local(world, V, T, device, shard_cols)
+    sc = comm.shard_cols
+    ld_s = sc  # shard row stride (a multiple of 8)
+    full = np.full((T, sc * world), 0x7FC1, np.uint16)
+    full[:, :V] = logits_bits[:, :V]
+    shards = [to_dev_bits(np.ascontiguousarray(full[:, q * sc:(q + 1) * sc]), device)
+              for q in range(world)]
+    assert all(s.shape == (T, ld_s) for s in shards)
+    bounds = np.linspace(0, T, chunks + 1).astype(np.int64)
+    for _ in range(calls):
+        dsh = [torch.full((T, ld_s), 0x7FC3, dtype=torch.int16, device=device)
+               for _ in range(world)] if want_dlogits else None
+        logp = torch.full((T,), float("nan"), device=device)
+        lse = torch.full((T,), float("nan"), device=device)
+        scale = torch.full((T,), float("nan"), device=device)
+        traj_sum = torch.zeros(batch.N, dtype=torch.float64, device=device)
+        stats = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=device)
+        for c in range(chunks):
+            b, e = int(bounds[c]), int(bounds[c + 1])
+            loss.loss_chunk_vp(comm, [s[b:e] for s in shards], b, e - b, db.target_ids[b:e],
+                               db.logp_behav[b:e], db.cu_seqlens, adv, inv, traj_sum, stats,
+                               dshards=[d[b:e] for d in dsh] if dsh else None,
+                               logp_out=logp[b:e], lse_out=lse[b:e], scale_out=scale[b:e], V=V)
+        torch.cuda.synchronize()
+    out = dict(
+        traj_flags=vo.traj_flags.cpu().numpy().view(np.uint32)[:batch.N],
+        group_count=vo.group_count.cpu().numpy(),
+        stale_hist=vo.stale_hist.cpu().numpy().reshape(batch.P, batch.K + 1),
+        summary=vo.summary_dict(),
+        adv=adv.cpu().numpy(), inv_norm=inv.cpu().numpy(),
+        logp=logp.cpu().numpy().astype(np.float64), lse=lse.cpu().numpy().astype(np.float64),
+        scale=scale.cpu().numpy().astype(np.float64),
+        traj_sum=traj_sum.cpu().numpy(), stats=stats.cpu().numpy(),
+        launches=loss.launches, inplace=False, epoch=comm.epoch)
+    if want_dlogits:
+        cat = np.concatenate([d.cpu().numpy().view(np.uint16) for d in dsh], axis=1)
+        raw = np.full((T, ld), 0x7FC3, np.uint16)
+        raw[:, :V] = cat[:, :V]
+        out["dlogits_raw"] = raw
+        out["dlogits"] = bf16_bits_to_f32(raw[:, :V]).astype(np.float64)
+        out["shard_pad_untouched"] = bool(np.all(cat[:, V:] == 0x7FC3))
+    return out

@@ -1,0 +1,58 @@
+"""-m gpu: NEXT(3) -- the fused loss over vocabulary-parallel logits
+(grpo_async_loss_fwd_vp, Megatron-style LM-head sharding) against the
+fp64 oracle on the unsharded row.  All ranks of the group run in one cooperative
+launch on one GPU (the same peer-memory exchange protocol as on R GPUs); the 2-GPU
+NVLink run is scripts/vp_multi_gpu.py."""
+import numpy as np
+import pytest
+
+from synth.gen import make_batch
+from tests.gpu_util import compare, run_gpu_vp, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+@pytest.mark.parametrize("name", ["tiny", "mid32k", "mid152k", "ragged"])
+def test_vp_parity(dev, name, world):
+    b = make_batch(name, 5)
+    bits = b.logits_bits()
+    ref = run_oracle(b, bits)
+    gpu = run_gpu_vp(b, bits, dev, world)
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+    assert gpu["shard_pad_untouched"]
+
+
+def test_vp_chunks_and_epochs(dev):
+    """Several row chunks and repeated calls on the same exchange buffers (counters are
+    never reset: call e waits for (e+1)*R arrivals)."""
+    b = make_batch("mid32k", 6)
+    bits = b.logits_bits()
+    ref = run_oracle(b, bits)
+    gpu = run_gpu_vp(b, bits, dev, 4, chunks=3, calls=3)
+    assert gpu["epoch"] == 9
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+
+
+@pytest.mark.parametrize("opts", [dict(eps_hi=0.28, norm="token")])
+def test_vp_dapo(dev, opts):
+    b = make_batch("ragged", 7)
+    bits = b.logits_bits()
+    mask = (b.lengths < np.percentile(b.lengths, 80)).astype(np.uint8)
+    ref = run_oracle(b, bits, traj_mask=mask, **opts)
+    gpu = run_gpu_vp(b, bits, dev, 2, traj_mask=mask, **opts)
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:], eps_hi=opts["eps_hi"])
+
+
+def test_vp_forward_only_and_empty_shards(dev):
+    """dlogits NULL (forward only), and shard_cols = 512 over V = 1024 with world 4:
+    shards 2 and 3 hold no column (their partial is (-inf, 0)) yet take part in the
+    exchange."""
+    b = make_batch("tiny", 8)
+    bits = b.logits_bits()
+    ref = run_oracle(b, bits, want_dlogits=False)
+    gpu = run_gpu_vp(b, bits, dev, 8, want_dlogits=False)
+    compare(gpu, ref, b, check_dlogits=False)
+    ref = run_oracle(b, bits)
+    gpu = run_gpu_vp(b, bits, dev, 4, shard_cols=512)
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
