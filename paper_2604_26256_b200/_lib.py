@@ -73,7 +73,7 @@ VP_MAX_RANKS = 8
 class VpComm(C.Structure):
     """grpo_vp_comm_t: the vocabulary-parallel group (device pointers as integers)."""
     _fields_ = [("world", C.c_int32), ("rank_begin", C.c_int32), ("n_local", C.c_int32),
-                ("shard_cols", C.c_int32), ("logits", C.c_void_p * VP_MAX_RANKS),
+                ("shard_cols", C.c_int32), ("slots", C.c_int64), ("logits", C.c_void_p * VP_MAX_RANKS),
                 ("dlogits", C.c_void_p * VP_MAX_RANKS), ("xbuf", C.c_void_p * VP_MAX_RANKS),
                 ("flags", C.c_void_p * VP_MAX_RANKS), ("epoch", C.c_uint32)]
 
@@ -306,20 +306,21 @@ def _addr(x, name):
     return int(x)
 
 
-def grpo_async_loss_fwd_vp(world, rank_begin, shard_cols, logits, dlogits, xbuf, flags, epoch,
+def grpo_async_loss_fwd_vp(world, rank_begin, shard_cols, slots, logits, dlogits, xbuf, flags, epoch,
                            row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens, N,
                            traj_index, adv, inv_norm, eps_lo, eps_hi, norm, traj_mask, grad_scale,
                            logp_out, lse_out, token_scale_out, traj_sum, stats, workspace,
                            stream=None):
     """logits / dlogits: the n_local local shards (bf16 tensors or raw device addresses);
-    xbuf / flags: all `world` exchange buffers as seen from this process (peer addresses)."""
+    xbuf / flags: all `world` exchange buffers as seen from this process (peer addresses),
+    each with 2 * slots row slots."""
     n_local = len(logits)
     if len(xbuf) != world or len(flags) != world or world > VP_MAX_RANKS:
         raise ValueError("xbuf/flags need one entry per rank, world <= 8")
     dl = list(dlogits) if dlogits is not None else [None] * n_local
     c = VpComm()
-    c.world, c.rank_begin, c.n_local, c.shard_cols, c.epoch = world, rank_begin, n_local, \
-        shard_cols, epoch
+    c.world, c.rank_begin, c.n_local, c.shard_cols, c.slots, c.epoch = world, rank_begin, \
+        n_local, shard_cols, slots, epoch
     for i in range(n_local):
         c.logits[i] = _addr(logits[i], "logits")
         c.dlogits[i] = _addr(dl[i], "dlogits")

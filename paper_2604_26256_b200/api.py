@@ -155,7 +155,8 @@ class GrpoAsyncLoss:
         N = cu_seqlens.numel() - 1
         V = V if V is not None else comm.world * comm.shard_cols
         ws = self.workspace(n_rows, V, N, shards[0].device)
-        L.grpo_async_loss_fwd_vp(comm.world, comm.rank_begin, comm.shard_cols, shards, dshards,
+        L.grpo_async_loss_fwd_vp(comm.world, comm.rank_begin, comm.shard_cols, comm.slots,
+                                 shards, dshards,
                                  comm.xbuf, comm.flags, comm.epoch, row_begin, n_rows, V, ld,
                                  target_ids, logp_behav, cu_seqlens, N, traj_index, adv, inv_norm,
                                  self.eps, self.eps_hi, self.norm, self.traj_mask, self.grad_scale,
@@ -173,15 +174,17 @@ class GrpoAsyncLoss:
 class VpGroup:
     """Exchange buffers of a vocabulary-parallel group (grpo_vp_comm_t without the logits).
 
-    xbuf[q] (>= max_rows * world * 16 B) and flags[q] (uint32 [max_rows], zeroed once)
-    belong to rank q; every process holds all `world` addresses (its own plus peer
+    xbuf[q] (2 * slots * world * 16 B) and flags[q] (uint32 [2 * slots], zeroed once)
+    belong to rank q (slots = the most rows one call may process; two halves so that
+    consecutive calls never share a slot); every process holds all `world` addresses (its own plus peer
     mappings).  `local(...)` builds the single-GPU group in which one process runs all
     ranks; `from_symmetric(...)` maps the buffers of a torch.distributed group through
     torch symmetric memory (NVLink peer pointers).  epoch counts the calls made.
     """
 
-    def __init__(self, world, rank_begin, shard_cols, xbuf, flags, keep=()):
+    def __init__(self, world, rank_begin, shard_cols, slots, xbuf, flags, keep=()):
         self.world, self.rank_begin, self.shard_cols = world, rank_begin, shard_cols
+        self.slots = slots
         self.xbuf, self.flags = list(xbuf), list(flags)
         self.epoch = 0
         self._keep = keep
@@ -193,11 +196,12 @@ class VpGroup:
     @staticmethod
     def local(world, V, max_rows, device, shard_cols=None):
         sc = shard_cols or VpGroup.shard_cols_for(V, world)
-        xb = [torch.empty(max(max_rows, 1) * world * 4, dtype=torch.float32, device=device)
+        slots = max(max_rows, 1)
+        xb = [torch.empty(2 * slots * world * 4, dtype=torch.float32, device=device)
               for _ in range(world)]
-        fl = [torch.zeros(max(max_rows, 1), dtype=torch.int32, device=device) for _ in range(world)]
-        return VpGroup(world, 0, sc, [x.data_ptr() for x in xb], [f.data_ptr() for f in fl],
-                       keep=(xb, fl))
+        fl = [torch.zeros(2 * slots, dtype=torch.int32, device=device) for _ in range(world)]
+        return VpGroup(world, 0, sc, slots, [x.data_ptr() for x in xb],
+                       [f.data_ptr() for f in fl], keep=(xb, fl))
 
     @staticmethod
     def from_symmetric(V, max_rows, device, group=None):
@@ -205,18 +209,19 @@ class VpGroup:
         import torch.distributed._symmetric_memory as symm
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         sc = VpGroup.shard_cols_for(V, world)
-        n_x = max(max_rows, 1) * world * 4
-        buf = symm.empty(n_x + max(max_rows, 1) + 64, dtype=torch.float32, device=device)
+        slots = max(max_rows, 1)
+        n_x = 2 * slots * world * 4
+        buf = symm.empty(n_x + 2 * slots + 64, dtype=torch.float32, device=device)
         buf[n_x:].view(torch.int32).zero_()
         h = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
         xb, fl = [], []
         for q in range(world):
-            peer = h.get_buffer(q, (n_x + max(max_rows, 1),), torch.float32)
+            peer = h.get_buffer(q, (n_x + 2 * slots,), torch.float32)
             xb.append(peer.data_ptr())
             fl.append(peer.data_ptr() + n_x * 4)
         torch.cuda.synchronize(device)
         dist.barrier(group)
-        return VpGroup(world, rank, sc, xb, fl, keep=(buf, h))
+        return VpGroup(world, rank, sc, slots, xb, fl, keep=(buf, h))
 
 
 def lpt_partition(lengths, world_size):

@@ -356,6 +356,9 @@ grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_beg
                     comm->shard_cols, V);
     if (n_rows < 0 || N <= 0 || V <= 0 || row_begin < 0)
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: n_rows/N/V/row_begin");
+    if (comm->slots < n_rows)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: n_rows=%lld > comm->slots=%lld",
+                    (long long)n_rows, (long long)comm->slots);
     if (!(opts->eps_lo > 0.0f && opts->eps_lo < 1.0f) || !(opts->eps_hi > 0.0f))
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: eps_lo not in (0,1) or eps_hi <= 0");
     if (!cu_seqlens || !adv || !inv_norm || !traj_sum || !stats)

@@ -14,7 +14,8 @@
 //
 // Each rank's CTA g walks the same row sequence, so a row's partials are produced
 // at about the same time on all ranks; a CTA waits on its peers for at most one row.
-// Counters are never reset: call number e on a buffer set expects (e+1)*R arrivals.
+// Call e uses half e % 2 of the buffers and each rank re-zeroes its own counter of a
+// row once it has read the row's partials (the protocol argument is at the re-arm).
 // With fewer GPUs than ranks, one launch runs several ranks (n_local > 1) as a
 // cooperative grid over one GPU's memory -- the protocol is identical.
 #include <cstdio>
@@ -30,7 +31,7 @@ struct VpParams {
     uint16_t *dlogits[GRPO_VP_MAX_RANKS];
     float4 *xbuf[GRPO_VP_MAX_RANKS];
     uint32_t *flags[GRPO_VP_MAX_RANKS];
-    uint32_t target;  // arrivals that complete a row on this call: (epoch + 1) * world
+    int64_t half;     // (epoch % 2) * slots: the half of xbuf / flags this call uses
     int64_t ld;
     int32_t V;
     int64_t n_rows;
@@ -127,17 +128,18 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
             const bool mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
             const float zy = mine ? __uint_as_float(((uint32_t)zrow[y_loc]) << 16) : 0.0f;
             // ---- the exchange: this rank's partial into row `row` of every rank's buffer
+            const int64_t slot = p.half + row;
             if (lane < p.world) {
-                float4 *dst = p.xbuf[lane] + row * p.world + rank;
+                float4 *dst = p.xbuf[lane] + slot * p.world + rank;
                 asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst),
                              "f"(cm), "f"(cs), "f"(zy), "f"(mine ? 1.0f : 0.0f)
                              : "memory");
                 __threadfence_system();
-                atomicAdd_system(p.flags[lane] + row, 1u);
+                atomicAdd_system(p.flags[lane] + slot, 1u);
                 // wait for all world partials of this row in this rank's buffer
-                const uint32_t *f = p.flags[rank] + row;
+                const uint32_t *f = p.flags[rank] + slot;
                 long long spins = 0;
-                while (ld_acquire_sys(f) < p.target) {
+                while (ld_acquire_sys(f) < (uint32_t)p.world) {
                     __nanosleep(64);
                     if (++spins > (1ll << 27)) __trap();  // a peer never arrived: fail, don't hang
                 }
@@ -146,12 +148,19 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
             float M = -INFINITY, S = 0.0f, zsrc = 0.0f;
             bool own = false;
             if (lane < p.world) {
-                const float4 m4 = ld_relaxed_sys_v4(p.xbuf[rank] + row * p.world + lane);
+                const float4 m4 = ld_relaxed_sys_v4(p.xbuf[rank] + slot * p.world + lane);
                 M = m4.x;
                 S = m4.y;
                 zsrc = m4.z;
                 own = m4.w != 0.0f;
             }
+            __syncwarp();
+            // re-arm this rank's counter.  The next arrival on this slot belongs to call
+            // e+2, which a peer can only start after seeing this rank's partial of call
+            // e+1 -- released (fence.sc.sys) after this store in program order.
+            if (lane == 0)
+                asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p.flags[rank] + slot), "r"(0u)
+                             : "memory");
             warp_lse2_combine(M, S);  // same inputs in the same lanes on every rank
             const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
             const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
@@ -248,7 +257,7 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, cudaStream_
         p.xbuf[q] = static_cast<float4 *>(comm->xbuf[q]);
         p.flags[q] = comm->flags[q];
     }
-    p.target = (comm->epoch + 1u) * (uint32_t)comm->world;
+    p.half = (int64_t)(comm->epoch & 1u) * comm->slots;
     p.ld = a.ld;
     p.V = a.V;
     p.n_rows = a.n_rows;
