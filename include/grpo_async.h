@@ -254,13 +254,13 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
  *   (n_local = 1 on a multi-GPU run; n_local = R when one GPU runs the whole group as a
  *   cooperative grid); shard_cols % 8 == 0; logits[i] / dlogits[i] bf16 [n_rows, ld] of
  *   local rank i (ld >= shard_cols, 16-byte aligned; dlogits may be NULL = forward only);
- *   xbuf[q] >= 2*slots*world*16 bytes and flags[q] uint32[2*slots] of EVERY rank q,
- *   mapped into this process (peer pointers); flags zero-initialised once (each rank
- *   re-zeroes its own counter of a row after reading it); slots >= n_rows; epoch = number
- *   of earlier calls on these buffers (the same on every rank): call e uses the half
- *   e % 2, so a fast rank's next call never overwrites a partial a slow rank has not yet
- *   read.  All ranks must call with the same arguments except the pointers they own; a
- *   rank whose peers never arrive traps (GRPO_ERR_CUDA, context lost).
+ *   xbuf[q] >= 2*slots*world*32 bytes of EVERY rank q, mapped into this process (peer
+ *   pointers), zero-initialised once; slots >= n_rows; epoch = number of earlier calls
+ *   on these buffers (the same on every rank): call e uses the half e % 2 and tags its
+ *   words with e + 1, so a fast rank's next call never overwrites a partial a slow rank
+ *   has not yet read and stale words are never mistaken for new ones.  All ranks must
+ *   call with the same arguments except the pointers they own; a rank whose peers never
+ *   arrive traps (GRPO_ERR_CUDA, context lost).
  * Other arguments as grpo_async_loss_fwd_ex (per-row outputs written by local rank 0).
  * Errors: GRPO_ERR_INVALID_ARG (bad comm, NULL pointers), GRPO_ERR_ALIGNMENT,
  *   GRPO_ERR_WORKSPACE, GRPO_ERR_CUDA.
@@ -275,8 +275,11 @@ typedef struct {
     const uint16_t *logits[GRPO_VP_MAX_RANKS];
     uint16_t *dlogits[GRPO_VP_MAX_RANKS];
     void *xbuf[GRPO_VP_MAX_RANKS];
-    uint32_t *flags[GRPO_VP_MAX_RANKS];
     uint32_t epoch;
+    int32_t lag;  /* 1 (default): wait for row k-1's partials after pass 1 of row k; 0: wait
+                     right after each row's pass 1 (same results, bit for bit) */
+    int32_t static_rows; /* 0 (default): CTAs take rows in the order they ask for them;
+                            1: CTA g takes rows g, g + grid, ... (same results) */
 } grpo_vp_comm_t;
 
 grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_begin,

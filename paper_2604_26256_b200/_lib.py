@@ -75,7 +75,7 @@ class VpComm(C.Structure):
     _fields_ = [("world", C.c_int32), ("rank_begin", C.c_int32), ("n_local", C.c_int32),
                 ("shard_cols", C.c_int32), ("slots", C.c_int64), ("logits", C.c_void_p * VP_MAX_RANKS),
                 ("dlogits", C.c_void_p * VP_MAX_RANKS), ("xbuf", C.c_void_p * VP_MAX_RANKS),
-                ("flags", C.c_void_p * VP_MAX_RANKS), ("epoch", C.c_uint32)]
+                ("epoch", C.c_uint32), ("lag", C.c_int32), ("static_rows", C.c_int32)]
 
 
 class GrpoError(RuntimeError):
@@ -306,27 +306,28 @@ def _addr(x, name):
     return int(x)
 
 
-def grpo_async_loss_fwd_vp(world, rank_begin, shard_cols, slots, logits, dlogits, xbuf, flags, epoch,
+def grpo_async_loss_fwd_vp(world, rank_begin, shard_cols, slots, logits, dlogits, xbuf, epoch,
                            row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens, N,
                            traj_index, adv, inv_norm, eps_lo, eps_hi, norm, traj_mask, grad_scale,
                            logp_out, lse_out, token_scale_out, traj_sum, stats, workspace,
-                           stream=None):
+                           stream=None, lag=1, static_rows=0):
     """logits / dlogits: the n_local local shards (bf16 tensors or raw device addresses);
-    xbuf / flags: all `world` exchange buffers as seen from this process (peer addresses),
-    each with 2 * slots row slots."""
+    xbuf: all `world` exchange buffers as seen from this process (peer addresses), each
+    2 * slots * world * 32 bytes."""
     n_local = len(logits)
-    if len(xbuf) != world or len(flags) != world or world > VP_MAX_RANKS:
-        raise ValueError("xbuf/flags need one entry per rank, world <= 8")
+    if len(xbuf) != world or world > VP_MAX_RANKS:
+        raise ValueError("xbuf needs one entry per rank, world <= 8")
     dl = list(dlogits) if dlogits is not None else [None] * n_local
     c = VpComm()
     c.world, c.rank_begin, c.n_local, c.shard_cols, c.slots, c.epoch = world, rank_begin, \
         n_local, shard_cols, slots, epoch
+    c.lag = int(lag)
+    c.static_rows = int(static_rows)
     for i in range(n_local):
         c.logits[i] = _addr(logits[i], "logits")
         c.dlogits[i] = _addr(dl[i], "dlogits")
     for q in range(world):
         c.xbuf[q] = _addr(xbuf[q], "xbuf")
-        c.flags[q] = _addr(flags[q], "flags")
     o = _opts(eps_lo, eps_hi, norm, traj_mask)
     _check(LIB.grpo_async_loss_fwd_vp(
         C.byref(c), row_begin, n_rows, V, ld,

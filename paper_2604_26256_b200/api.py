@@ -157,10 +157,11 @@ class GrpoAsyncLoss:
         ws = self.workspace(n_rows, V, N, shards[0].device)
         L.grpo_async_loss_fwd_vp(comm.world, comm.rank_begin, comm.shard_cols, comm.slots,
                                  shards, dshards,
-                                 comm.xbuf, comm.flags, comm.epoch, row_begin, n_rows, V, ld,
+                                 comm.xbuf, comm.epoch, row_begin, n_rows, V, ld,
                                  target_ids, logp_behav, cu_seqlens, N, traj_index, adv, inv_norm,
                                  self.eps, self.eps_hi, self.norm, self.traj_mask, self.grad_scale,
-                                 logp_out, lse_out, scale_out, traj_sum, stats, ws, stream)
+                                 logp_out, lse_out, scale_out, traj_sum, stats, ws, stream,
+                                 lag=comm.lag, static_rows=comm.static_rows)
         comm.epoch += 1
         self.launches += L.grpo_last_launch_count()
 
@@ -174,18 +175,20 @@ class GrpoAsyncLoss:
 class VpGroup:
     """Exchange buffers of a vocabulary-parallel group (grpo_vp_comm_t without the logits).
 
-    xbuf[q] (2 * slots * world * 16 B) and flags[q] (uint32 [2 * slots], zeroed once)
-    belong to rank q (slots = the most rows one call may process; two halves so that
-    consecutive calls never share a slot); every process holds all `world` addresses (its own plus peer
-    mappings).  `local(...)` builds the single-GPU group in which one process runs all
-    ranks; `from_symmetric(...)` maps the buffers of a torch.distributed group through
-    torch symmetric memory (NVLink peer pointers).  epoch counts the calls made.
+    xbuf[q] (2 * slots * world * 32 B, zeroed once) belongs to rank q (slots = the most
+    rows one call may process; two halves so that consecutive calls never share a
+    slot); every process holds all `world` addresses (its own plus peer mappings).
+    `local(...)` builds the single-GPU group in which one process runs all ranks;
+    `from_symmetric(...)` maps the buffers of a torch.distributed group through torch
+    symmetric memory (NVLink peer pointers).  epoch counts the calls made.
     """
 
-    def __init__(self, world, rank_begin, shard_cols, slots, xbuf, flags, keep=()):
+    def __init__(self, world, rank_begin, shard_cols, slots, xbuf, keep=()):
         self.world, self.rank_begin, self.shard_cols = world, rank_begin, shard_cols
         self.slots = slots
-        self.xbuf, self.flags = list(xbuf), list(flags)
+        self.lag = 1              # grpo_vp_comm_t.lag
+        self.static_rows = 0      # grpo_vp_comm_t.static_rows
+        self.xbuf = list(xbuf)
         self.epoch = 0
         self._keep = keep
 
@@ -194,14 +197,16 @@ class VpGroup:
         return -(-V // (world * 8)) * 8
 
     @staticmethod
+    def _words(slots, world):
+        return 2 * slots * world * 4  # int64 words
+
+    @staticmethod
     def local(world, V, max_rows, device, shard_cols=None):
         sc = shard_cols or VpGroup.shard_cols_for(V, world)
         slots = max(max_rows, 1)
-        xb = [torch.empty(2 * slots * world * 4, dtype=torch.float32, device=device)
+        xb = [torch.zeros(VpGroup._words(slots, world), dtype=torch.int64, device=device)
               for _ in range(world)]
-        fl = [torch.zeros(2 * slots, dtype=torch.int32, device=device) for _ in range(world)]
-        return VpGroup(world, 0, sc, slots, [x.data_ptr() for x in xb],
-                       [f.data_ptr() for f in fl], keep=(xb, fl))
+        return VpGroup(world, 0, sc, slots, [x.data_ptr() for x in xb], keep=(xb,))
 
     @staticmethod
     def from_symmetric(V, max_rows, device, group=None):
@@ -210,18 +215,14 @@ class VpGroup:
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         sc = VpGroup.shard_cols_for(V, world)
         slots = max(max_rows, 1)
-        n_x = 2 * slots * world * 4
-        buf = symm.empty(n_x + 2 * slots + 64, dtype=torch.float32, device=device)
-        buf[n_x:].view(torch.int32).zero_()
+        n = VpGroup._words(slots, world)
+        buf = symm.empty(n, dtype=torch.int64, device=device)
+        buf.zero_()
         h = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
-        xb, fl = [], []
-        for q in range(world):
-            peer = h.get_buffer(q, (n_x + 2 * slots,), torch.float32)
-            xb.append(peer.data_ptr())
-            fl.append(peer.data_ptr() + n_x * 4)
+        xb = [h.get_buffer(q, (n,), torch.int64).data_ptr() for q in range(world)]
         torch.cuda.synchronize(device)
         dist.barrier(group)
-        return VpGroup(world, rank, sc, slots, xb, fl, keep=(buf, h))
+        return VpGroup(world, rank, sc, slots, xb, keep=(buf, h))
 
 
 def lpt_partition(lengths, world_size):

@@ -132,7 +132,8 @@ size_t grpo_async_workspace_size(int64_t n_rows, int32_t V, int32_t N) {
     if (N < 0) N = 0;
     return align256((size_t)n_rows * sizeof(grpo::RowInfo)) + align256((size_t)n_rows * 4) +
            align256((size_t)n_rows * 4) + align256((size_t)n_rows) +
-           align256((size_t)N * 5 * sizeof(double)) + 256;
+           align256((size_t)N * 5 * sizeof(double)) +
+           align256(GRPO_VP_MAX_RANKS * sizeof(unsigned long long)) + 256;
 }
 
 grpo_status_t grpo_async_validate(const int64_t *version_ids, const int64_t *token_version,
@@ -374,8 +375,8 @@ grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_beg
             return fail(GRPO_ERR_ALIGNMENT, "loss_fwd_vp: logits/dlogits[%d] not 16-byte aligned", q);
     }
     for (int q = 0; q < comm->world; ++q)
-        if (!comm->xbuf[q] || !comm->flags[q] || !aligned16(comm->xbuf[q]))
-            return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: xbuf/flags[%d] NULL or misaligned", q);
+        if (!comm->xbuf[q] || !aligned16(comm->xbuf[q]))
+            return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: xbuf[%d] NULL or misaligned", q);
     const size_t need = grpo_async_workspace_size(n_rows, V, N);
     if (!workspace || workspace_bytes < need)
         return fail(GRPO_ERR_WORKSPACE, "loss_fwd_vp: workspace %zu B < required %zu B",
@@ -410,15 +411,19 @@ grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_beg
     a.flag_ws = w;
     w += align256((size_t)n_rows);
     a.part_ws = reinterpret_cast<double *>(w);
+    w += align256((size_t)N * 5 * sizeof(double));
+    unsigned long long *row_ctr = reinterpret_cast<unsigned long long *>(w);
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
     char why[256] = {0};
-    cudaError_t e = grpo::launch_rowinfo(a, s, &launches);
+    cudaError_t e = cudaMemsetAsync(row_ctr, 0, GRPO_VP_MAX_RANKS * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/memset");
+    e = grpo::launch_rowinfo(a, s, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/rowinfo");
     const bool traced = n_rows > 0 && prof_on();
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/profile");
-    e = grpo::launch_vp(a, comm, s, &launches, &g_last_plan, why, sizeof why);
+    e = grpo::launch_vp(a, comm, row_ctr, s, &launches, &g_last_plan, why, sizeof why);
     if (e != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/vp_kernel", why);
     if (traced && (e = prof_end(s, ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd_vp/profile");
     e = grpo::launch_segment_reduce(a, s, &launches);

@@ -393,7 +393,8 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
 cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
                                  int *launches, grpo_plan_t *plan);
 cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches);
-cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, cudaStream_t s, int *launches,
+cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned long long *row_ctr,
+                      cudaStream_t s, int *launches,
                       grpo_plan_t *plan, char *why, size_t why_len);
 cudaError_t launch_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
                             const int64_t *target_ids, const float *lse, const float *scale,

@@ -6,16 +6,17 @@
 // loss kernel over NVLink peer memory instead of a separate all-reduce:
 //
 //   pass 1 over the local shard (as rowwise_kernel) -> (a, s, z_y?) -> warp 0 stores
-//   the 16-byte partial into row t's slot of EVERY rank's exchange buffer (peer
-//   pointers) and, after a system-scope fence, adds 1 to that rank's arrival
-//   counter for row t -> waits until its own counter for row t shows all R
-//   partials (acquire, system scope) -> combines them in rank order (bit-identical
-//   on every rank) -> epilogue -> pass 2 (dlogits of the local shard).
+//   the 32-byte tagged partial into row t's slot of EVERY rank's exchange buffer
+//   (peer pointers) -> waits until its own buffer holds all R partials of row t with
+//   this call's tag -> combines them in rank order (bit-identical on every rank) ->
+//   epilogue -> pass 2 (dlogits of the local shard).
 //
 // Each rank's CTA g walks the same row sequence, so a row's partials are produced
 // at about the same time on all ranks; a CTA waits on its peers for at most one row.
-// Call e uses half e % 2 of the buffers and each rank re-zeroes its own counter of a
-// row once it has read the row's partials (the protocol argument is at the re-arm).
+// Call e uses half e % 2 of the buffers with tag e + 1.  A peer can only write call
+// e+2's partial of row t (the same half) after completing call e+1, which needs this
+// rank's call-e+1 partial of row t, which this rank posts after it has finished
+// reading call e: a slot is never overwritten before it is read.
 // With fewer GPUs than ranks, one launch runs several ranks (n_local > 1) as a
 // cooperative grid over one GPU's memory -- the protocol is identical.
 #include <cstdio>
@@ -29,9 +30,11 @@ struct VpParams {
     int32_t world, rank_begin, n_local, shard_cols;
     const uint16_t *logits[GRPO_VP_MAX_RANKS];
     uint16_t *dlogits[GRPO_VP_MAX_RANKS];
-    float4 *xbuf[GRPO_VP_MAX_RANKS];
-    uint32_t *flags[GRPO_VP_MAX_RANKS];
-    int64_t half;     // (epoch % 2) * slots: the half of xbuf / flags this call uses
+    ulonglong2 *xbuf[GRPO_VP_MAX_RANKS];
+    int64_t half;     // (epoch % 2) * slots: the half of xbuf this call uses
+    uint32_t tag;     // epoch + 1: marks this call's words (0 = never written)
+    unsigned long long *row_ctr;  // [n_local] next row to take (zeroed before the launch)
+    int dynamic;      // 1: CTAs take rows from row_ctr; 0: CTA g takes g, g + g_per, ...
     int64_t ld;
     int32_t V;
     int64_t n_rows;
@@ -42,22 +45,22 @@ struct VpParams {
     int32_t cache_vecs;
 };
 
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ void st_relaxed_sys_v2(ulonglong2 *p, uint64_t a, uint64_t b) {
+    asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ ulonglong2 ld_relaxed_sys_v2(const ulonglong2 *p) {
+    ulonglong2 v;
+    asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
     return v;
 }
 
-__device__ __forceinline__ float4 ld_relaxed_sys_v4(const float4 *p) {
-    float4 v;
-    asm volatile("ld.relaxed.sys.global.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p)
-                 : "memory");
-    return v;
-}
-
-template <int NT, int U>
+// LAG = 1 defers the wait: the partial of row k is posted right after its pass 1,
+// and the CTA waits for the peers' partials of row k-1 only after pass 1 of row k --
+// a whole pass of slack for the peer skew and the NVLink latency.  The row cache is
+// split into two halves (rows alternate) so that row k-1's head is still there for
+// its pass 2.
+template <int NT, int U, int LAG>
 __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(const VpParams p) {
     using B = RowwiseBatch<NT, U>;
     constexpr int NW = NT / 32;
@@ -76,16 +79,18 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
     const int tail_vi = (n_vec > 0 && tail_valid < 8) ? n_vec - 1 : -1;
     const int n_batch = (n_vec + BV - 1) / BV;
     const int n_full = tail_vi >= 0 ? tail_vi / BV : n_vec / BV;
-    const int cache_vecs = min(p.cache_vecs, n_batch * U);
+    const int half_vecs = LAG ? p.cache_vecs / 2 : p.cache_vecs;  // per thread, per row
+    const int cache_vecs = min(half_vecs, n_batch * U);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
     const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair,
                                      kBf16NegInfPair);
     const uint16_t *shard = p.logits[lr];
     uint16_t *dshard = p.dlogits[lr];
-    for (int64_t row = g; row < p.n_rows; row += g_per) {
+
+    // pass 1 of `row` into `cache`, then warp 0 posts the row's partial to every rank
+    auto pass1 = [&](int64_t row, uint4 *cache) {
         const uint16_t *zrow = shard + row * p.ld;
-        // ---- pass 1 over the local shard
         float a = -INFINITY, s = 0.0f;
         for (int bi = 0; bi < n_full; ++bi) {
             const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + bi * BV + threadIdx.x;
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
                 x[j] = ldg_policy(src + j * NT, bi * U + j < cache_vecs ? pol_stream : pol_keep);
 #pragma unroll
             for (int j = 0; j < U; ++j)
-                if (bi * U + j < cache_vecs) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
+                if (bi * U + j < cache_vecs) cache[(bi * U + j) * NT + threadIdx.x] = x[j];
             B::reduce(x, a, s);
         }
         for (int bi = n_full; bi < n_batch; ++bi) {
@@ -110,7 +115,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
             }
 #pragma unroll
             for (int j = 0; j < U; ++j)
-                if (bi * U + j < cache_vecs) row_cache[(bi * U + j) * NT + threadIdx.x] = x[j];
+                if (bi * U + j < cache_vecs) cache[(bi * U + j) * NT + threadIdx.x] = x[j];
             B::reduce(x, a, s);
         }
         warp_lse2_combine(a, s);
@@ -123,48 +128,54 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
                 cs = red[lane].y;
             }
             warp_lse2_combine(cm, cs);
-            const RowInfo ri = p.rowinfo[row];
-            const int y_loc = ri.target - c0;
-            const bool mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
+            const int32_t y = p.rowinfo[row].target;
+            const int y_loc = y - c0;
+            const bool mine = y >= 0 && y < p.V && y_loc >= 0 && y_loc < vc;
             const float zy = mine ? __uint_as_float(((uint32_t)zrow[y_loc]) << 16) : 0.0f;
-            // ---- the exchange: this rank's partial into row `row` of every rank's buffer
-            const int64_t slot = p.half + row;
+            // ---- the exchange: this rank's partial into row `row` of every rank's buffer.
+            // Each 64-bit word carries the call's tag next to its payload, and 64-bit
+            // accesses are single-copy atomic: a reader that sees the tag in all four
+            // words has the whole message -- no fence, no counter, no flag to re-arm.
             if (lane < p.world) {
-                float4 *dst = p.xbuf[lane] + slot * p.world + rank;
-                asm volatile("st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst),
-                             "f"(cm), "f"(cs), "f"(zy), "f"(mine ? 1.0f : 0.0f)
-                             : "memory");
-                __threadfence_system();
-                atomicAdd_system(p.flags[lane] + slot, 1u);
-                // wait for all world partials of this row in this rank's buffer
-                const uint32_t *f = p.flags[rank] + slot;
-                long long spins = 0;
-                while (ld_acquire_sys(f) < (uint32_t)p.world) {
-                    __nanosleep(64);
-                    if (++spins > (1ll << 27)) __trap();  // a peer never arrived: fail, don't hang
-                }
+                const uint64_t hi = (uint64_t)p.tag << 32;
+                ulonglong2 *dst = p.xbuf[lane] + ((p.half + row) * p.world + rank) * 2;
+                st_relaxed_sys_v2(dst, hi | __float_as_uint(cm), hi | __float_as_uint(cs));
+                st_relaxed_sys_v2(dst + 1, hi | __float_as_uint(zy), hi | (mine ? 1u : 0u));
             }
-            __syncwarp();
+        }
+    };
+
+    // wait for all partials of `row`, combine, epilogue, pass 2 from `cache`
+    auto finish = [&](int64_t row, const uint4 *cache) {
+        const uint16_t *zrow = shard + row * p.ld;
+        if (warp == 0) {
             float M = -INFINITY, S = 0.0f, zsrc = 0.0f;
             bool own = false;
             if (lane < p.world) {
-                const float4 m4 = ld_relaxed_sys_v4(p.xbuf[rank] + slot * p.world + lane);
-                M = m4.x;
-                S = m4.y;
-                zsrc = m4.z;
-                own = m4.w != 0.0f;
+                const ulonglong2 *src = p.xbuf[rank] + ((p.half + row) * p.world + lane) * 2;
+                ulonglong2 w0, w1;
+                long long spins = 0;
+                for (;;) {
+                    w0 = ld_relaxed_sys_v2(src);
+                    w1 = ld_relaxed_sys_v2(src + 1);
+                    if ((uint32_t)(w0.x >> 32) == p.tag && (uint32_t)(w0.y >> 32) == p.tag &&
+                        (uint32_t)(w1.x >> 32) == p.tag && (uint32_t)(w1.y >> 32) == p.tag)
+                        break;
+                    __nanosleep(32);
+                    if (++spins > (1ll << 27)) __trap();  // a peer never arrived: fail, don't hang
+                }
+                M = __uint_as_float((uint32_t)w0.x);
+                S = __uint_as_float((uint32_t)w0.y);
+                zsrc = __uint_as_float((uint32_t)w1.x);
+                own = (uint32_t)w1.y != 0u;
             }
-            __syncwarp();
-            // re-arm this rank's counter.  The next arrival on this slot belongs to call
-            // e+2, which a peer can only start after seeing this rank's partial of call
-            // e+1 -- released (fence.sc.sys) after this store in program order.
-            if (lane == 0)
-                asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p.flags[rank] + slot), "r"(0u)
-                             : "memory");
             warp_lse2_combine(M, S);  // same inputs in the same lanes on every rank
             const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
             const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
             if (lane == 0) {
+                const RowInfo ri = p.rowinfo[row];
+                const int y_loc = ri.target - c0;
+                const bool mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
                 const bool y_valid = own_mask != 0u;
                 const float zyv = y_valid ? zsh : __int_as_float(0x7FC00000);
                 const float l2s = log2f(S);
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
                         const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + v0;
 #pragma unroll
                         for (int j = 0; j < U; ++j)
-                            x[j] = (bi * U + j < cache_vecs) ? row_cache[(bi * U + j) * NT + threadIdx.x]
+                            x[j] = (bi * U + j < cache_vecs) ? cache[(bi * U + j) * NT + threadIdx.x]
                                                              : ldg_policy(src + j * NT, pol_stream);
 #pragma unroll
                         for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad(x[j], sc, lse2));
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
 #pragma unroll
                         for (int j = 0; j < U; ++j) {
                             const int vi = v0 + j * NT;
-                            x[j] = (bi * U + j < cache_vecs) ? row_cache[(bi * U + j) * NT + threadIdx.x]
+                            x[j] = (bi * U + j < cache_vecs) ? cache[(bi * U + j) * NT + threadIdx.x]
                                    : (vi < n_vec ? ldg_policy(zrow + (int64_t)vi * 8, pol_stream) : neg_inf);
                         }
 #pragma unroll
@@ -237,13 +248,48 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
             }
         }
         __syncthreads();
+    };
+
+    // rows: static (CTA g takes g, g + g_per, ...) or dynamic (in the order CTAs ask for
+    // them; every rank hands out rows in increasing order and posts a row's partial
+    // before it waits for anything, so a waited-for row is always eventually posted)
+    __shared__ int64_t next_row[2];
+    auto take = [&](int64_t cur, int slot) {
+        if (threadIdx.x == 0)
+            next_row[slot] = p.dynamic ? (int64_t)atomicAdd(p.row_ctr + lr, 1ull) : cur + g_per;
+    };
+    if (threadIdx.x == 0) next_row[0] = p.dynamic ? (int64_t)atomicAdd(p.row_ctr + lr, 1ull) : g;
+    __syncthreads();
+    int k = 0;
+    int64_t row = next_row[0];
+    if (LAG == 0) {
+        while (row < p.n_rows) {
+            take(row, (k + 1) & 1);
+            pass1(row, row_cache);
+            finish(row, row_cache);  // ends with __syncthreads: next_row is visible
+            row = next_row[(++k) & 1];
+        }
+    } else {
+        const int half_stride = half_vecs * NT;
+        int64_t prev = -1;
+        while (row < p.n_rows) {
+            take(row, (k + 1) & 1);
+            pass1(row, row_cache + (k & 1) * half_stride);
+            if (prev >= 0) finish(prev, row_cache + ((k - 1) & 1) * half_stride);
+            else __syncthreads();
+            prev = row;
+            row = next_row[(++k) & 1];
+        }
+        if (prev >= 0) finish(prev, row_cache + ((k - 1) & 1) * half_stride);
     }
 }
 
-cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, cudaStream_t s, int *launches,
+cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned long long *row_ctr,
+                      cudaStream_t s, int *launches,
                       grpo_plan_t *plan, char *why, size_t why_len) {
     if (a.n_rows == 0) return cudaSuccess;
     constexpr int NT = 512, U = 8, CPS = 2;
+    const int lag = comm->lag ? 1 : 0;
     VpParams p = {};
     p.world = comm->world;
     p.rank_begin = comm->rank_begin;
@@ -253,10 +299,10 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, cudaStream_
         p.logits[q] = comm->logits[q];
         p.dlogits[q] = comm->dlogits[q];
     }
-    for (int q = 0; q < comm->world; ++q) {
-        p.xbuf[q] = static_cast<float4 *>(comm->xbuf[q]);
-        p.flags[q] = comm->flags[q];
-    }
+    for (int q = 0; q < comm->world; ++q) p.xbuf[q] = static_cast<ulonglong2 *>(comm->xbuf[q]);
+    p.tag = comm->epoch + 1u;
+    p.row_ctr = row_ctr;
+    p.dynamic = comm->static_rows ? 0 : 1;
     p.half = (int64_t)(comm->epoch & 1u) * comm->slots;
     p.ld = a.ld;
     p.V = a.V;
@@ -273,11 +319,12 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, cudaStream_
     p.flag_ws = a.flag_ws;
     const int n_vec = (comm->shard_cols + 7) / 8;
     int cv = (int)((size_t)(160 * 1024) / CPS / ((size_t)NT * 16));
-    const int nv = (n_vec + NT - 1) / NT;
+    const int nv = (n_vec + NT - 1) / NT * (lag ? 2 : 1);
+    if (lag) cv &= ~1;
     if (cv > nv) cv = nv;
     p.cache_vecs = cv;
     const size_t smem = (size_t)cv * NT * 16;
-    auto kern = vp_kernel<NT, U>;
+    auto kern = lag ? vp_kernel<NT, U, 1> : vp_kernel<NT, U, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, n_sm = 148, occ = 0;
@@ -313,6 +360,7 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, cudaStream_
         plan->stages = cv;
         plan->max_clusters = occ;
         plan->smem_bytes = (int32_t)smem;
+        plan->lag = lag;
     }
     *launches += 1;
     return cudaSuccess;

@@ -107,8 +107,21 @@ def timing(rank, world, dev, rows, steps, warmup):
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
+    modes = {}
+    for name, lag, st in (("static_lag0", 0, 1), ("static_lag1", 1, 1), ("dynamic_lag0", 0, 0),
+                          ("dynamic_lag1", 1, 0)):
+        comm.lag, comm.static_rows = lag, st
+        modes[name] = timed(vp)
+    comm.lag, comm.static_rows = 1, 0
     ms_vp = timed(vp)
     plan = G.grpo_async_last_plan()
+    # the same per-rank bytes through the single-GPU kernel: a V = shard_cols problem
+    tgt_h = tgt % sc
+
+    def single_half():
+        loss.loss_chunk(mine, 0, R, tgt_h, lw, db.cu_seqlens, adv, inv, traj_sum, stats,
+                        dlogits=dmine, V=sc)
+    ms_half = timed(single_half)
     del mine, dmine
     ms_single = None
     if rank == 0:
@@ -129,7 +142,9 @@ def timing(rank, world, dev, rows, steps, warmup):
         ms_single = e0.elapsed_time(e1) / steps
     dist.barrier()
     bytes_rank = R * (hi - lo) * 2 * 2
-    return dict(rows=R, V=V, shard_cols=sc, ms_vp_step=ms_vp, ms_single_gpu=ms_single,
+    return dict(rows=R, V=V, shard_cols=sc, ms_vp_step=ms_vp, ms_vp_modes=modes,
+                ms_single_kernel_on_shard=ms_half,
+                ms_single_gpu=ms_single,
                 vp_GBps_per_rank=bytes_rank / ms_vp / 1e6,
                 speedup_vs_single=(ms_single / ms_vp) if ms_single else None, plan=plan)
 

@@ -23,6 +23,21 @@ def test_vp_parity(dev, name, world):
     assert gpu["shard_pad_untouched"]
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_vp_schedules_match_bitwise(dev, world):
+    """The deferred wait (lag 1, default) and the immediate wait (lag 0), dynamic and
+    static row assignment, combine the same partials in the same order: identical
+    per-row outputs and dlogits, bit for bit (traj_sum / J are fp64 sums whose order
+    follows the segment reduce, not the schedule)."""
+    b = make_batch("mid32k", 9)
+    bits = b.logits_bits()
+    ref = run_gpu_vp(b, bits, dev, world, lag=1, static_rows=0)
+    for lag, st in ((0, 0), (0, 1), (1, 1)):
+        g = run_gpu_vp(b, bits, dev, world, lag=lag, static_rows=st)
+        for k in ("logp", "lse", "scale", "traj_sum", "stats", "dlogits_raw"):
+            assert np.array_equal(g[k], ref[k], equal_nan=True), (k, lag, st)
+
+
 def test_vp_chunks_and_epochs(dev):
     """Several row chunks and repeated calls on the same exchange buffers (counters are
     never reset: call e waits for (e+1)*R arrivals)."""
