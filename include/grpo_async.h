@@ -105,6 +105,8 @@ typedef struct {
                                /* from the token-mean denominator (overlong filtering, masking of */
                                /* C1-violating partial rollouts); group statistics keep    */
                                /* every member                                                    */
+    int32_t std_unbiased;      /* 0: population std (eq:group_advantage as read, Z1); 1: sample   */
+                               /* std with n - 1 (verl-style); a one-member group has A = 0      */
 } grpo_loss_opts_t;
 
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
@@ -178,7 +180,8 @@ grpo_status_t grpo_async_advantage(const float *rewards, const int32_t *group_id
 /*
  * grpo_async_advantage_ex -- grpo_async_advantage with grpo_loss_opts_t:
  *   inv_norm_i = 1/(P * count_p * L_i) (GRPO_NORM_SEQ) or 1/sum_kept L (GRPO_NORM_TOKEN),
- *   and 0 for trajectories the mask drops.  opts->eps_* are not used here.
+ *   and 0 for trajectories the mask drops; opts->std_unbiased selects the sample std
+ *   (n - 1) for A_i.  opts->eps_* are not used here.
  * Errors: as grpo_async_advantage, plus GRPO_ERR_INVALID_ARG for NULL opts or a bad norm.
  */
 grpo_status_t grpo_async_advantage_ex(const float *rewards, const int32_t *group_ids,

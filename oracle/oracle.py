@@ -60,6 +60,8 @@ def lib():
         _lib.oracle_validate.restype = C.c_int
         _lib.oracle_advantage.argtypes = [i32, i32, P, P, P, f64, P, P, P]
         _lib.oracle_advantage.restype = None
+        _lib.oracle_advantage_ex.argtypes = [i32, i32, P, P, P, f64, i32, P, P, P]
+        _lib.oracle_advantage_ex.restype = None
         _lib.oracle_log_softmax_row.argtypes = [i32, P, i64, P, P]
         _lib.oracle_log_softmax_row.restype = None
         _lib.oracle_token.argtypes = [f64, f32, f64, f64, f32, f64, P, P, P, P]
@@ -117,7 +119,8 @@ def validate(version_ids, cu_seqlens, group_ids, target_ids, *, P, V, G, tbs,
 
 
 # --------------------------------------------------------------------------- O2
-def advantage(rewards, group_ids, cu_seqlens, P, std_floor=1e-8):
+def advantage(rewards, group_ids, cu_seqlens, P, std_floor=1e-8, unbiased=False):
+    """eq:group_advantage; unbiased=True: sample std (n - 1), SURVEY NEXT(1)."""
     R = _c(rewards, np.float32)
     g = _c(group_ids, np.int32)
     cu = _c(cu_seqlens, np.int64)
@@ -125,7 +128,8 @@ def advantage(rewards, group_ids, cu_seqlens, P, std_floor=1e-8):
     adv = np.zeros(N, np.float64)
     inv = np.zeros(N, np.float64)
     gc = np.zeros(max(P, 1), np.int32)
-    lib().oracle_advantage(N, P, _p(R), _p(g), _p(cu), float(std_floor), _p(adv), _p(inv), _p(gc))
+    lib().oracle_advantage_ex(N, P, _p(R), _p(g), _p(cu), float(std_floor), int(bool(unbiased)),
+                              _p(adv), _p(inv), _p(gc))
     return adv, inv, gc[:P]
 
 
@@ -251,7 +255,7 @@ def objective_nested(cu_seqlens, group_ids, version_ids, term, P):
 
 # --------------------------------------------------------------------- full path
 def run_batch(batch, logits_bits, eps=0.2, grad_scale=1.0, std_floor=1e-8, want_dlogits=True,
-              eps_hi=None, norm=0, traj_mask=None):
+              eps_hi=None, norm=0, traj_mask=None, std_unbiased=False):
     """Whole hot path on a small batch: validate, advantage, rows, J.
 
     ``batch`` is a synth.gen.Batch (or anything with the same fields);
@@ -260,7 +264,8 @@ def run_batch(batch, logits_bits, eps=0.2, grad_scale=1.0, std_floor=1e-8, want_
     val = validate(batch.version_ids, batch.cu_seqlens, batch.group_ids, batch.target_ids,
                    P=batch.P, V=batch.V, G=batch.G, tbs=batch.tbs, v_theta=batch.v_theta,
                    K=batch.K, token_version=batch.token_version, logp_behav=batch.logp_behav)
-    adv, inv, gc = advantage(batch.rewards, batch.group_ids, batch.cu_seqlens, batch.P, std_floor)
+    adv, inv, gc = advantage(batch.rewards, batch.group_ids, batch.cu_seqlens, batch.P, std_floor,
+                             unbiased=std_unbiased)
     if norm != 0 or traj_mask is not None:
         inv = weights(batch.group_ids, batch.cu_seqlens, gc, batch.P, norm, traj_mask)
     T = int(batch.cu_seqlens[-1])

@@ -56,7 +56,7 @@ NORM_SEQ, NORM_TOKEN = 0, 1
 
 class LossOpts(C.Structure):
     _fields_ = [("eps_lo", C.c_float), ("eps_hi", C.c_float), ("norm", C.c_int32),
-                ("traj_mask", C.c_void_p)]
+                ("traj_mask", C.c_void_p), ("std_unbiased", C.c_int32)]
 
 
 class Plan(C.Structure):
@@ -230,14 +230,15 @@ def grpo_async_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor, adv, i
         _ptr(group_count, torch.int32, "group_count"), _stream(stream)))
 
 
-def _opts(eps_lo, eps_hi, norm, traj_mask):
+def _opts(eps_lo, eps_hi, norm, traj_mask, std_unbiased=False):
     return LossOpts(float(eps_lo), float(eps_hi), int(norm),
-                    _ptr(traj_mask, torch.uint8, "traj_mask"))
+                    _ptr(traj_mask, torch.uint8, "traj_mask"), int(bool(std_unbiased)))
 
 
 def grpo_async_advantage_ex(rewards, group_ids, cu_seqlens, N, P, std_floor, eps_lo, eps_hi, norm,
-                            traj_mask, adv, inv_norm, group_count=None, stream=None):
-    o = _opts(eps_lo, eps_hi, norm, traj_mask)
+                            traj_mask, adv, inv_norm, group_count=None, stream=None,
+                            std_unbiased=False):
+    o = _opts(eps_lo, eps_hi, norm, traj_mask, std_unbiased)
     _check(LIB.grpo_async_advantage_ex(
         _ptr(rewards, torch.float32, "rewards"), _ptr(group_ids, torch.int32, "group_ids"),
         _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, P, float(std_floor), C.byref(o),

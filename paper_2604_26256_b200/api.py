@@ -74,14 +74,16 @@ class GrpoAsyncLoss:
 
     eps: clip range; grad_scale multiplies dlogits; std_floor: Z2.
     DAPO options: eps_hi (clip-higher upper range, default eps),
-    norm ("seq" = eq:grpo_async as written, "token" = DAPO token mean) and traj_mask
-    (uint8 device tensor [N], 0 drops a trajectory from the loss).
+    norm ("seq" = eq:grpo_async as written, "token" = DAPO token mean), traj_mask
+    (uint8 device tensor [N], 0 drops a trajectory from the loss) and std_unbiased
+    (sample std, n - 1, in the group advantage).
     tune: optional dict for grpo_tune_t (kernel / cluster_size / ctas_per_sm / stages / ...).
     """
 
     def __init__(self, eps=0.2, std_floor=1e-8, grad_scale=1.0, tune=None, eps_hi=None,
-                 norm="seq", traj_mask=None):
+                 norm="seq", traj_mask=None, std_unbiased=False):
         self.eps = float(eps)
+        self.std_unbiased = bool(std_unbiased)
         self.eps_hi = float(eps if eps_hi is None else eps_hi)
         self.norm = {"seq": L.NORM_SEQ, "token": L.NORM_TOKEN}[norm]
         self.traj_mask = traj_mask
@@ -112,12 +114,14 @@ class GrpoAsyncLoss:
         else:
             L.grpo_async_advantage_ex(db.rewards, db.group_ids, db.cu_seqlens, db.N, db.P,
                                       self.std_floor, self.eps, self.eps_hi, self.norm,
-                                      self.traj_mask, adv, inv, None, stream)
+                                      self.traj_mask, adv, inv, None, stream,
+                                      std_unbiased=self.std_unbiased)
         self.launches += L.grpo_last_launch_count()
         return adv, inv
 
     def _default_opts(self):
-        return self.eps_hi == self.eps and self.norm == L.NORM_SEQ and self.traj_mask is None
+        return (self.eps_hi == self.eps and self.norm == L.NORM_SEQ and self.traj_mask is None
+                and not self.std_unbiased)
 
     def workspace(self, n_rows, V, N, device):
         need = L.grpo_async_workspace_size(n_rows, V, N)

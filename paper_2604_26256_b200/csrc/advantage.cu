@@ -1,7 +1,7 @@
 // advantage.cu -- group-relative advantages, eq:group_advantage:
 // (with grpo_async_advantage_ex: DAPO token-mean weights and trajectory masks)
 //   A_i = (R_i - mean_p) / std_p  over the members of prompt group p,
-// population std (Z1), A = 0 exactly for a group whose rewards are
+// population std (Z1; sample std with opts->std_unbiased), A = 0 exactly for a group whose rewards are
 // bitwise equal, else denominator max(std, floor) (Z2), and the token weight
 // inv_norm_i = 1 / (P * G_p * L_i) of eq:grpo_async (Z5, Z6).
 //
@@ -24,7 +24,7 @@ __device__ __forceinline__ bool kept(const int32_t *group_ids, const int64_t *cu
 __global__ void __launch_bounds__(256)
     advantage_kernel(const float *__restrict__ rewards, const int32_t *__restrict__ group_ids,
                      const int64_t *__restrict__ cu, int32_t N, int32_t P, float std_floor,
-                     int32_t norm, const uint8_t *__restrict__ traj_mask,
+                     int32_t norm, int32_t unbiased, const uint8_t *__restrict__ traj_mask,
                      float *__restrict__ adv, float *__restrict__ inv_norm,
                      int32_t *__restrict__ group_count) {
     const int lane = threadIdx.x & 31;
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256)
             mask &= mask - 1;
         }
     }
-    const double sd = sqrt(ss / (double)n);
+    const double sd = sqrt(ss / (double)(unbiased && n > 1 ? n - 1 : n));
     const double den = sd > (double)std_floor ? sd : (double)std_floor;
     // pass 3: outputs of the members (each lane writes its own)
     for (int32_t base = 0; base < N; base += 32) {
@@ -109,15 +109,16 @@ __global__ void advantage_invalid_kernel(const int32_t *__restrict__ group_ids, 
 
 cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, const int64_t *cu,
                              int32_t N, int32_t P, float std_floor, int32_t norm,
-                             const uint8_t *traj_mask, float *adv, float *inv_norm,
-                             int32_t *group_count, cudaStream_t s, int *launches) {
+                             int32_t unbiased, const uint8_t *traj_mask, float *adv,
+                             float *inv_norm, int32_t *group_count, cudaStream_t s, int *launches) {
     if (N > 0) {
         advantage_invalid_kernel<<<(N + 255) / 256, 256, 0, s>>>(group_ids, N, P, adv, inv_norm);
         *launches += 1;
     }
     const int64_t threads = (int64_t)P * 32;
     advantage_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-        rewards, group_ids, cu, N, P, std_floor, norm, traj_mask, adv, inv_norm, group_count);
+        rewards, group_ids, cu, N, P, std_floor, norm, unbiased, traj_mask, adv, inv_norm,
+        group_count);
     *launches += 1;
     return cudaGetLastError();
 }

@@ -204,7 +204,7 @@ grpo_status_t grpo_async_advantage(const float *rewards, const int32_t *group_id
         return fail(GRPO_ERR_INVALID_ARG, "advantage: NULL pointer");
     int launches = 0;
     cudaError_t e = grpo::launch_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor,
-                                           GRPO_NORM_SEQ, nullptr, adv, inv_norm, group_count,
+                                           GRPO_NORM_SEQ, 0, nullptr, adv, inv_norm, group_count,
                                            (cudaStream_t)stream, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "advantage");
     return ok(launches);
@@ -224,7 +224,8 @@ grpo_status_t grpo_async_advantage_ex(const float *rewards, const int32_t *group
         return fail(GRPO_ERR_INVALID_ARG, "advantage_ex: NULL pointer");
     int launches = 0;
     cudaError_t e = grpo::launch_advantage(rewards, group_ids, cu_seqlens, N, P, std_floor,
-                                           opts->norm, opts->traj_mask, adv, inv_norm,
+                                           opts->norm, opts->std_unbiased ? 1 : 0,
+                                           opts->traj_mask, adv, inv_norm,
                                            group_count, (cudaStream_t)stream, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "advantage_ex");
     return ok(launches);

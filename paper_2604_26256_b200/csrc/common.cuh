@@ -407,7 +407,7 @@ cudaError_t launch_validate(const int64_t *version_ids, const int64_t *token_ver
                             grpo_validate_summary_t *summary, cudaStream_t s, int *launches);
 cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, const int64_t *cu,
                              int32_t N, int32_t P, float std_floor, int32_t norm,
-                             const uint8_t *traj_mask, float *adv, float *inv_norm,
-                             int32_t *group_count, cudaStream_t s, int *launches);
+                             int32_t unbiased, const uint8_t *traj_mask, float *adv,
+                             float *inv_norm, int32_t *group_count, cudaStream_t s, int *launches);
 
 }  // namespace grpo

@@ -24,13 +24,13 @@ def dev_bits_to_f64(t: torch.Tensor, V: int) -> np.ndarray:
 
 
 def run_gpu(batch, logits_bits, device, tune=None, chunks=1, inplace=False, want_dlogits=True,
-            grad_scale=1.0, eps=0.2, eps_hi=None, norm="seq", traj_mask=None):
+            grad_scale=1.0, eps=0.2, eps_hi=None, norm="seq", traj_mask=None, std_unbiased=False):
     """Whole path on the GPU: validate, advantage, fused loss over `chunks` row chunks."""
     db = G.DeviceBatch.from_host(batch, device)
     mask_d = None if traj_mask is None else torch.from_numpy(
         np.ascontiguousarray(traj_mask, np.uint8)).to(device)
     loss = G.GrpoAsyncLoss(eps=eps, grad_scale=grad_scale, tune=tune, eps_hi=eps_hi, norm=norm,
-                           traj_mask=mask_d)
+                           traj_mask=mask_d, std_unbiased=std_unbiased)
     vo = loss.validate(db)
     adv, inv = loss.advantage(db)
     T, ld, V = batch.T, batch.ld, batch.V
@@ -69,10 +69,11 @@ def run_gpu(batch, logits_bits, device, tune=None, chunks=1, inplace=False, want
 
 
 def run_oracle(batch, logits_bits, want_dlogits=True, eps=0.2, grad_scale=1.0, eps_hi=None,
-               norm="seq", traj_mask=None):
+               norm="seq", traj_mask=None, std_unbiased=False):
     return O.run_batch(batch, logits_bits, eps=eps, grad_scale=grad_scale,
                        std_floor=float(np.float32(1e-8)), want_dlogits=want_dlogits,
-                       eps_hi=eps_hi, norm={"seq": 0, "token": 1}[norm], traj_mask=traj_mask)
+                       eps_hi=eps_hi, norm={"seq": 0, "token": 1}[norm], traj_mask=traj_mask,
+                       std_unbiased=std_unbiased)
 
 
 def near_boundary(r, eps=EPS32, tol=1e-5, eps_hi=None):

@@ -46,3 +46,15 @@ def test_masks_c1_and_overlong(dev, norm):
         rows = np.repeat(mask == 0, b.lengths)
         assert np.all(gpu["dlogits"][rows] == 0.0)
         assert np.all(gpu["inv_norm"][mask == 0] == 0.0)
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_std_unbiased(dev, kernel):
+    """NEXT(1) sample-std advantages (verl-style) through grpo_async_advantage_ex, with the
+    DAPO options on; adv/inv_norm stay bit-exact against the oracle."""
+    b = make_batch("mid32k", 4)
+    bits = b.logits_bits()
+    for opts in (dict(std_unbiased=True), dict(std_unbiased=True, eps_hi=0.28, norm="token")):
+        ref = run_oracle(b, bits, **opts)
+        gpu = run_gpu(b, bits, dev, tune={"kernel": kernel}, **opts)
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:], eps_hi=opts.get("eps_hi"))

@@ -77,6 +77,43 @@ def test_advantage_invariants(seed):
     np.testing.assert_allclose(a3, a1, atol=1e-12)
 
 
+def test_advantage_unbiased_closed_form():
+    """NEXT(1) sample std: [2,0,1] has sample std 1 -> A = (+1, -1, 0) exactly; a binary
+    group of G with k ones has A_i = (R_i - k/G) / sqrt(k(G-k)/(G(G-1)))."""
+    adv, _, _ = O.advantage([2, 0, 1], [0, 0, 0], [0, 1, 2, 3], 1, unbiased=True)
+    assert list(adv) == [1.0, -1.0, 0.0]
+    G, k = 8, 3
+    R = np.array([1.0] * k + [0.0] * (G - k), np.float32)
+    adv, _, _ = O.advantage(R, [0] * G, np.arange(G + 1), 1, unbiased=True)
+    sd = math.sqrt(k * (G - k) / (G * (G - 1)))
+    np.testing.assert_allclose(adv[:k], (1 - k / G) / sd, rtol=1e-14)
+    np.testing.assert_allclose(adv[k:], (0 - k / G) / sd, rtol=1e-14)
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_advantage_unbiased_vs_numpy_ddof1(seed):
+    """Against numpy's sample std (ddof=1) per group; the single-member group and the
+    bitwise-equal group keep A = 0; unbiased = population * sqrt((n-1)/n)."""
+    rng = np.random.default_rng(100 + seed)
+    P, G = 6, int(rng.integers(2, 12))
+    g = rng.permutation(np.repeat(np.arange(P), G)).astype(np.int32)
+    R = rng.normal(size=P * G).astype(np.float32)
+    g = np.concatenate([g, [P]]).astype(np.int32)          # group P: one member
+    R = np.concatenate([R, np.float32([0.7])])
+    R[g == 0] = np.float32(0.25)                           # group 0: bitwise equal
+    cu = np.arange(len(R) + 1)
+    a_u, _, gc = O.advantage(R, g, cu, P + 1, unbiased=True)
+    a_p, _, _ = O.advantage(R, g, cu, P + 1)
+    assert gc[P] == 1 and a_u[g == P][0] == 0.0 and np.all(a_u[g == 0] == 0.0)
+    for p in range(1, P):
+        m = g == p
+        r = R[m].astype(np.float64)
+        np.testing.assert_allclose(a_u[m], (r - r.mean()) / np.std(r, ddof=1), rtol=1e-12,
+                                   atol=1e-14)
+        np.testing.assert_allclose(a_u[m], a_p[m] * math.sqrt((G - 1) / G), rtol=1e-12,
+                                   atol=1e-14)
+
+
 def test_inv_norm_weights_sum_to_one():
     """inv_norm_i = 1/(P G_p L_i): sum_i inv_norm_i * L_i = 1 (each prompt weighs 1/P, Z5)."""
     b = make_batch("mid32k", 3)
