@@ -2,7 +2,8 @@
 
 ctypes binding to the plain fp64 C oracle in ``oracle/grpo_oracle.c``
 (arxiv 2604.26256, PAPER.md eq:grpo_async P:9-26, eq:ratio_async P:28-40,
-eq:group_advantage P:153-156).  Only tests/, ``__graft_entry__.smoke()`` and
+eq:group_advantage P:153-156), plus the LM-head composition of SURVEY NEXT(2)
+(logits = X W^T in fp64, pinned by the one-hot and finite-difference tests).  Only tests/, ``__graft_entry__.smoke()`` and
 bench.py's cpu_baseline / ``--impl reference`` leg may import this module.
 It never imports the CUDA package and the CUDA package never imports it.
 """
@@ -283,3 +284,41 @@ def run_batch(batch, logits_bits, eps=0.2, grad_scale=1.0, std_floor=1e-8, want_
 def _traj_index(cu_seqlens):
     cu = np.asarray(cu_seqlens, np.int64)
     return np.repeat(np.arange(len(cu) - 1), np.diff(cu))
+
+
+# ------------------------------------------------------- NEXT(2): LM-head-fused loss
+def _bf16_to_f64(bits):
+    """bf16 bit patterns -> float64 (exact: a bf16 is a float32 with 16 zero low bits)."""
+    b = np.ascontiguousarray(bits, np.uint16)
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def lmhead_logits(hidden_bits, W_bits):
+    """z = X W^T (the trainer's LM head) in fp64 from bf16 X [n, d] and W [V, d].
+    Every product of two bf16 values is exact in fp64; the library matmul is the step."""
+    return _bf16_to_f64(hidden_bits) @ _bf16_to_f64(W_bits).T
+
+
+def run_batch_lmhead(batch, hidden_bits, W_bits, eps=0.2, grad_scale=1.0, std_floor=1e-8,
+                     want_grads=True, eps_hi=None, norm=0, traj_mask=None, std_unbiased=False):
+    """The whole path with logits = X W^T: validate, advantage, O3-O5 on
+    the fp64 logits, J; with want_grads the chain rule through the LM head:
+      dz = dJ/dz (O5 rows), dJ/dX = dz W, dJ/dW = dz^T X."""
+    val = validate(batch.version_ids, batch.cu_seqlens, batch.group_ids, batch.target_ids,
+                   P=batch.P, V=batch.V, G=batch.G, tbs=batch.tbs, v_theta=batch.v_theta,
+                   K=batch.K, token_version=batch.token_version, logp_behav=batch.logp_behav)
+    adv, inv, gc = advantage(batch.rewards, batch.group_ids, batch.cu_seqlens, batch.P, std_floor,
+                             unbiased=std_unbiased)
+    if norm != 0 or traj_mask is not None:
+        inv = weights(batch.group_ids, batch.cu_seqlens, gc, batch.P, norm, traj_mask)
+    T = int(batch.cu_seqlens[-1])
+    z = lmhead_logits(hidden_bits, W_bits)
+    rr = rows_f64(np.arange(T, dtype=np.int64), z, batch.target_ids, batch.logp_behav,
+                  batch.cu_seqlens, adv, inv, eps, grad_scale, want_grads, eps_hi=eps_hi)
+    J, traj_sum = objective_tokens(batch.cu_seqlens, inv, rr.term)
+    out = dict(validate=val, adv=adv, inv_norm=inv, group_count=gc, rows=rr, J=J, loss=-J,
+               traj_sum=traj_sum, logits=z, n_clipped=int(rr.clipped.sum()))
+    if want_grads:
+        out["dhidden"] = rr.dlogits @ _bf16_to_f64(W_bits)
+        out["dW"] = rr.dlogits.T @ _bf16_to_f64(hidden_bits)
+    return out
