@@ -309,9 +309,54 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
                                   const float *token_scale, float grad_scale_mult,
                                   uint16_t *dlogits, grpo_stream_t stream);
 
+/*
+ * ---- LM-head-fused loss (the step before the path: the trainer's LM
+ * head, Megatron-LM).  z = X W^T is computed on the tensor cores (tcgen05.mma,
+ * bf16 x bf16 -> f32 in TMEM) and consumed tile by tile in the kernel's epilogue, so the
+ * [n_rows, V] logits never reach HBM (Cut-Cross-Entropy style).
+ *   hidden  bf16 [n_rows, d] row-major (the final hidden states of the chunk's rows)
+ *   W       bf16 [V, d] row-major (the LM-head weight, vocabulary-major)
+ *   d % 64 == 0, 64 <= d; both 16-byte aligned; V >= 1.
+ *
+ * grpo_async_lmhead_fwd -- as grpo_async_loss_fwd_ex but with logits = hidden W^T:
+ *   per-row logp / lse / token_scale, per-trajectory term sums and the stats, with the
+ *   same row chunking (row_begin, cu_seqlens, traj_index) and options.  Workspace:
+ *   grpo_async_lmhead_workspace_size(n_rows, V, N) bytes.
+ * grpo_async_lmhead_bwd -- the backward from the forward's lse and token_scale:
+ *   recomputes z tile by tile and writes dz = grad_scale_mult * s_t (softmax(z) - onehot(y))
+ *   as bf16 [n_rows, ld_dz] (ld_dz >= V, multiple of 8; columns [V, ld_dz) untouched), then
+ *   dhidden = dz W (bf16 [n_rows, d], NULL to skip) and dW += dz^T hidden (f32 [V, d],
+ *   accumulated so chunks add up; NULL to skip) as two cuBLAS GEMMs.
+ * grpo_async_lmhead_logits -- the plain logits hidden W^T as bf16 [n_rows, ld_out] (the
+ *   unfused producer for grpo_async_loss_fwd, and the check of the GEMM).
+ * Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_WORKSPACE, GRPO_ERR_CUDA.
+ */
+size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N);
+
+grpo_status_t grpo_async_lmhead_fwd(const uint16_t *hidden, const uint16_t *W, int64_t row_begin,
+                                    int64_t n_rows, int32_t d, int32_t V,
+                                    const int64_t *target_ids, const float *logp_behav,
+                                    const int64_t *cu_seqlens, int32_t N,
+                                    const int32_t *traj_index, const float *adv,
+                                    const float *inv_norm, const grpo_loss_opts_t *opts,
+                                    float grad_scale, float *logp_out, float *lse_out,
+                                    float *token_scale_out, double *traj_sum, double *stats,
+                                    void *workspace, size_t workspace_bytes, grpo_stream_t stream);
+
+grpo_status_t grpo_async_lmhead_bwd(const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
+                                    int32_t d, int32_t V, const int64_t *target_ids,
+                                    const float *lse, const float *token_scale,
+                                    float grad_scale_mult, uint16_t *dz, int64_t ld_dz,
+                                    uint16_t *dhidden, float *dW, grpo_stream_t stream);
+
+grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
+                                       int32_t d, int32_t V, uint16_t *out, int64_t ld_out,
+                                       grpo_stream_t stream);
+
 /* Launch plan of the last fused-loss launch made by the calling thread. */
 typedef struct {
-    int32_t kernel;        /* 1 cluster-resident, 2 row-wise                          */
+    int32_t kernel;        /* 1 cluster-resident, 2 row-wise, 3 vocab-parallel, 4/5/6 LM-head  */
+                           /* (tcgen05) loss partials / logits gradient / logits           */
     int32_t cluster_size;  /* CTAs per row (kernel 1)                                 */
     int32_t ctas_per_sm;   /* requested residency (kernel 1)                          */
     int32_t stages;        /* shared-memory row stages per CTA (kernel 1)             */

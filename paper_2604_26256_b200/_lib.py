@@ -33,6 +33,8 @@ SUMMARY_FIELDS = ("n_traj", "n_tokens", "n_stale", "n_future", "n_zero_len", "n_
 EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advantage",
             "grpo_async_advantage_ex", "grpo_async_loss_fwd", "grpo_async_loss_fwd_ex",
             "grpo_async_loss_fwd_vp", "grpo_async_loss_bwd", "grpo_async_workspace_size",
+            "grpo_async_lmhead_workspace_size", "grpo_async_lmhead_fwd", "grpo_async_lmhead_bwd",
+            "grpo_async_lmhead_logits",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -110,6 +112,15 @@ def _load():
     lib.grpo_async_loss_fwd_vp.argtypes = [P, i64, i64, i32, i64, P, P, P, i32, P, P, P, P, f32,
                                            P, P, P, P, P, P, sz, P]
     lib.grpo_async_loss_fwd_vp.restype = st
+    lib.grpo_async_lmhead_workspace_size.argtypes = [i64, i32, i32]
+    lib.grpo_async_lmhead_workspace_size.restype = sz
+    lib.grpo_async_lmhead_fwd.argtypes = [P, P, i64, i64, i32, i32, P, P, P, i32, P, P, P, P, f32,
+                                          P, P, P, P, P, P, sz, P]
+    lib.grpo_async_lmhead_fwd.restype = st
+    lib.grpo_async_lmhead_bwd.argtypes = [P, P, i64, i32, i32, P, P, P, f32, P, i64, P, P, P]
+    lib.grpo_async_lmhead_bwd.restype = st
+    lib.grpo_async_lmhead_logits.argtypes = [P, P, i64, i32, i32, P, i64, P]
+    lib.grpo_async_lmhead_logits.restype = st
     lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
     lib.grpo_async_loss_bwd.restype = st
     lib.grpo_async_workspace_size.argtypes = [i64, i32, i32]
@@ -351,3 +362,45 @@ def grpo_async_loss_bwd(logits, n_rows, V, ld, target_ids, lse, token_scale, gra
         _ptr(logits, None, "logits"), n_rows, V, ld, _ptr(target_ids, torch.int64, "target_ids"),
         _ptr(lse, torch.float32, "lse"), _ptr(token_scale, torch.float32, "token_scale"),
         float(grad_scale_mult), _ptr(dlogits, None, "dlogits"), _stream(stream)))
+
+
+# ---- LM-head-fused loss
+def _bf16(x, name):
+    if x is not None and x.element_size() != 2:
+        raise TypeError(f"{name}: expected a 16-bit (bf16) tensor")
+    return _ptr(x, None, name)
+
+
+def grpo_async_lmhead_workspace_size(n_rows: int, V: int, N: int) -> int:
+    return int(LIB.grpo_async_lmhead_workspace_size(n_rows, V, N))
+
+
+def grpo_async_lmhead_fwd(hidden, W, row_begin, n_rows, d, V, target_ids, logp_behav, cu_seqlens,
+                          N, traj_index, adv, inv_norm, eps_lo, eps_hi, norm, traj_mask,
+                          grad_scale, logp_out, lse_out, token_scale_out, traj_sum, stats,
+                          workspace, stream=None):
+    o = _opts(eps_lo, eps_hi, norm, traj_mask)
+    _check(LIB.grpo_async_lmhead_fwd(
+        _bf16(hidden, "hidden"), _bf16(W, "W"), row_begin, n_rows, d, V,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(logp_behav, torch.float32, "logp_behav"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, _ptr(traj_index, torch.int32, "traj_index"),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"), C.byref(o),
+        float(grad_scale), _ptr(logp_out, torch.float32, "logp_out"),
+        _ptr(lse_out, torch.float32, "lse_out"), _ptr(token_scale_out, torch.float32, "token_scale_out"),
+        _ptr(traj_sum, torch.float64, "traj_sum"), _ptr(stats, torch.float64, "stats"),
+        _ptr(workspace, torch.uint8, "workspace"),
+        workspace.numel() if workspace is not None else 0, _stream(stream)))
+
+
+def grpo_async_lmhead_bwd(hidden, W, n_rows, d, V, target_ids, lse, token_scale, grad_scale_mult,
+                          dz, ld_dz, dhidden, dW, stream=None):
+    _check(LIB.grpo_async_lmhead_bwd(
+        _bf16(hidden, "hidden"), _bf16(W, "W"), n_rows, d, V,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(lse, torch.float32, "lse"),
+        _ptr(token_scale, torch.float32, "token_scale"), float(grad_scale_mult), _bf16(dz, "dz"),
+        ld_dz, _bf16(dhidden, "dhidden"), _ptr(dW, torch.float32, "dW"), _stream(stream)))
+
+
+def grpo_async_lmhead_logits(hidden, W, n_rows, d, V, out, ld_out, stream=None):
+    _check(LIB.grpo_async_lmhead_logits(_bf16(hidden, "hidden"), _bf16(W, "W"), n_rows, d, V,
+                                        _bf16(out, "out"), ld_out, _stream(stream)))

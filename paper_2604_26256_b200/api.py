@@ -150,6 +150,35 @@ class GrpoAsyncLoss:
                                      self.tune, stream)
         self.launches += L.grpo_last_launch_count()
 
+    # ---- LM-head-fused loss: logits = hidden W^T on the tensor cores
+    def lmhead_workspace(self, n_rows, V, N, device):
+        need = L.grpo_async_lmhead_workspace_size(n_rows, V, N)
+        if self._ws is None or self._ws.numel() < need or self._ws.device != device:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+        return self._ws
+
+    def lmhead_fwd(self, hidden, W, row_begin, n_rows, target_ids, logp_behav, cu_seqlens, adv,
+                   inv_norm, traj_sum, stats, traj_index=None, logp_out=None, lse_out=None,
+                   scale_out=None, stream=None):
+        """hidden bf16 [n_rows, d], W bf16 [V, d]; outputs as loss_chunk (no logits in HBM)."""
+        V, d = W.shape
+        N = cu_seqlens.numel() - 1
+        ws = self.lmhead_workspace(n_rows, V, N, W.device)
+        L.grpo_async_lmhead_fwd(hidden, W, row_begin, n_rows, d, V, target_ids, logp_behav,
+                                cu_seqlens, N, traj_index, adv, inv_norm, self.eps, self.eps_hi,
+                                self.norm, self.traj_mask, self.grad_scale, logp_out, lse_out,
+                                scale_out, traj_sum, stats, ws, stream)
+        self.launches += L.grpo_last_launch_count()
+
+    def lmhead_bwd(self, hidden, W, n_rows, target_ids, lse, token_scale, dz, dhidden=None,
+                   dW=None, mult=1.0, stream=None):
+        """dz bf16 [n_rows, ld_dz] (written), dhidden bf16 [n_rows, d] (written), dW f32 [V, d]
+        (accumulated)."""
+        V, d = W.shape
+        L.grpo_async_lmhead_bwd(hidden, W, n_rows, d, V, target_ids, lse, token_scale, mult, dz,
+                                dz.shape[1], dhidden, dW, stream)
+        self.launches += L.grpo_last_launch_count()
+
     # ---- fused loss over vocabulary-parallel logits (SURVEY NEXT(3), P:282)
     def loss_chunk_vp(self, comm, shards, row_begin, n_rows, target_ids, logp_behav, cu_seqlens,
                       adv, inv_norm, traj_sum, stats, dshards=None, traj_index=None,

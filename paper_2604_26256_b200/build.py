@@ -22,6 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-cudart", "static",
               "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+LINK = ["-lcublas"]
 
 
 def sources():
@@ -41,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-shared", "-o", tmp, *sources()]
+    cmd = [NVCC, *ARCH, *NVCC_FLAGS, "-I", INCLUDE, "-shared", "-o", tmp, *sources(), *LINK]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(ROOT, "build", "ptxas_grpo_async.log")
     with open(log, "w") as f:

@@ -1,6 +1,8 @@
 // api.cu -- the extern "C" boundary declared in include/grpo_async.h.
 // Host-side argument checks, workspace carve-up, kernel selection, error text.
 #include <cstdarg>
+
+#include <cublas_v2.h>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -449,6 +451,183 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
                                           grad_scale_mult, dlogits, (cudaStream_t)stream,
                                           &launches);
     if (e != cudaSuccess) return cuda_fail(e, "loss_bwd");
+    return ok(launches);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- LM head (NEXT(2))
+namespace {
+
+grpo_status_t lm_check(const char *fn, const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
+                       int32_t d, int32_t V) {
+    if (n_rows < 0 || V <= 0 || d < 64 || d % 64 != 0 || n_rows > INT32_MAX)
+        return fail(GRPO_ERR_INVALID_ARG, "%s: n_rows=%lld d=%d V=%d (d a positive multiple of 64)", fn,
+                    (long long)n_rows, d, V);
+    if (!W || (n_rows > 0 && !hidden)) return fail(GRPO_ERR_INVALID_ARG, "%s: NULL hidden/W", fn);
+    if (!aligned16(W) || (hidden && !aligned16(hidden)))
+        return fail(GRPO_ERR_ALIGNMENT, "%s: hidden/W must be 16-byte aligned", fn);
+    return GRPO_OK;
+}
+
+cublasHandle_t cublas_handle() {
+    static thread_local cublasHandle_t h = nullptr;
+    static thread_local int h_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!h || h_dev != dev) {
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
+        h_dev = dev;
+    }
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N) {
+    if (n_rows < 0) n_rows = 0;
+    if (V < 1) V = 1;
+    const size_t split = (size_t)grpo::lmhead_n_split(n_rows, V);
+    return grpo_async_workspace_size(n_rows, V, N) + align256(split * (size_t)n_rows * 8) +
+           align256((size_t)n_rows * 4) + 256;
+}
+
+grpo_status_t grpo_async_lmhead_fwd(const uint16_t *hidden, const uint16_t *W, int64_t row_begin,
+                                    int64_t n_rows, int32_t d, int32_t V,
+                                    const int64_t *target_ids, const float *logp_behav,
+                                    const int64_t *cu_seqlens, int32_t N,
+                                    const int32_t *traj_index, const float *adv,
+                                    const float *inv_norm, const grpo_loss_opts_t *opts,
+                                    float grad_scale, float *logp_out, float *lse_out,
+                                    float *token_scale_out, double *traj_sum, double *stats,
+                                    void *workspace, size_t workspace_bytes, grpo_stream_t stream) {
+    grpo_status_t st = lm_check("lmhead_fwd", hidden, W, n_rows, d, V);
+    if (st != GRPO_OK) return st;
+    if (!opts) return fail(GRPO_ERR_INVALID_ARG, "lmhead_fwd: NULL opts");
+    if (!(opts->eps_lo > 0.0f && opts->eps_lo < 1.0f) || !(opts->eps_hi > 0.0f))
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_fwd: eps_lo not in (0,1) or eps_hi <= 0");
+    if (N <= 0 || row_begin < 0) return fail(GRPO_ERR_INVALID_ARG, "lmhead_fwd: N/row_begin");
+    if (!cu_seqlens || !adv || !inv_norm || !traj_sum || !stats)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_fwd: NULL cu_seqlens/adv/inv_norm/traj_sum/stats");
+    if (n_rows > 0 && (!target_ids || !logp_behav))
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_fwd: NULL target_ids/logp_behav");
+    const size_t need = grpo_async_lmhead_workspace_size(n_rows, V, N);
+    if (!workspace || workspace_bytes < need)
+        return fail(GRPO_ERR_WORKSPACE, "lmhead_fwd: workspace %zu B < required %zu B", workspace_bytes,
+                    need);
+    grpo::LossArgs a{};
+    a.V = V;
+    a.row_begin = row_begin;
+    a.n_rows = n_rows;
+    a.target_ids = target_ids;
+    a.logp_behav = logp_behav;
+    a.cu_seqlens = cu_seqlens;
+    a.N = N;
+    a.traj_index = traj_index;
+    a.adv = adv;
+    a.inv_norm = inv_norm;
+    a.eps_lo = opts->eps_lo;
+    a.eps_hi = opts->eps_hi;
+    a.grad_scale = grad_scale;
+    a.logp_out = logp_out;
+    a.lse_out = lse_out;
+    a.scale_out = token_scale_out;
+    a.traj_sum = traj_sum;
+    a.stats = stats;
+    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
+    uint8_t *const w0 = w;
+    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
+    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
+    a.term_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.logp_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.flag_ws = w;
+    w += align256((size_t)n_rows);
+    a.part_ws = reinterpret_cast<double *>(w);
+    w = w0 + grpo_async_workspace_size(n_rows, V, N) - 256;  // past the standard carve-up
+    const int32_t n_split = grpo::lmhead_n_split(n_rows, V);
+    float2 *part = reinterpret_cast<float2 *>(w);
+    w += align256((size_t)n_split * (size_t)n_rows * 8);
+    float *zy = reinterpret_cast<float *>(w);
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_rowinfo(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_fwd/rowinfo");
+    const bool traced = n_rows > 0 && prof_on();
+    std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+    if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "lmhead_fwd/profile");
+    e = grpo::launch_lmhead(0, hidden, W, n_rows, d, V, a.rowinfo, part, zy, nullptr, 0, nullptr, nullptr,
+                            nullptr, 1.0f, s, &launches, &g_last_plan, why, sizeof why);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_fwd/tcgen05", why);
+    if (traced && (e = prof_end(s, ev)) != cudaSuccess) return cuda_fail(e, "lmhead_fwd/profile");
+    e = grpo::launch_lmhead_combine(part, zy, n_split, a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_fwd/combine");
+    e = grpo::launch_segment_reduce(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_fwd/segment_reduce");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_lmhead_bwd(const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
+                                    int32_t d, int32_t V, const int64_t *target_ids,
+                                    const float *lse, const float *token_scale,
+                                    float grad_scale_mult, uint16_t *dz, int64_t ld_dz,
+                                    uint16_t *dhidden, float *dW, grpo_stream_t stream) {
+    grpo_status_t st = lm_check("lmhead_bwd", hidden, W, n_rows, d, V);
+    if (st != GRPO_OK) return st;
+    if (n_rows > 0 && (!target_ids || !lse || !token_scale || !dz))
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_bwd: NULL target_ids/lse/token_scale/dz");
+    if (ld_dz < V || ld_dz % 8 != 0 || (dz && !aligned16(dz)))
+        return fail(GRPO_ERR_ALIGNMENT, "lmhead_bwd: ld_dz=%lld must be >= V, a multiple of 8, dz aligned",
+                    (long long)ld_dz);
+    if (n_rows == 0) return ok(0);
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_lmhead(1, hidden, W, n_rows, d, V, nullptr, nullptr, nullptr, dz, ld_dz,
+                                        target_ids, lse, token_scale, grad_scale_mult, s, &launches,
+                                        &g_last_plan, why, sizeof why);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_bwd/tcgen05", why);
+    if (dhidden || dW) {
+        cublasHandle_t h = cublas_handle();
+        if (!h) return fail(GRPO_ERR_CUDA, "lmhead_bwd: cublasCreate failed");
+        if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_bwd: cublasSetStream");
+        const float one = 1.0f, zero = 0.0f;
+        // column-major views: W -> [d, V], dz -> [V, n_rows] (ld ld_dz), hidden -> [d, n_rows]
+        if (dhidden) {  // dhidden^T [d, n] = W^T [d, V] * dz^T [V, n]
+            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, d, (int)n_rows, V, &one, W, CUDA_R_16BF,
+                                             d, dz, CUDA_R_16BF, (int)ld_dz, &zero, dhidden, CUDA_R_16BF, d,
+                                             CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_bwd: dhidden GEMM status %d", (int)cs);
+        }
+        if (dW) {  // dW^T [d, V] += hidden^T [d, n] * dz [n, V]
+            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, d, V, (int)n_rows, &one, hidden,
+                                             CUDA_R_16BF, d, dz, CUDA_R_16BF, (int)ld_dz, &one, dW, CUDA_R_32F, d,
+                                             CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_bwd: dW GEMM status %d", (int)cs);
+        }
+    }
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
+                                       int32_t d, int32_t V, uint16_t *out, int64_t ld_out,
+                                       grpo_stream_t stream) {
+    grpo_status_t st = lm_check("lmhead_logits", hidden, W, n_rows, d, V);
+    if (st != GRPO_OK) return st;
+    if (n_rows > 0 && !out) return fail(GRPO_ERR_INVALID_ARG, "lmhead_logits: NULL out");
+    if (ld_out < V || ld_out % 8 != 0 || (out && !aligned16(out)))
+        return fail(GRPO_ERR_ALIGNMENT, "lmhead_logits: ld_out=%lld must be >= V, a multiple of 8",
+                    (long long)ld_out);
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_lmhead(2, hidden, W, n_rows, d, V, nullptr, nullptr, nullptr, out, ld_out,
+                                        nullptr, nullptr, nullptr, 1.0f, (cudaStream_t)stream, &launches,
+                                        &g_last_plan, why, sizeof why);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_logits/tcgen05", why);
     return ok(launches);
 }
 

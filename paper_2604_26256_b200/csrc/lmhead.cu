@@ -1,0 +1,387 @@
+// lmhead.cu -- SURVEY NEXT(2): the loss fused with the LM head that produces the
+// logits.  z = X W^T (X: hidden states [n, d], W: LM-head weight [V, d], both bf16)
+// runs on the 5th-generation tensor cores (tcgen05.mma, accumulators in TMEM,
+// operands staged by TMA in 128-byte-swizzled shared memory) and the epilogue
+// consumes each 128 x 256 accumulator tile straight out of TMEM:
+//
+//   EPI_STATS  per-row log2-domain softmax partials (max, sum 2^(t - max)) and z_y
+//              -> lmhead_combine_kernel -> log pi_theta(y_t) and the
+//              per-token epilogue of eq:grpo_async -- the logits never reach HBM;
+//   EPI_DZ     the logits gradient dJ/dz = s_t (softmax(z) - onehot(y_t)) of the same
+//              tile (recomputed in the backward, as Cut-Cross-Entropy does) -> bf16;
+//   EPI_LOGITS the bf16 logits themselves (the unfused producer; also the GEMM check).
+//
+// One CTA per SM, persistent, warp-specialised: warp 0 issues TMA, warp 1 issues
+// tcgen05.mma (one thread) into one of two 256-column TMEM accumulators, warps 2-5
+// drain the other accumulator (each thread owns one row = one TMEM lane).
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace grpo {
+namespace lm {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 192;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /* align */ + 256 /* barriers */;
+constexpr uint32_t TMEM_COLS = 2 * BN;
+
+enum { EPI_STATS = 0, EPI_DZ = 1, EPI_LOGITS = 2 };
+
+struct Params {
+    int32_t n_rows, V, d;
+    int32_t m_tiles, n_vt, vt_per_unit, n_units;
+    // EPI_STATS
+    const RowInfo *rowinfo;
+    float2 *part;  // [n_split][n_rows] log2-domain (max, sum)
+    float *zy;     // [n_rows]
+    // EPI_DZ / EPI_LOGITS
+    uint16_t *out;  // [n_rows][ld_out] bf16
+    int64_t ld_out;
+    const int64_t *targets;
+    const float *lse;    // natural-log lse per row (from the forward)
+    const float *scale;  // s_t per row
+    float mult;          // extra factor on s_t (EPI_DZ)
+};
+
+__device__ __forceinline__ void decode(const Params &p, int unit, int &m_tile, int &split) {
+    split = unit / p.m_tiles;
+    m_tile = unit - split * p.m_tiles;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    lmhead_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                  const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = smem;                             // STAGES x A_BYTES
+    uint8_t *sB = smem + STAGES * A_BYTES;          // STAGES x B_BYTES
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES,
+             *tempty = bars + 2 * STAGES + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nk = p.d / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tc::prefetch_tmap(&tmX);
+        tc::prefetch_tmap(&tmW);
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_normal();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+                int m_tile, split;
+                decode(p, unit, m_tile, split);
+                const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
+                for (int vt = vt0; vt < vt1; ++vt)
+                    for (int kb = 0; kb < nk; ++kb) {
+                        mbar_wait(empty + stage, phase ^ 1u);
+                        mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
+                        tc::tma_load_2d(sA + stage * A_BYTES, &tmX, kb * BK, m_tile * BM, full + stage, pol_a);
+                        tc::tma_load_2d(sB + stage * B_BYTES, &tmW, kb * BK, vt * BN, full + stage, pol_b);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+                int m_tile, split;
+                decode(p, unit, m_tile, split);
+                const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
+                for (int vt = vt0; vt < vt1; ++vt) {
+                    mbar_wait(tempty + acc, acc_phase ^ 1u);
+                    tc::fence_after();
+                    const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+                    for (int kb = 0; kb < nk; ++kb) {
+                        mbar_wait(full + stage, phase);
+                        tc::fence_after();
+                        const uint64_t ad = tc::desc_k_sw128(sA + stage * A_BYTES);
+                        const uint64_t bd = tc::desc_k_sw128(sB + stage * B_BYTES);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the swizzle atom
+                            tc::mma_bf16(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                        tc::commit(empty + stage);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    }
+                    tc::commit(tfull + acc);
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 2-5)
+        const int q = warp & 3;                 // TMEM lane quarter this warp may access
+        const int r_in_tile = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+            int m_tile, split;
+            decode(p, unit, m_tile, split);
+            const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
+            const int row = m_tile * BM + r_in_tile;
+            const bool valid = row < p.n_rows;
+            int32_t y = -1;
+            float lse2 = 0.0f, sc = 0.0f;
+            if (EPI == EPI_STATS) {
+                y = valid ? p.rowinfo[row].target : -1;
+            } else if (EPI == EPI_DZ && valid) {
+                const int64_t t = p.targets[row];
+                y = (t >= 0 && t < p.V) ? (int32_t)t : -1;
+                lse2 = p.lse[row] * kLog2e;
+                sc = p.scale[row] * p.mult;
+            }
+            float M = -INFINITY, S = 0.0f, zy = 0.0f;
+            bool have_y = false;
+            for (int vt = vt0; vt < vt1; ++vt) {
+                mbar_wait(tfull + acc, acc_phase);
+                tc::fence_after();
+                const int v0 = vt * BN;
+                const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tc::tmem_ld32(t_row + (uint32_t)(c * 32), r);
+                    tc::tmem_wait_ld();
+                    const int cb = v0 + c * 32;          // first vocabulary column of the chunk
+                    const int nvalid = min(32, p.V - cb);  // > 0 except in a ragged last tile
+                    if (EPI == EPI_STATS) {
+                        float t[32];
+                        float cm = -INFINITY;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            t[j] = j < nvalid ? __uint_as_float(r[j]) * kLog2e : -INFINITY;
+                            cm = fmaxf(cm, t[j]);
+                        }
+                        if (cm > M) {
+                            S = (M == -INFINITY) ? 0.0f : S * ex2(M - cm);
+                            M = cm;
+                        }
+                        if (M != -INFINITY) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) S += ex2(t[j] - M);
+                        }
+                        if (y >= cb && y < cb + 32) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (cb + j == y) zy = __uint_as_float(r[j]);
+                            have_y = true;
+                        }
+                    } else if (valid && nvalid > 0) {
+                        uint32_t w[16];
+                        if (EPI == EPI_LOGITS) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                w[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+                        } else {  // EPI_DZ: s (p - onehot); exact zeros when s == 0
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                float g[2];
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) {
+                                    const int jj = 2 * j + h;
+                                    const float pr = ex2(fmaf(__uint_as_float(r[jj]), kLog2e, -lse2));
+                                    g[h] = sc == 0.0f ? 0.0f : sc * (pr - (cb + jj == y ? 1.0f : 0.0f));
+                                }
+                                w[j] = pack_bf16x2(g[0], g[1]);
+                            }
+                        }
+                        uint16_t *dst = p.out + (int64_t)row * p.ld_out + cb;
+                        if (nvalid == 32) {
+                            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                d4[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (j < nvalid) dst[j] = (uint16_t)(j & 1 ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xFFFFu));
+                        }
+                    }
+                }
+                tc::fence_before();
+                mbar_arrive(tempty + acc);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1u;
+            }
+            if (EPI == EPI_STATS && valid) {
+                p.part[(int64_t)split * p.n_rows + row] = make_float2(M, S);
+                if (have_y) p.zy[row] = zy;
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem_base, TMEM_COLS);
+}
+
+// per row: merge the n_split partials in split order (deterministic), then the
+// per-token epilogue shared with the logits kernels
+__global__ void __launch_bounds__(256) lmhead_combine_kernel(const float2 *__restrict__ part,
+                                                             const float *__restrict__ zy_ws,
+                                                             int32_t n_split, LossArgs a) {
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= a.n_rows) return;
+    float M = -INFINITY, S = 0.0f;
+    for (int s = 0; s < n_split; ++s) {
+        const float2 v = part[(int64_t)s * a.n_rows + row];
+        lse2_merge(M, S, v.x, v.y);
+    }
+    const RowInfo ri = a.rowinfo[row];
+    const bool y_valid = ri.target >= 0 && ri.target < a.V;
+    const float zyv = y_valid ? zy_ws[row] : __int_as_float(0x7FC00000);
+    const float l2s = log2f(S);
+    const double logp_d = row_logp(zyv, M, l2s);
+    const RowOut o = row_epilogue(logp_d, ri, a.eps_lo, a.eps_hi, a.grad_scale);
+    const float logp = (float)logp_d;
+    if (a.logp_out) a.logp_out[row] = logp;
+    if (a.lse_out) a.lse_out[row] = (M + l2s) * kLn2;
+    if (a.scale_out) a.scale_out[row] = o.s;
+    a.term_ws[row] = o.term;
+    a.logp_ws[row] = logp;
+    a.flag_ws[row] = o.flags;
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// [rows, d] bf16 row-major, box [box_rows, 64] with the 128-byte swizzle
+static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int32_t d, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace lm
+
+// vocabulary tiles per work unit: units = m_tiles x ceil(n_vt / vt_per_unit)
+int32_t lmhead_vt_per_unit(int64_t n_rows) {
+    const int64_t m_tiles = (n_rows + lm::BM - 1) / lm::BM;
+    return (int32_t)std::max<int64_t>(1, std::min<int64_t>(8, (m_tiles + 1) / 2));
+}
+int32_t lmhead_n_split(int64_t n_rows, int32_t V) {
+    const int32_t n_vt = (V + lm::BN - 1) / lm::BN;
+    const int32_t vpu = lmhead_vt_per_unit(n_rows);
+    return (n_vt + vpu - 1) / vpu;
+}
+
+cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows, int32_t d, int32_t V,
+                          const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,
+                          const int64_t *targets, const float *lse, const float *scale, float mult,
+                          cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len) {
+    using namespace lm;
+    if (n_rows == 0) return cudaSuccess;
+    CUtensorMap mx, mw;
+    if (!make_map(&mx, X, n_rows, d, BM) || !make_map(&mw, W, V, d, BN)) {
+        if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
+        return cudaErrorInvalidValue;
+    }
+    Params p{};
+    p.n_rows = (int32_t)n_rows;
+    p.V = V;
+    p.d = d;
+    p.m_tiles = (int32_t)((n_rows + BM - 1) / BM);
+    p.n_vt = (V + BN - 1) / BN;
+    p.vt_per_unit = lmhead_vt_per_unit(n_rows);
+    const int32_t n_split = (p.n_vt + p.vt_per_unit - 1) / p.vt_per_unit;
+    p.n_units = p.m_tiles * n_split;
+    p.rowinfo = rowinfo;
+    p.part = part;
+    p.zy = zy;
+    p.out = out;
+    p.ld_out = ld_out;
+    p.targets = targets;
+    p.lse = lse;
+    p.scale = scale;
+    p.mult = mult;
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min(p.n_units, n_sm);
+    cudaError_t e;
+#define GRPO_LM_LAUNCH(E)                                                                               \
+    do {                                                                                                \
+        e = cudaFuncSetAttribute(lmhead_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); \
+        if (e != cudaSuccess) return e;                                                                 \
+        lmhead_kernel<E><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mx, mw, p);                             \
+    } while (0)
+    if (epi == EPI_STATS) GRPO_LM_LAUNCH(EPI_STATS);
+    else if (epi == EPI_DZ) GRPO_LM_LAUNCH(EPI_DZ);
+    else GRPO_LM_LAUNCH(EPI_LOGITS);
+#undef GRPO_LM_LAUNCH
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+    if (plan) {
+        *plan = grpo_plan_t{};
+        plan->kernel = 4 + epi;
+        plan->grid = grid;
+        plan->ctas_per_sm = 1;
+        plan->stages = STAGES;
+        plan->vec_per_thread = p.vt_per_unit;
+        plan->max_clusters = p.n_units;
+        plan->smem_bytes = SMEM_BYTES;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_lmhead_combine(const float2 *part, const float *zy, int32_t n_split, const LossArgs &a,
+                                  cudaStream_t s, int *launches) {
+    if (a.n_rows == 0) return cudaSuccess;
+    lm::lmhead_combine_kernel<<<(unsigned)((a.n_rows + 255) / 256), 256, 0, s>>>(part, zy, n_split, a);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace grpo

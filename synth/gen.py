@@ -335,3 +335,14 @@ def make_manual(P, G, K, V, lengths, group_ids, rewards, version_ids, target_ids
                  None if token_version is None else np.asarray(token_version, np.int64),
                  np.asarray(rewards, np.float32), np.asarray(target_ids, np.int64),
                  np.asarray(logp_behav, np.float32), L, None)
+
+
+def lmhead_inputs(T, V, d, seed, w_scale=2.5):
+    """NEXT(2) inputs (TEST/BENCH INPUT GENERATOR): bf16 bit patterns of hidden states
+    X [T, d] ~ N(0, 1) and an LM-head weight W [V, d] ~ N(0, (w_scale / sqrt(d))^2), so the
+    logits z = X W^T have a standard deviation of about w_scale (DESIGN.md input recipe)."""
+    rng = np.random.default_rng(np.random.SeedSequence([int(seed), 0x4C4D]))
+    X = f32_to_bf16_bits(rng.standard_normal((T, d), dtype=np.float32))
+    W = f32_to_bf16_bits(rng.standard_normal((V, d), dtype=np.float32) *
+                         np.float32(w_scale / np.sqrt(d)))
+    return X, W

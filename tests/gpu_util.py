@@ -204,3 +204,73 @@ def run_gpu_vp(batch, logits_bits, device, world, chunks=1, grad_scale=1.0, eps=
         out["dlogits"] = bf16_bits_to_f32(raw[:, :V]).astype(np.float64)
         out["shard_pad_untouched"] = bool(np.all(cat[:, V:] == 0x7FC3))
     return out
+
+
+def lmhead_batch(name, seed, d, sigma=0.05):
+    """A synth batch with LM-head inputs X, W and behaviour log-probs built from the
+    oracle's own logp (test-side input construction): logp_w = f32(logp - delta),
+    delta ~ N(0, (sigma (1 + staleness gap))^2)."""
+    import dataclasses
+
+    from synth.gen import lmhead_inputs, make_batch
+    b = make_batch(name, seed)
+    X, W = lmhead_inputs(b.T, b.V, d, seed)
+    z = O.lmhead_logits(X, W)
+    m = z.max(axis=1, keepdims=True)
+    lse = (m + np.log(np.exp(z - m).sum(axis=1, keepdims=True)))[:, 0]
+    logp = z[np.arange(b.T), b.target_ids] - lse
+    gap = np.repeat(b.v_theta - b.version_ids, b.lengths).astype(np.float64)
+    rng = np.random.default_rng(seed + 77)
+    lw = (logp - rng.normal(size=b.T) * sigma * (1 + gap)).astype(np.float32)
+    return dataclasses.replace(b, logp_behav=lw), X, W
+
+
+def run_gpu_lmhead(batch, X, W, device, chunks=1, want_grads=True, grad_scale=1.0, eps=0.2,
+                   eps_hi=None, norm="seq", traj_mask=None):
+    """NEXT(2) on the GPU: validate, advantage, lmhead_fwd over row chunks, lmhead_bwd."""
+    db = G.DeviceBatch.from_host(batch, device)
+    mask_d = None if traj_mask is None else torch.from_numpy(
+        np.ascontiguousarray(traj_mask, np.uint8)).to(device)
+    loss = G.GrpoAsyncLoss(eps=eps, grad_scale=grad_scale, eps_hi=eps_hi, norm=norm,
+                           traj_mask=mask_d)
+    vo = loss.validate(db)
+    adv, inv = loss.advantage(db)
+    T, V = batch.T, batch.V
+    d = X.shape[1]
+    Xd = to_dev_bits(X, device).view(torch.bfloat16)
+    Wd = to_dev_bits(W, device).view(torch.bfloat16)
+    logp = torch.full((T,), float("nan"), device=device)
+    lse = torch.full((T,), float("nan"), device=device)
+    scale = torch.full((T,), float("nan"), device=device)
+    traj_sum = torch.zeros(batch.N, dtype=torch.float64, device=device)
+    stats = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=device)
+    ld = (V + 7) // 8 * 8 + 8
+    dz = torch.full((T, ld), 0x7FC3, dtype=torch.int16, device=device).view(torch.bfloat16)
+    dX = torch.full((T, d), float("nan"), device=device).bfloat16()
+    dW = torch.zeros((V, d), dtype=torch.float32, device=device)
+    bounds = np.linspace(0, T, chunks + 1).astype(np.int64)
+    for c in range(chunks):
+        b, e = int(bounds[c]), int(bounds[c + 1])
+        loss.lmhead_fwd(Xd[b:e], Wd, b, e - b, db.target_ids[b:e], db.logp_behav[b:e],
+                        db.cu_seqlens, adv, inv, traj_sum, stats, logp_out=logp[b:e],
+                        lse_out=lse[b:e], scale_out=scale[b:e])
+        if want_grads:
+            loss.lmhead_bwd(Xd[b:e], Wd, e - b, db.target_ids[b:e], lse[b:e], scale[b:e], dz[b:e],
+                            dhidden=dX[b:e], dW=dW)
+    torch.cuda.synchronize()
+    out = dict(
+        traj_flags=vo.traj_flags.cpu().numpy().view(np.uint32)[:batch.N],
+        group_count=vo.group_count.cpu().numpy(),
+        stale_hist=vo.stale_hist.cpu().numpy().reshape(batch.P, batch.K + 1),
+        summary=vo.summary_dict(), adv=adv.cpu().numpy(), inv_norm=inv.cpu().numpy(),
+        logp=logp.cpu().numpy().astype(np.float64), lse=lse.cpu().numpy().astype(np.float64),
+        scale=scale.cpu().numpy().astype(np.float64), traj_sum=traj_sum.cpu().numpy(),
+        stats=stats.cpu().numpy(), launches=loss.launches, inplace=False)
+    if want_grads:
+        raw = dz.view(torch.int16).cpu().numpy().view(np.uint16)
+        out["dlogits_raw"] = raw
+        out["dlogits"] = bf16_bits_to_f32(raw[:, :V]).astype(np.float64)
+        out["dz_pad_untouched"] = bool(np.all(raw[:, V:] == 0x7FC3))
+        out["dhidden"] = dX.float().cpu().numpy().astype(np.float64)
+        out["dW"] = dW.cpu().numpy().astype(np.float64)
+    return out
