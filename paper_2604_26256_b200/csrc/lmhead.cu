@@ -48,9 +48,18 @@ struct Params {
     float mult;          // extra factor on s_t (EPI_DZ)
 };
 
+// Units are rastered in groups of GROUP_M row tiles: the CTAs running at the same
+// time cover ~GROUP_M row tiles x ~grid/GROUP_M vocabulary tiles, so the X and W tiles
+// they stream (re-read once per tile of the other operand) stay resident in L2.
+constexpr int GROUP_M = 16;
 __device__ __forceinline__ void decode(const Params &p, int unit, int &m_tile, int &split) {
-    split = unit / p.m_tiles;
-    m_tile = unit - split * p.m_tiles;
+    const int n_split = (p.n_vt + p.vt_per_unit - 1) / p.vt_per_unit;
+    const int per_group = GROUP_M * n_split;
+    const int grp = unit / per_group;
+    const int rem = unit - grp * per_group;
+    const int gm = min(GROUP_M, p.m_tiles - grp * GROUP_M);  // row tiles in this group
+    split = rem / gm;
+    m_tile = grp * GROUP_M + (rem - split * gm);
 }
 
 template <int EPI>
