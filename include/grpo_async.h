@@ -111,13 +111,17 @@ typedef struct {
 
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
-    int32_t kernel;        /* 0 auto (= 2 today), 1 cluster-resident fused, 2 row-wise two-pass */
+    int32_t kernel;        /* 0 auto (= 2 today), 1 cluster-resident fused, 2 row-wise two-pass, */
+                           /* 3 one row per SM streamed through a bulk-copy ring (K3c)       */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
-    int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1); 1,2,4,8 (kernel 2: 1024/512/256/256 threads) */
+    int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1); 1,2,4,8 (kernel 2: 1024/512/256/256 threads); */
+                           /* kernel 3: 256 / 1024 consumer threads (default 512)              */
     int32_t stages;        /* 0 auto, else lag+2..8 shared-memory row stages per CTA (kernel 1); */
-                           /* kernel 2: 4, 8 or 16 vectors in flight per thread             */
+                           /* kernel 2: 4, 8 or 16 vectors in flight per thread; kernel 3:  */
+                           /* 16 KB ring slots, 2..13 (0 = 13)                              */
     int32_t lag;           /* 0 auto, else 1..2: rows between a row's reduction and its       */
-                           /* backward, hiding the cluster exchange (kernel 1)               */
+                           /* backward, hiding the cluster exchange (kernel 1); kernel 3:    */
+                           /* ring slots left free at the end of pass 1 (0 = 3)              */
     int32_t prefetch;      /* kernel 2: 1 = TMA-prefetch each CTA's next row into L2         */
     int32_t row_cache;     /* kernel 2: leading vectors per thread of each row kept in shared */
                            /* memory for the second pass (0 auto = 160 KB per SM, -1 none) */
@@ -355,8 +359,9 @@ grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W
 
 /* Launch plan of the last fused-loss launch made by the calling thread. */
 typedef struct {
-    int32_t kernel;        /* 1 cluster-resident, 2 row-wise, 3 vocab-parallel, 4/5/6 LM-head  */
-                           /* (tcgen05) loss partials / logits gradient / logits           */
+    int32_t kernel;        /* 1 cluster-resident, 2 row-wise, 3 streamed ring, 4/5/6 LM-head */
+                           /* (tcgen05) loss partials / logits gradient / logits, 7 vocab-  */
+                           /* parallel                                                      */
     int32_t cluster_size;  /* CTAs per row (kernel 1)                                 */
     int32_t ctas_per_sm;   /* requested residency (kernel 1)                          */
     int32_t stages;        /* shared-memory row stages per CTA (kernel 1)             */

@@ -278,7 +278,7 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     if (!workspace || workspace_bytes < need)
         return fail(GRPO_ERR_WORKSPACE, "loss_fwd: workspace %zu B < required %zu B",
                     workspace_bytes, need);
-    if (tune && (tune->kernel < 0 || tune->kernel > 2))
+    if (tune && (tune->kernel < 0 || tune->kernel > 3))
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: tune->kernel %d", tune->kernel);
 
     grpo::LossArgs a;
@@ -329,6 +329,9 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     if (kernel == 0 || kernel == 2) {
         e = grpo::launch_fused_rowwise(a, tune, s, &launches, &g_last_plan);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");
+    } else if (kernel == 3) {
+        e = grpo::launch_fused_stream(a, tune, s, &launches, &g_last_plan, why, sizeof why);
+        if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/stream", why);
     } else {
         e = grpo::launch_fused_cluster(a, tune, s, &launches, why, sizeof why, &g_last_plan);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/fused_cluster", why);

@@ -393,6 +393,8 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
 cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
                                  int *launches, grpo_plan_t *plan);
 cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches);
+cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s, int *launches,
+                                grpo_plan_t *plan, char *why, size_t why_len);
 int32_t lmhead_n_split(int64_t n_rows, int32_t V);
 cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows, int32_t d, int32_t V,
                           const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,

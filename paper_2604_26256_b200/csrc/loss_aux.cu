@@ -117,6 +117,16 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
     int parity = 0;
     for (int64_t row = grp; row < p.n_rows; row += n_grp, parity ^= 1) {
         const uint16_t *zrow = p.logits + row * p.ld + (int64_t)vec_lo * 8;
+        // the epilogue's dependent global reads (row info, then z_y), issued before pass 1
+        // so that they do not stall the CTA at its end
+        RowInfo ri_pre;
+        uint16_t zy_pre = 0;
+        if (warp == 0) {
+            ri_pre = p.rowinfo[row];
+            const int y_loc = ri_pre.target - vec_lo * 8;
+            if (ri_pre.target >= 0 && ri_pre.target < p.V && y_loc >= 0 && y_loc < n_vec * 8)
+                zy_pre = zrow[y_loc];
+        }
         // ---- pass 1
         float a = -INFINITY, s = 0.0f;
         for (int bi = 0; bi < n_full; ++bi) {
@@ -156,11 +166,11 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                 cs = red[lane].y;
             }
             warp_lse2_combine(cm, cs);
-            const RowInfo ri = p.rowinfo[row];  // broadcast load
+            const RowInfo ri = ri_pre;
             const bool y_valid = ri.target >= 0 && ri.target < p.V;
             const int y_loc = ri.target - vec_lo * 8;
             const bool mine = y_valid && y_loc >= 0 && y_loc < n_vec * 8;
-            float zy = mine ? __uint_as_float(((uint32_t)zrow[y_loc]) << 16) : 0.0f;
+            float zy = mine ? __uint_as_float(((uint32_t)zy_pre) << 16) : 0.0f;
             if (C > 1) {
                 // every CTA of the cluster gets this CTA's partial (and z_y if it owns y)
                 if (lane < C) {

@@ -1,0 +1,327 @@
+// loss_stream.cu -- K3c: the fused loss as one row per SM streamed through a TMA ring.
+//
+// K3b (loss_aux.cu) keeps the head of each row in shared memory and re-reads the rest
+// from L2 in pass 2; with two 304 KB rows in flight per SM about 10 % of the re-reads
+// miss L2.  K3c gives each SM one row at a time and moves it with the bulk-copy engine
+// (cp.async.bulk global -> shared, completion on mbarriers) into a FIFO ring of NS
+// 16 KB slots, so the loads need neither registers nor L1 staging and almost the whole
+// shared memory holds row data:
+//
+//   producer (one thread)   loads, per row, chunks 0..n-1 (pass 1) and then re-loads
+//                           chunks 0..n-R-1 (the part of the row that did not stay
+//                           resident) for pass 2, slot k % NS for the k-th load;
+//   consumers (NT threads)  pass 1 over chunks 0..n-1 (log2-domain max / sum), releasing
+//                           chunks 0..n-R-1; block reduction + fp64 row epilogue; pass 2
+//                           over the resident chunks n-R..n-1, then the re-loaded ones,
+//                           writing dlogits and releasing every slot.
+//
+// Consumption order equals load order, so the ring is strictly FIFO: load k waits for
+// the release of load k - NS (parity (k / NS) & 1).  R = NS - PF keeps PF slots free at
+// the end of pass 1 so the re-loads (from L2: the row was read moments ago) are in flight
+// while the CTA reduces; the next row's pass-1 loads fill the slots pass 2 releases.
+#include <cstdio>
+
+#include "common.cuh"
+#include "rowwise.cuh"
+
+namespace grpo {
+namespace k3c {
+
+constexpr int CHUNK_BYTES = 16384;
+constexpr int CHUNK_VECS = CHUNK_BYTES / 16;  // 1024 8-element vectors
+
+struct Params {
+    const uint16_t *logits;
+    uint16_t *dlogits;
+    int64_t ld;
+    int32_t V;
+    int64_t n_rows;
+    const RowInfo *rowinfo;
+    float eps_lo, eps_hi, grad_scale;
+    float *logp_out, *lse_out, *scale_out, *term_ws, *logp_ws;
+    uint8_t *flag_ws;
+    int32_t ns;  // ring slots
+    int32_t pf;  // slots kept free at the end of pass 1
+};
+
+struct Geometry {
+    int n_vec;       // 8-element vectors per row (ceil(V / 8))
+    int n;           // chunks per row
+    int R;           // chunks resident after pass 1 (re-consumed without a load)
+    int loads;       // loads per row: n + (n - R)
+    int tail_valid;  // valid elements of the last vector
+};
+
+__device__ __forceinline__ Geometry geometry(const Params &p, bool two_pass) {
+    Geometry g;
+    g.n_vec = (p.V + 7) / 8;
+    g.n = (g.n_vec + CHUNK_VECS - 1) / CHUNK_VECS;
+    g.R = two_pass ? min(g.n, max(0, p.ns - p.pf)) : 0;
+    g.loads = two_pass ? 2 * g.n - g.R : g.n;
+    g.tail_valid = p.V - (g.n_vec - 1) * 8;
+    return g;
+}
+
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
+    constexpr int U = CHUNK_VECS / NT;  // vectors per consumer thread per chunk
+    constexpr int NW = NT / 32;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint4 *ring = reinterpret_cast<uint4 *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.ns * CHUNK_BYTES);
+    uint64_t *empty = full + p.ns;
+    __shared__ float2 red[NW];
+    __shared__ float row_scalars[4];
+    const bool two_pass = p.dlogits != nullptr;
+    const Geometry g = geometry(p, two_pass);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.ns; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int64_t row0 = blockIdx.x, rstep = gridDim.x;
+    if (warp == NW) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pol_keep = policy_evict_last(), pol_once = policy_evict_first();
+            const int64_t row_bytes = (int64_t)g.n_vec * 16;
+            int slot = 0;
+            uint32_t par = 0;  // parity of the slot's current use
+            for (int64_t row = row0; row < p.n_rows; row += rstep) {
+                const uint8_t *src = reinterpret_cast<const uint8_t *>(p.logits + row * p.ld);
+                for (int i = 0; i < g.loads; ++i) {
+                    const int c = i < g.n ? i : i - g.n;  // chunk (pass-1 load or re-load)
+                    mbar_wait(empty + slot, par ^ 1u);
+                    const int64_t off = (int64_t)c * CHUNK_BYTES;
+                    const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
+                    // chunks read again from L2 in pass 2 stay; the rest streams through
+                    const uint64_t pol = (i < g.n && c < g.n - g.R && two_pass) ? pol_keep : pol_once;
+                    mbar_arrive_expect_tx(full + slot, bytes);
+                    bulk_g2s(ring + (size_t)slot * CHUNK_VECS, src + off, bytes, full + slot, pol);
+                    if (++slot == p.ns) {
+                        slot = 0;
+                        par ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
+    int slot = 0;      // slot of the next load this CTA consumes
+    uint32_t par = 0;  // and the parity of that slot's use
+    for (int64_t row = row0; row < p.n_rows; row += rstep) {
+        const int base_slot = slot;  // slot of this row's pass-1 chunk 0
+        // the epilogue's two dependent global reads (row info, then z_y), issued now so
+        // that they complete under pass 1 instead of stalling the whole CTA at its end
+        RowInfo ri;
+        uint16_t zy_bits = 0;
+        if (threadIdx.x == 0) {
+            ri = p.rowinfo[row];
+            if (ri.target >= 0 && ri.target < p.V) zy_bits = p.logits[row * p.ld + ri.target];
+        }
+        // ---- pass 1: log2-domain running (max, sum) per thread
+        float a = -INFINITY, s = 0.0f;
+        for (int c = 0; c < g.n; ++c) {
+            const int sl = slot;
+            mbar_wait(full + sl, par);
+            if (++slot == p.ns) {
+                slot = 0;
+                par ^= 1u;
+            }
+            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            uint4 x[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+            if (c == g.n - 1) {  // the ragged end of the row (uniform branch)
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
+                    if (vi >= g.n_vec) x[j] = neg_inf;
+                    else if (vi == g.n_vec - 1 && g.tail_valid < 8) x[j] = mask_tail(x[j], g.tail_valid);
+                }
+            }
+            // running max as the exponent reference: one extra ex2 only when it grows
+            uint32_t mx2 = bmax2(bmax2(x[0].x, x[0].y), bmax2(x[0].z, x[0].w));
+#pragma unroll
+            for (int j = 1; j < U; ++j) mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
+            const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
+            if (va > a) {
+                s = (a == -INFINITY) ? 0.0f : s * ex2(a - va);
+                a = va;
+            }
+            // with a = -inf every element so far is -inf: reference 0 keeps the terms 0
+            const float ref = a == -INFINITY ? 0.0f : a;
+            float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                t0 += ex2(fmaf(bf_lo(x[j].x), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].x), kLog2e, -ref)) +
+                      ex2(fmaf(bf_lo(x[j].y), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].y), kLog2e, -ref));
+                t1 += ex2(fmaf(bf_lo(x[j].z), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].z), kLog2e, -ref)) +
+                      ex2(fmaf(bf_lo(x[j].w), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].w), kLog2e, -ref));
+            }
+            s += t0 + t1;
+            if (c < g.n - g.R) {  // not resident: release now
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + sl);
+            }
+        }
+        // ---- block reduction and the per-row epilogue
+        warp_lse2_combine(a, s);
+        if (lane == 0) red[warp] = make_float2(a, s);
+        named_bar_sync(1, NT);
+        if (warp == 0) {
+            float cm = lane < NW ? red[lane].x : -INFINITY, cs = lane < NW ? red[lane].y : 0.0f;
+            warp_lse2_combine(cm, cs);
+            if (lane == 0) {
+                const bool y_valid = ri.target >= 0 && ri.target < p.V;
+                const float zy = y_valid ? __uint_as_float(((uint32_t)zy_bits) << 16) : __int_as_float(0x7FC00000);
+                const float l2s = log2f(cs);
+                const float lse2 = cm + l2s;
+                const double logp_d = row_logp(zy, cm, l2s);
+                const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
+                const float logp = (float)logp_d;
+                if (p.logp_out) p.logp_out[row] = logp;
+                if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
+                if (p.scale_out) p.scale_out[row] = o.s;
+                p.term_ws[row] = o.term;
+                p.logp_ws[row] = logp;
+                p.flag_ws[row] = o.flags;
+                row_scalars[0] = lse2;
+                row_scalars[1] = o.s;
+                row_scalars[2] = zy;
+                row_scalars[3] = __int_as_float(y_valid ? ri.target : -1);
+            }
+        }
+        named_bar_sync(1, NT);
+        if (!two_pass) continue;
+        // ---- pass 2: resident chunks n-R..n-1 (loads base+n-R..), then the re-loads
+        const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
+        const int32_t y = __float_as_int(row_scalars[3]);
+        const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
+        uint16_t *drow = p.dlogits + row * p.ld;
+        uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
+        for (int i = 0; i < g.n; ++i) {
+            const bool resident = i < g.R;
+            const int c = resident ? g.n - g.R + i : i - g.R;
+            int sl;
+            if (resident) {
+                sl = (base_slot + c) % p.ns;  // the pass-1 load of chunk c, still in its slot
+            } else {
+                sl = slot;
+                mbar_wait(full + sl, par);
+                if (++slot == p.ns) {
+                    slot = 0;
+                    par ^= 1u;
+                }
+            }
+            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            const int v0 = c * CHUNK_VECS + threadIdx.x;
+            if (c != g.n - 1) {  // full chunk: no checks
+                if (sc == 0.0f) {
+#pragma unroll
+                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, make_uint4(0u, 0u, 0u, 0u));
+                } else {
+                    uint4 x[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad(x[j], sc, lse2));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int vi = v0 + j * NT;
+                    if (vi >= g.n_vec) break;
+                    const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
+                                               : RowwiseBatch<NT, U>::grad(chunk[j * NT + threadIdx.x], sc, lse2);
+                    if (vi == g.n_vec - 1 && g.tail_valid < 8) store_tail(drow + (int64_t)vi * 8, d, g.tail_valid);
+                    else stg_stream(dst4 + vi, d);
+                }
+            }
+            // the target's own column, rewritten by the thread that stored its vector
+            if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
+                const float py = ex2(fmaf(zy, kLog2e, -lse2));
+                drow[y] = f2bf(sc * (py - 1.0f));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + sl);
+        }
+    }
+}
+
+}  // namespace k3c
+
+cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s, int *launches,
+                                grpo_plan_t *plan, char *why, size_t why_len) {
+    using namespace k3c;
+    if (a.n_rows == 0) return cudaSuccess;
+    Params p{};
+    p.logits = a.logits;
+    p.dlogits = a.dlogits;
+    p.ld = a.ld;
+    p.V = a.V;
+    p.n_rows = a.n_rows;
+    p.rowinfo = a.rowinfo;
+    p.eps_lo = a.eps_lo;
+    p.eps_hi = a.eps_hi;
+    p.grad_scale = a.grad_scale;
+    p.logp_out = a.logp_out;
+    p.lse_out = a.lse_out;
+    p.scale_out = a.scale_out;
+    p.term_ws = a.term_ws;
+    p.logp_ws = a.logp_ws;
+    p.flag_ws = a.flag_ws;
+    p.ns = (tune && tune->stages > 0) ? tune->stages : ((tune && tune->row_cache == 2) ? 6 : 13);
+    p.pf = (tune && tune->lag > 0) ? tune->lag : 3;
+    // consumer threads (ctas_per_sm 256 / 512) and CTAs per SM (row_cache 1 / 2)
+    const int nt = (tune && tune->ctas_per_sm == 256) ? 256 : 512;
+    const int cps = (tune && tune->row_cache == 2) ? 2 : 1;
+    if (p.ns < 2 || p.ns > (cps == 2 ? 6 : 13) || p.pf >= p.ns) {
+        if (why) snprintf(why, why_len, "stream kernel: stages %d (2..%d), lag %d (< stages)", p.ns,
+                          cps == 2 ? 6 : 13, p.pf);
+        return cudaErrorInvalidValue;
+    }
+    const size_t smem = (size_t)p.ns * CHUNK_BYTES + 2 * (size_t)p.ns * 8;
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)std::min<int64_t>(a.n_rows, (int64_t)n_sm * cps);
+    cudaError_t e;
+#define GRPO_K3C(NT_, MB_)                                                                              \
+    do {                                                                                               \
+        e = cudaFuncSetAttribute(stream_kernel<NT_, MB_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)smem);                                                           \
+        if (e != cudaSuccess) return e;                                                                \
+        stream_kernel<NT_, MB_><<<grid, NT_ + 32, smem, s>>>(p);                                       \
+    } while (0)
+    if (nt == 512 && cps == 1) GRPO_K3C(512, 1);
+    else if (nt == 512) GRPO_K3C(512, 2);
+    else if (cps == 1) GRPO_K3C(256, 1);
+    else GRPO_K3C(256, 2);
+#undef GRPO_K3C
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+    if (plan) {
+        *plan = grpo_plan_t{};
+        plan->kernel = 3;
+        plan->ctas_per_sm = cps;
+        plan->stages = p.ns;
+        plan->lag = p.pf;
+        plan->vec_per_thread = nt;
+        plan->grid = grid;
+        plan->smem_bytes = (int32_t)smem;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace grpo

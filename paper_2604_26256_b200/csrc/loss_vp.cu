@@ -353,7 +353,7 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned lo
     if (e != cudaSuccess) return e;
     if (plan) {
         *plan = grpo_plan_t{};
-        plan->kernel = 3;
+        plan->kernel = 7;
         plan->ctas_per_sm = CPS;
         plan->grid = (int32_t)(g_per * comm->n_local);
         plan->vec_per_thread = NT;

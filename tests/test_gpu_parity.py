@@ -10,7 +10,10 @@ from tests.gpu_util import compare, run_gpu, run_oracle, to_dev_bits
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [{"kernel": 1}, {"kernel": 2}]
+KERNELS = [{"kernel": 1}, {"kernel": 2}, {"kernel": 3}]
+STREAM_PLANS = [{"kernel": 3, "stages": st, "lag": lg, "ctas_per_sm": nt}
+                for st, lg, nt in ((13, 3, 0), (13, 1, 0), (13, 12, 0), (2, 1, 0), (5, 2, 0),
+                                   (8, 3, 256), (13, 3, 256))]
 ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u, "row_cache": rc, "cluster_size": cl}
                  for c, u, rc, cl in ((1, 4, -1, 1), (1, 2, 0, 1), (1, 8, 1, 1), (2, 4, -1, 1),
                                       (2, 4, 0, 1), (2, 8, 1, 1), (2, 8, 0, 1), (2, 2, 0, 1),
@@ -25,7 +28,7 @@ def _case(name, seed, **kw):
     return b, bits
 
 
-@pytest.mark.parametrize("tune", KERNELS, ids=["cluster", "rowwise"])
+@pytest.mark.parametrize("tune", KERNELS, ids=["cluster", "rowwise", "stream"])
 @pytest.mark.parametrize("seed", range(8))
 def test_tiny_full_parity(dev, tune, seed):
     b, bits = _case("tiny", seed)
@@ -34,7 +37,7 @@ def test_tiny_full_parity(dev, tune, seed):
     compare(gpu, ref, b, logits_pad=bits[:, b.V:])
 
 
-@pytest.mark.parametrize("tune", KERNELS, ids=["cluster", "rowwise"])
+@pytest.mark.parametrize("tune", KERNELS, ids=["cluster", "rowwise", "stream"])
 @pytest.mark.parametrize("name", ["mid32k", "mid152k", "ragged", "large_small"])
 def test_config_parity(dev, tune, name):
     b, bits = _case(name, 1)
@@ -88,7 +91,7 @@ def test_chunked_equals_oracle(dev, chunks):
     compare(gpu, ref, b, logits_pad=bits[:, b.V:])
 
 
-@pytest.mark.parametrize("tune", KERNELS, ids=["cluster", "rowwise"])
+@pytest.mark.parametrize("tune", KERNELS, ids=["cluster", "rowwise", "stream"])
 def test_inplace_and_forward_only(dev, tune):
     b, bits = _case("ragged", 4)
     ref = run_oracle(b, bits)
@@ -248,3 +251,19 @@ def test_sharded_equals_unsharded(dev, R):
     assert abs(st[Gp.STAT_J] - full["stats"][Gp.STAT_J]) <= 1e-12 * full["stats"][Gp.STAT_ABS]
     assert np.array_equal(logp.astype(np.float32), full["logp"].astype(np.float32))
     assert np.array_equal(traj_sum, full["traj_sum"])
+
+
+@pytest.mark.parametrize("plan", STREAM_PLANS,
+                         ids=lambda d: f"ns{d['stages']}pf{d['lag']}nt{d['ctas_per_sm'] or 512}")
+def test_stream_plans(dev, plan):
+    """K3c (one row per SM through the bulk-copy ring) for ring sizes from 2 slots (every
+    chunk but one re-loaded) to 13 (rows shorter than the ring: several rows resident),
+    out-of-place and forward-only, against the oracle."""
+    for name in ("tiny", "ragged", "mid152k"):
+        b, bits = _case(name, 8)
+        ref = run_oracle(b, bits)
+        gpu = run_gpu(b, bits, dev, tune=plan, chunks=2)
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+    ref = run_oracle(b, bits, want_dlogits=False)
+    gpu = run_gpu(b, bits, dev, tune=plan, want_dlogits=False)
+    compare(gpu, ref, b, check_dlogits=False)
