@@ -283,10 +283,10 @@ typedef struct {
     uint16_t *dlogits[GRPO_VP_MAX_RANKS];
     void *xbuf[GRPO_VP_MAX_RANKS];
     uint32_t epoch;
-    int32_t lag;  /* 1 (default): wait for row k-1's partials after pass 1 of row k; 0: wait
-                     right after each row's pass 1 (same results, bit for bit) */
-    int32_t static_rows; /* 0 (default): CTAs take rows in the order they ask for them;
-                            1: CTA g takes rows g, g + grid, ... (same results) */
+    int32_t lag;          /* 0 (default): wait for a row's partials right after its pass 1; */
+                          /* 1: after pass 1 of the next row (same results, bit for bit)     */
+    int32_t dynamic_rows; /* 0 (default): CTA g takes rows g, g + grid, ...; 1: CTAs take     */
+                          /* rows in the order they ask for them (same results)             */
 } grpo_vp_comm_t;
 
 grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_begin,

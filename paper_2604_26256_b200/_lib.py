@@ -77,7 +77,7 @@ class VpComm(C.Structure):
     _fields_ = [("world", C.c_int32), ("rank_begin", C.c_int32), ("n_local", C.c_int32),
                 ("shard_cols", C.c_int32), ("slots", C.c_int64), ("logits", C.c_void_p * VP_MAX_RANKS),
                 ("dlogits", C.c_void_p * VP_MAX_RANKS), ("xbuf", C.c_void_p * VP_MAX_RANKS),
-                ("epoch", C.c_uint32), ("lag", C.c_int32), ("static_rows", C.c_int32)]
+                ("epoch", C.c_uint32), ("lag", C.c_int32), ("dynamic_rows", C.c_int32)]
 
 
 class GrpoError(RuntimeError):
@@ -322,7 +322,7 @@ def grpo_async_loss_fwd_vp(world, rank_begin, shard_cols, slots, logits, dlogits
                            row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens, N,
                            traj_index, adv, inv_norm, eps_lo, eps_hi, norm, traj_mask, grad_scale,
                            logp_out, lse_out, token_scale_out, traj_sum, stats, workspace,
-                           stream=None, lag=1, static_rows=0):
+                           stream=None, lag=0, dynamic_rows=0):
     """logits / dlogits: the n_local local shards (bf16 tensors or raw device addresses);
     xbuf: all `world` exchange buffers as seen from this process (peer addresses), each
     2 * slots * world * 32 bytes."""
@@ -334,7 +334,7 @@ def grpo_async_loss_fwd_vp(world, rank_begin, shard_cols, slots, logits, dlogits
     c.world, c.rank_begin, c.n_local, c.shard_cols, c.slots, c.epoch = world, rank_begin, \
         n_local, shard_cols, slots, epoch
     c.lag = int(lag)
-    c.static_rows = int(static_rows)
+    c.dynamic_rows = int(dynamic_rows)
     for i in range(n_local):
         c.logits[i] = _addr(logits[i], "logits")
         c.dlogits[i] = _addr(dl[i], "dlogits")

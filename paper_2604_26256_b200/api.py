@@ -194,7 +194,7 @@ class GrpoAsyncLoss:
                                  target_ids, logp_behav, cu_seqlens, N, traj_index, adv, inv_norm,
                                  self.eps, self.eps_hi, self.norm, self.traj_mask, self.grad_scale,
                                  logp_out, lse_out, scale_out, traj_sum, stats, ws, stream,
-                                 lag=comm.lag, static_rows=comm.static_rows)
+                                 lag=comm.lag, dynamic_rows=comm.dynamic_rows)
         comm.epoch += 1
         self.launches += L.grpo_last_launch_count()
 
@@ -219,8 +219,8 @@ class VpGroup:
     def __init__(self, world, rank_begin, shard_cols, slots, xbuf, keep=()):
         self.world, self.rank_begin, self.shard_cols = world, rank_begin, shard_cols
         self.slots = slots
-        self.lag = 1              # grpo_vp_comm_t.lag
-        self.static_rows = 0      # grpo_vp_comm_t.static_rows
+        self.lag = 0              # grpo_vp_comm_t.lag
+        self.dynamic_rows = 0     # grpo_vp_comm_t.dynamic_rows
         self.xbuf = list(xbuf)
         self.epoch = 0
         self._keep = keep

@@ -322,12 +322,16 @@ cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cud
     p.prefetch = (tune && (tune->prefetch & 1)) ? 1 : 0;
     p.flags = 1;  // pass 2 newest-first (measured +2% over forward order, K3b)
     const int n_vec = (a.V + 7) / 8;
-    const int cps = (tune && tune->ctas_per_sm > 0) ? tune->ctas_per_sm : (n_vec >= 4096 ? 2 : 8);
+    // auto residency by row length (measured on B200): long rows
+    // want 2 x 512-thread CTAs with 80 KB of row cache each; mid rows (V ~ 48k-112k, e.g.
+    // the vocabulary shards of the tensor-parallel head) 4 x 256 threads; short rows 8.
+    const int cps = (tune && tune->ctas_per_sm > 0) ? tune->ctas_per_sm
+                                                    : (n_vec >= 14000 ? 2 : (n_vec >= 6000 ? 4 : 8));
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     int64_t blocks = 0;
-    const int U = (tune && tune->stages > 0) ? tune->stages : (cps <= 2 ? 8 : 4);
+    const int U = (tune && tune->stages > 0) ? tune->stages : (cps <= 4 ? 8 : 4);
     int nt = 0;
 #define GRPO_RW(NT_, U_, C_)                                                               \
     if (nt == 0 && cps_nt == NT_ && U == U_ && Cl == C_) {                                 \

@@ -284,39 +284,10 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
     }
 }
 
-cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned long long *row_ctr,
-                      cudaStream_t s, int *launches,
-                      grpo_plan_t *plan, char *why, size_t why_len) {
-    if (a.n_rows == 0) return cudaSuccess;
-    constexpr int NT = 512, U = 8, CPS = 2;
-    const int lag = comm->lag ? 1 : 0;
-    VpParams p = {};
-    p.world = comm->world;
-    p.rank_begin = comm->rank_begin;
-    p.n_local = comm->n_local;
-    p.shard_cols = comm->shard_cols;
-    for (int q = 0; q < comm->n_local; ++q) {
-        p.logits[q] = comm->logits[q];
-        p.dlogits[q] = comm->dlogits[q];
-    }
-    for (int q = 0; q < comm->world; ++q) p.xbuf[q] = static_cast<ulonglong2 *>(comm->xbuf[q]);
-    p.tag = comm->epoch + 1u;
-    p.row_ctr = row_ctr;
-    p.dynamic = comm->static_rows ? 0 : 1;
-    p.half = (int64_t)(comm->epoch & 1u) * comm->slots;
-    p.ld = a.ld;
-    p.V = a.V;
-    p.n_rows = a.n_rows;
-    p.rowinfo = a.rowinfo;
-    p.eps_lo = a.eps_lo;
-    p.eps_hi = a.eps_hi;
-    p.grad_scale = a.grad_scale;
-    p.logp_out = a.logp_out;
-    p.lse_out = a.lse_out;
-    p.scale_out = a.scale_out;
-    p.term_ws = a.term_ws;
-    p.logp_ws = a.logp_ws;
-    p.flag_ws = a.flag_ws;
+template <int NT, int U, int CPS>
+static cudaError_t launch_vp_plan(VpParams p, const grpo_vp_comm_t *comm, int lag, int64_t n_rows,
+                                  cudaStream_t s, int *launches, grpo_plan_t *plan, char *why,
+                                  size_t why_len) {
     const int n_vec = (comm->shard_cols + 7) / 8;
     int cv = (int)((size_t)(160 * 1024) / CPS / ((size_t)NT * 16));
     const int nv = (n_vec + NT - 1) / NT * (lag ? 2 : 1);
@@ -334,7 +305,7 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned lo
     if (e != cudaSuccess) return e;
     // every CTA must be resident (a CTA may wait for a peer rank's CTA of the same index)
     int64_t g_per = (int64_t)n_sm * (occ < CPS ? occ : CPS) / comm->n_local;
-    if (g_per > a.n_rows) g_per = a.n_rows;
+    if (g_per > n_rows) g_per = n_rows;
     if (g_per < 1) {
         if (why) snprintf(why, why_len, "vp kernel: no resident CTA per local rank");
         return cudaErrorInvalidConfiguration;
@@ -364,6 +335,45 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned lo
     }
     *launches += 1;
     return cudaSuccess;
+}
+
+cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned long long *row_ctr,
+                      cudaStream_t s, int *launches,
+                      grpo_plan_t *plan, char *why, size_t why_len) {
+    if (a.n_rows == 0) return cudaSuccess;
+    const int lag = comm->lag ? 1 : 0;
+    VpParams p = {};
+    p.world = comm->world;
+    p.rank_begin = comm->rank_begin;
+    p.n_local = comm->n_local;
+    p.shard_cols = comm->shard_cols;
+    for (int q = 0; q < comm->n_local; ++q) {
+        p.logits[q] = comm->logits[q];
+        p.dlogits[q] = comm->dlogits[q];
+    }
+    for (int q = 0; q < comm->world; ++q) p.xbuf[q] = static_cast<ulonglong2 *>(comm->xbuf[q]);
+    p.tag = comm->epoch + 1u;
+    p.row_ctr = row_ctr;
+    p.dynamic = comm->dynamic_rows ? 1 : 0;
+    p.half = (int64_t)(comm->epoch & 1u) * comm->slots;
+    p.ld = a.ld;
+    p.V = a.V;
+    p.n_rows = a.n_rows;
+    p.rowinfo = a.rowinfo;
+    p.eps_lo = a.eps_lo;
+    p.eps_hi = a.eps_hi;
+    p.grad_scale = a.grad_scale;
+    p.logp_out = a.logp_out;
+    p.lse_out = a.lse_out;
+    p.scale_out = a.scale_out;
+    p.term_ws = a.term_ws;
+    p.logp_ws = a.logp_ws;
+    p.flag_ws = a.flag_ws;
+    // the row-wise kernel's residency rule on the shard's row length (loss_aux.cu)
+    const int n_vec = (comm->shard_cols + 7) / 8;
+    if (n_vec >= 14000) return launch_vp_plan<512, 8, 2>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);
+    if (n_vec >= 6000) return launch_vp_plan<256, 8, 4>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);
+    return launch_vp_plan<256, 4, 8>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);
 }
 
 }  // namespace grpo

@@ -13,9 +13,14 @@ ap.add_argument("--rows", type=int, default=65536)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--plans", default="")
 ap.add_argument("--fwd-only", action="store_true")
+ap.add_argument("--vocab", type=int, default=0, help="override the config's V (e.g. a vocab shard)")
 args = ap.parse_args()
 dev = torch.device("cuda:0")
-b = make_batch(args.config, 0, period=args.rows)
+import dataclasses
+cfg = CONFIGS[args.config]
+if args.vocab:
+    cfg = dataclasses.replace(cfg, V=args.vocab)
+b = make_batch(cfg, 0, period=args.rows)
 R = args.rows
 V, ld = b.V, b.ld
 lg = torch.empty((R, ld), dtype=torch.int16, device=dev)

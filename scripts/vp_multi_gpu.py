@@ -108,11 +108,11 @@ def timing(rank, world, dev, rows, steps, warmup):
         return float(ms.item())
 
     modes = {}
-    for name, lag, st in (("static_lag0", 0, 1), ("static_lag1", 1, 1), ("dynamic_lag0", 0, 0),
-                          ("dynamic_lag1", 1, 0)):
-        comm.lag, comm.static_rows = lag, st
+    for name, lag, dyn in (("static_lag0", 0, 0), ("static_lag1", 1, 0), ("dynamic_lag0", 0, 1),
+                           ("dynamic_lag1", 1, 1)):
+        comm.lag, comm.dynamic_rows = lag, dyn
         modes[name] = timed(vp)
-    comm.lag, comm.static_rows = 1, 0
+    comm.lag, comm.dynamic_rows = 0, 0
     ms_vp = timed(vp)
     plan = G.grpo_async_last_plan()
     # the same per-rank bytes through the single-GPU kernel: a V = shard_cols problem

@@ -147,7 +147,7 @@ def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5,
 
 def run_gpu_vp(batch, logits_bits, device, world, chunks=1, grad_scale=1.0, eps=0.2,
                eps_hi=None, norm="seq", traj_mask=None, want_dlogits=True, calls=1,
-               shard_cols=None, lag=1, static_rows=0):
+               shard_cols=None, lag=0, dynamic_rows=0):
     """The vocabulary-parallel path (NEXT(3)) with all `world` ranks in one cooperative
     launch on one GPU: the logits are cut into world column shards of shard_cols columns,
     the per-rank dlogits shards are re-assembled into [T, ld] (padding left 0x7FC3).
@@ -162,7 +162,7 @@ def run_gpu_vp(batch, logits_bits, device, world, chunks=1, grad_scale=1.0, eps=
     T, ld, V = batch.T, batch.ld, batch.V
     comm = G.VpGroup.local(world, V, T, device, shard_cols)
     comm.lag = lag
-    comm.static_rows = static_rows
+    comm.dynamic_rows = dynamic_rows
     sc = comm.shard_cols
     ld_s = sc  # shard row stride (a multiple of 8)
     full = np.full((T, sc * world), 0x7FC1, np.uint16)

@@ -25,17 +25,17 @@ def test_vp_parity(dev, name, world):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_vp_schedules_match_bitwise(dev, world):
-    """The deferred wait (lag 1, default) and the immediate wait (lag 0), dynamic and
-    static row assignment, combine the same partials in the same order: identical
+    """The immediate wait (lag 0, default) and the deferred wait (lag 1), static and
+    dynamic row assignment, combine the same partials in the same order: identical
     per-row outputs and dlogits, bit for bit (traj_sum / J are fp64 sums whose order
     follows the segment reduce, not the schedule)."""
     b = make_batch("mid32k", 9)
     bits = b.logits_bits()
-    ref = run_gpu_vp(b, bits, dev, world, lag=1, static_rows=0)
-    for lag, st in ((0, 0), (0, 1), (1, 1)):
-        g = run_gpu_vp(b, bits, dev, world, lag=lag, static_rows=st)
+    ref = run_gpu_vp(b, bits, dev, world, lag=0, dynamic_rows=0)
+    for lag, dyn in ((1, 0), (0, 1), (1, 1)):
+        g = run_gpu_vp(b, bits, dev, world, lag=lag, dynamic_rows=dyn)
         for k in ("logp", "lse", "scale", "traj_sum", "stats", "dlogits_raw"):
-            assert np.array_equal(g[k], ref[k], equal_nan=True), (k, lag, st)
+            assert np.array_equal(g[k], ref[k], equal_nan=True), (k, lag, dyn)
 
 
 def test_vp_chunks_and_epochs(dev):
