@@ -111,7 +111,7 @@ typedef struct {
 
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
-    int32_t kernel;        /* 0 auto (= 2 today), 1 cluster-resident fused, 2 row-wise two-pass, */
+    int32_t kernel;        /* 0 auto (2 for V < 176000, else 3), 1 cluster-resident fused, 2 row-wise two-pass, */
                            /* 3 one row per SM streamed through a bulk-copy ring (K3c)       */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
     int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1); 1,2,4,8 (kernel 2: 1024/512/256/256 threads); */

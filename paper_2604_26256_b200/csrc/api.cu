@@ -324,12 +324,16 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     const bool traced = n_rows > 0 && prof_on();
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
-    // kernel 0 (auto) = the row-wise two-pass kernel: the faster of the two on
-    // B200 today (DESIGN.md "Kernel K3" measurements); 1 = cluster-resident.
-    if (kernel == 0 || kernel == 2) {
+    // kernel 0 (auto): the row-wise two-pass kernel (K3b) up to V ~ 176k, the streamed
+    // one-row-per-SM kernel (K3c) above, where K3b's L2 re-reads grow (DESIGN.md §8:
+    // V = 262144: K3c 0.90 vs K3b 0.79 of HBM; V = 152064: K3b 0.88 vs K3c 0.84).
+    const bool untuned = !tune || (tune->ctas_per_sm == 0 && tune->stages == 0 && tune->lag == 0 &&
+                                   tune->row_cache == 0 && tune->cluster_size == 0);
+    const bool auto_stream = kernel == 0 && untuned && (V + 7) / 8 >= 22000;
+    if ((kernel == 0 && !auto_stream) || kernel == 2) {
         e = grpo::launch_fused_rowwise(a, tune, s, &launches, &g_last_plan);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");
-    } else if (kernel == 3) {
+    } else if (kernel == 3 || auto_stream) {
         e = grpo::launch_fused_stream(a, tune, s, &launches, &g_last_plan, why, sizeof why);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/stream", why);
     } else {
