@@ -346,7 +346,7 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f)
-        if int(tr.get("V", -1)) == V:
+        if int(tr.get("V", -1)) == V and int(tr.get("plan_kernel", -1)) == int(plan["kernel"]):
             traffic = float(tr["dram_bytes_per_row"]) * rows_per_launch
     except Exception:
         pass
@@ -412,7 +412,8 @@ def main():
                                  "chunk buffer (DESIGN.md input recipe)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": {1: "fused_cluster_kernel", 2: "rowwise_kernel"}.get(
+                         "kernel": {1: "fused_cluster_kernel", 2: "rowwise_kernel",
+                                    3: "stream_kernel"}.get(
                              plan["kernel"], str(plan["kernel"])),
                          "plan": plan,
                          "bytes_per_row": bytes_per_row, "launches": n_traced,

@@ -111,20 +111,22 @@ typedef struct {
 
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
-    int32_t kernel;        /* 0 auto (2 for V < 176000, else 3), 1 cluster-resident fused, 2 row-wise two-pass, */
+    int32_t kernel;        /* 0 auto (2 for V < 90000, else 3 with 32 KB slots), 1 cluster-resident, 2 row-wise, */
                            /* 3 one row per SM streamed through a bulk-copy ring (K3c)       */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
     int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1); 1,2,4,8 (kernel 2: 1024/512/256/256 threads); */
                            /* kernel 3: 256 / 1024 consumer threads (default 512)              */
     int32_t stages;        /* 0 auto, else lag+2..8 shared-memory row stages per CTA (kernel 1); */
                            /* kernel 2: 4, 8 or 16 vectors in flight per thread; kernel 3:  */
-                           /* 16 KB ring slots, 2..13 (0 = 13)                              */
+                           /* ring slots (0 = as many as fit: 13 of 16 KB, 6 of 32 KB)       */
     int32_t lag;           /* 0 auto, else 1..2: rows between a row's reduction and its       */
                            /* backward, hiding the cluster exchange (kernel 1); kernel 3:    */
                            /* ring slots left free at the end of pass 1 (0 = 3)              */
     int32_t prefetch;      /* kernel 2: 1 = TMA-prefetch each CTA's next row into L2         */
     int32_t row_cache;     /* kernel 2: leading vectors per thread of each row kept in shared */
-                           /* memory for the second pass (0 auto = 160 KB per SM, -1 none) */
+                           /* memory for the second pass (0 auto = 160 KB per SM, -1 none); */
+                           /* kernel 3: CTAs per SM, 1 (default) or 2                        */
+    int32_t chunk_kb;      /* kernel 3: ring slot size in KB, 16 (default) or 32              */
 } grpo_tune_t;
 
 /*

@@ -50,7 +50,7 @@ class ValidateSummary(C.Structure):
 class Tune(C.Structure):
     _fields_ = [("kernel", C.c_int32), ("cluster_size", C.c_int32),
                 ("ctas_per_sm", C.c_int32), ("stages", C.c_int32), ("lag", C.c_int32),
-                ("prefetch", C.c_int32), ("row_cache", C.c_int32)]
+                ("prefetch", C.c_int32), ("row_cache", C.c_int32), ("chunk_kb", C.c_int32)]
 
 
 NORM_SEQ, NORM_TOKEN = 0, 1
@@ -261,7 +261,7 @@ def _tune(tune):
     if tune is None:
         return None
     return C.byref(Tune(*[int(tune.get(k, 0)) for k in ("kernel", "cluster_size", "ctas_per_sm",
-                                                       "stages", "lag", "prefetch", "row_cache")]))
+                                                       "stages", "lag", "prefetch", "row_cache", "chunk_kb")]))
 
 
 def grpo_async_loss_fwd_ex(logits, row_begin, n_rows, V, ld, target_ids, logp_behav, cu_seqlens,
@@ -293,7 +293,7 @@ def grpo_async_loss_fwd(logits, row_begin, n_rows, V, ld, target_ids, logp_behav
     tune_p = None
     if tune is not None:
         t = Tune(*[int(tune.get(k, 0)) for k in ("kernel", "cluster_size", "ctas_per_sm", "stages",
-                                                  "lag", "prefetch", "row_cache")])
+                                                  "lag", "prefetch", "row_cache", "chunk_kb")])
         tune_p = C.byref(t)
     for name, x in (("logits", logits), ("dlogits", dlogits)):
         if x is not None and x.element_size() != 2:

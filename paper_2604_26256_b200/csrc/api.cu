@@ -324,12 +324,24 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     const bool traced = n_rows > 0 && prof_on();
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
-    // kernel 0 (auto): the row-wise two-pass kernel (K3b) up to V ~ 176k, the streamed
-    // one-row-per-SM kernel (K3c) above, where K3b's L2 re-reads grow (DESIGN.md §8:
-    // V = 262144: K3c 0.90 vs K3b 0.79 of HBM; V = 152064: K3b 0.88 vs K3c 0.84).
+    // kernel 0 (auto): the row-wise two-pass kernel (K3b) below V = 90000, the streamed
+    // one-row-per-SM kernel (K3c, 32 KB ring slots) from there on (V = 152064
+    // K3c 0.94 vs K3b 0.88 of HBM; V = 50688 K3b 0.85 vs K3c 0.74).
     const bool untuned = !tune || (tune->ctas_per_sm == 0 && tune->stages == 0 && tune->lag == 0 &&
-                                   tune->row_cache == 0 && tune->cluster_size == 0);
-    const bool auto_stream = kernel == 0 && untuned && (V + 7) / 8 >= 22000;
+                                   tune->row_cache == 0 && tune->cluster_size == 0 &&
+                                   tune->chunk_kb == 0);
+    const int n_vec_row = (V + 7) / 8;
+    const bool auto_stream = kernel == 0 && untuned && n_vec_row >= 11250;
+    grpo_tune_t stream_tune{};
+    if (auto_stream) {
+        stream_tune.kernel = 3;
+        stream_tune.chunk_kb = 32;
+        stream_tune.stages = 6;
+        // free slots at the end of pass 1: 3, or 1 on very long rows (> 14 slots of
+        // 32 KB) where the re-read part of every SM's row would crowd L2
+        stream_tune.lag = (n_vec_row + 2047) / 2048 > 14 ? 1 : 3;
+        tune = &stream_tune;
+    }
     if ((kernel == 0 && !auto_stream) || kernel == 2) {
         e = grpo::launch_fused_rowwise(a, tune, s, &launches, &g_last_plan);
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");

@@ -27,8 +27,6 @@
 namespace grpo {
 namespace k3c {
 
-constexpr int CHUNK_BYTES = 16384;
-constexpr int CHUNK_VECS = CHUNK_BYTES / 16;  // 1024 8-element vectors
 
 struct Params {
     const uint16_t *logits;
@@ -52,6 +50,7 @@ struct Geometry {
     int tail_valid;  // valid elements of the last vector
 };
 
+template <int CHUNK_VECS>
 __device__ __forceinline__ Geometry geometry(const Params &p, bool two_pass) {
     Geometry g;
     g.n_vec = (p.V + 7) / 8;
@@ -62,8 +61,9 @@ __device__ __forceinline__ Geometry geometry(const Params &p, bool two_pass) {
     return g;
 }
 
-template <int NT, int MINB>
+template <int NT, int MINB, int CHUNK_VECS>
 __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
+    constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr int U = CHUNK_VECS / NT;  // vectors per consumer thread per chunk
     constexpr int NW = NT / 32;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
     __shared__ float2 red[NW];
     __shared__ float row_scalars[4];
     const bool two_pass = p.dlogits != nullptr;
-    const Geometry g = geometry(p, two_pass);
+    const Geometry g = geometry<CHUNK_VECS>(p, two_pass);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -280,33 +280,45 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
     p.term_ws = a.term_ws;
     p.logp_ws = a.logp_ws;
     p.flag_ws = a.flag_ws;
-    p.ns = (tune && tune->stages > 0) ? tune->stages : ((tune && tune->row_cache == 2) ? 6 : 13);
+    p.ns = (tune && tune->stages > 0) ? tune->stages : 0;
     p.pf = (tune && tune->lag > 0) ? tune->lag : 3;
-    // consumer threads (ctas_per_sm 256 / 512) and CTAs per SM (row_cache 1 / 2)
+    // consumer threads (ctas_per_sm 256 / 512), CTAs per SM (row_cache 1 / 2), slot size
     const int nt = (tune && tune->ctas_per_sm == 256) ? 256 : 512;
     const int cps = (tune && tune->row_cache == 2) ? 2 : 1;
-    if (p.ns < 2 || p.ns > (cps == 2 ? 6 : 13) || p.pf >= p.ns) {
+    const int ckb = (tune && (tune->chunk_kb == 32 || tune->chunk_kb == 64)) ? tune->chunk_kb : 16;
+    const int max_ns = (cps == 2 ? 96 : 208) / ckb;
+    if (!(tune && tune->stages > 0)) p.ns = max_ns;
+    if (p.ns < 2 || p.ns > max_ns || p.pf >= p.ns) {
         if (why) snprintf(why, why_len, "stream kernel: stages %d (2..%d), lag %d (< stages)", p.ns,
-                          cps == 2 ? 6 : 13, p.pf);
+                          max_ns, p.pf);
         return cudaErrorInvalidValue;
     }
-    const size_t smem = (size_t)p.ns * CHUNK_BYTES + 2 * (size_t)p.ns * 8;
+    const size_t smem = (size_t)p.ns * ckb * 1024 + 2 * (size_t)p.ns * 8;
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int grid = (int)std::min<int64_t>(a.n_rows, (int64_t)n_sm * cps);
     cudaError_t e;
-#define GRPO_K3C(NT_, MB_)                                                                              \
+#define GRPO_K3C(NT_, MB_, CV_)                                                                         \
     do {                                                                                               \
-        e = cudaFuncSetAttribute(stream_kernel<NT_, MB_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)smem);                                                           \
+        e = cudaFuncSetAttribute(stream_kernel<NT_, MB_, CV_>,                                         \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
         if (e != cudaSuccess) return e;                                                                \
-        stream_kernel<NT_, MB_><<<grid, NT_ + 32, smem, s>>>(p);                                       \
+        stream_kernel<NT_, MB_, CV_><<<grid, NT_ + 32, smem, s>>>(p);                                  \
     } while (0)
-    if (nt == 512 && cps == 1) GRPO_K3C(512, 1);
-    else if (nt == 512) GRPO_K3C(512, 2);
-    else if (cps == 1) GRPO_K3C(256, 1);
-    else GRPO_K3C(256, 2);
+    if (ckb == 64) {
+        GRPO_K3C(512, 1, 4096);
+    } else if (ckb == 32) {
+        if (nt == 512 && cps == 1) GRPO_K3C(512, 1, 2048);
+        else if (nt == 512) GRPO_K3C(512, 2, 2048);
+        else if (cps == 1) GRPO_K3C(256, 1, 2048);
+        else GRPO_K3C(256, 2, 2048);
+    } else {
+        if (nt == 512 && cps == 1) GRPO_K3C(512, 1, 1024);
+        else if (nt == 512) GRPO_K3C(512, 2, 1024);
+        else if (cps == 1) GRPO_K3C(256, 1, 1024);
+        else GRPO_K3C(256, 2, 1024);
+    }
 #undef GRPO_K3C
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

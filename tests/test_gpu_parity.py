@@ -11,9 +11,11 @@ from tests.gpu_util import compare, run_gpu, run_oracle, to_dev_bits
 pytestmark = pytest.mark.gpu
 
 KERNELS = [{"kernel": 1}, {"kernel": 2}, {"kernel": 3}]
-STREAM_PLANS = [{"kernel": 3, "stages": st, "lag": lg, "ctas_per_sm": nt}
-                for st, lg, nt in ((13, 3, 0), (13, 1, 0), (13, 12, 0), (2, 1, 0), (5, 2, 0),
-                                   (8, 3, 256), (13, 3, 256))]
+STREAM_PLANS = [{"kernel": 3, "stages": st, "lag": lg, "ctas_per_sm": nt, "chunk_kb": kb}
+                for st, lg, nt, kb in ((13, 3, 0, 16), (13, 1, 0, 16), (13, 12, 0, 16), (2, 1, 0, 16),
+                                       (5, 2, 0, 16), (8, 3, 256, 16), (13, 3, 256, 16),
+                                       (6, 3, 0, 32), (6, 1, 0, 32), (2, 1, 0, 32), (6, 5, 0, 32),
+                                       (3, 1, 256, 32))]
 ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u, "row_cache": rc, "cluster_size": cl}
                  for c, u, rc, cl in ((1, 4, -1, 1), (1, 2, 0, 1), (1, 8, 1, 1), (2, 4, -1, 1),
                                       (2, 4, 0, 1), (2, 8, 1, 1), (2, 8, 0, 1), (2, 2, 0, 1),
@@ -254,7 +256,8 @@ def test_sharded_equals_unsharded(dev, R):
 
 
 @pytest.mark.parametrize("plan", STREAM_PLANS,
-                         ids=lambda d: f"ns{d['stages']}pf{d['lag']}nt{d['ctas_per_sm'] or 512}")
+                         ids=lambda d: f"ns{d['stages']}pf{d['lag']}nt{d['ctas_per_sm'] or 512}"
+                                       f"kb{d['chunk_kb']}")
 def test_stream_plans(dev, plan):
     """K3c (one row per SM through the bulk-copy ring) for ring sizes from 2 slots (every
     chunk but one re-loaded) to 13 (rows shorter than the ring: several rows resident),
