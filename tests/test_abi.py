@@ -94,3 +94,56 @@ def test_package_has_no_cpu_fallback():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "oracle" not in src.replace("oracle/", "").lower() or fn == "build.py", fn
+
+
+def test_host_side_errors_new_entry_points():
+    """NEXT(2) / NEXT(3) / K3c entry points: documented status codes on bad arguments,
+    returned by the host checks before any CUDA call."""
+    import paper_2604_26256_b200._lib as L
+    lib = L.LIB
+    fake = C.c_void_p(16)
+    ws = lib.grpo_async_lmhead_workspace_size(100, 1000, 4)
+    assert ws >= lib.grpo_async_workspace_size(100, 1000, 4)
+    opts = L.LossOpts(0.2, 0.2, 0, None, 0)
+    # LM head: d not a multiple of 64, misaligned W, workspace too small, NULL opts
+    st = lib.grpo_async_lmhead_fwd(fake, fake, 0, 10, 96, 1000, fake, fake, fake, 4, None, fake,
+                                   fake, C.byref(opts), 1.0, None, None, None, fake, fake, fake, ws,
+                                   None)
+    assert st == L.GRPO_ERR_INVALID_ARG and b"multiple of 64" in lib.grpo_last_error()
+    st = lib.grpo_async_lmhead_fwd(fake, C.c_void_p(18), 0, 10, 128, 1000, fake, fake, fake, 4, None,
+                                   fake, fake, C.byref(opts), 1.0, None, None, None, fake, fake, fake,
+                                   ws, None)
+    assert st == L.GRPO_ERR_ALIGNMENT
+    st = lib.grpo_async_lmhead_fwd(fake, fake, 0, 10, 128, 1000, fake, fake, fake, 4, None, fake,
+                                   fake, C.byref(opts), 1.0, None, None, None, fake, fake, fake, 8,
+                                   None)
+    assert st == L.GRPO_ERR_WORKSPACE
+    st = lib.grpo_async_lmhead_fwd(fake, fake, 0, 10, 128, 1000, fake, fake, fake, 4, None, fake,
+                                   fake, None, 1.0, None, None, None, fake, fake, fake, ws, None)
+    assert st == L.GRPO_ERR_INVALID_ARG
+    # LM-head backward: ld_dz < V; logits: ld_out not a multiple of 8
+    st = lib.grpo_async_lmhead_bwd(fake, fake, 10, 128, 1000, fake, fake, fake, 1.0, fake, 999,
+                                   None, None, None)
+    assert st == L.GRPO_ERR_ALIGNMENT
+    st = lib.grpo_async_lmhead_logits(fake, fake, 10, 128, 1000, fake, 1004, None)
+    assert st == L.GRPO_ERR_ALIGNMENT
+    # vocabulary-parallel: world > 8, shard_cols % 8, shards that do not cover V, slots < n_rows
+    c = L.VpComm()
+    c.world, c.rank_begin, c.n_local, c.shard_cols, c.slots = 9, 0, 1, 128, 100
+    vws = lib.grpo_async_workspace_size(10, 1000, 4)
+    args = lambda: (C.byref(c), 0, 10, 1000, 1024, fake, fake, fake, 4, None, fake, fake,
+                    C.byref(opts), 1.0, None, None, None, fake, fake, fake, vws, None)
+    assert lib.grpo_async_loss_fwd_vp(*args()) == L.GRPO_ERR_INVALID_ARG
+    c.world, c.shard_cols = 2, 500
+    assert lib.grpo_async_loss_fwd_vp(*args()) == L.GRPO_ERR_INVALID_ARG
+    c.shard_cols = 256
+    assert lib.grpo_async_loss_fwd_vp(*args()) == L.GRPO_ERR_INVALID_ARG   # 2 * 256 < V
+    c.shard_cols, c.slots = 504, 5
+    assert lib.grpo_async_loss_fwd_vp(*args()) == L.GRPO_ERR_INVALID_ARG   # slots < n_rows
+    # tune: kernel out of range
+    t = L.Tune(4, 0, 0, 0, 0, 0, 0, 0)
+    ws2 = lib.grpo_async_workspace_size(10, 1000, 4)
+    st = lib.grpo_async_loss_fwd(fake, 0, 10, 1000, 1000, fake, fake, fake, 4, None, fake, fake,
+                                 0.2, 1.0, None, None, None, fake, fake, None, fake, ws2,
+                                 C.byref(t), None)
+    assert st == L.GRPO_ERR_INVALID_ARG
