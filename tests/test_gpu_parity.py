@@ -270,3 +270,17 @@ def test_stream_plans(dev, plan):
     ref = run_oracle(b, bits, want_dlogits=False)
     gpu = run_gpu(b, bits, dev, tune=plan, want_dlogits=False)
     compare(gpu, ref, b, check_dlogits=False)
+
+
+@pytest.mark.parametrize("V", [2, 7, 8, 9, 100, 16391, 32776, 90007])
+def test_odd_vocabulary_sizes(dev, V):
+    """Small and ragged vocabularies (V % 8 != 0; one vector past a 16 KB / 32 KB ring slot;
+    the K3b/K3c switch point) for the row-wise and both ring geometries."""
+    rng = np.random.default_rng(V)
+    rows = [(rng.normal(size=V) * 2, int(rng.integers(0, V))) for _ in range(12)]
+    b, bits = _adversarial_batch(V, rows)
+    ref = run_oracle(b, bits)
+    for tune in ({"kernel": 2}, {"kernel": 3}, {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 3},
+                 {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 1}, None):
+        gpu = run_gpu(b, bits, dev, tune=tune)
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
