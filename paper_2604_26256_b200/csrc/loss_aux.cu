@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
         // ---- pass 2: dlogits = s (softmax - onehot), written once
         if (p.dlogits) {
             const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
+            const auto gref = B::grad_ref(sc, lse2);
             const int32_t y = __float_as_int(row_scalars[3]);
             const int y_loc = y >= 0 ? y - vec_lo * 8 : -1;
             const int yv = (y_loc >= 0 && y_loc < n_vec * 8) ? (y_loc >> 3) : -1;
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                             x[j] = (bi * U + j < cache_vecs) ? row_cache[(bi * U + j) * NT + threadIdx.x]
                                                              : ldg_policy(src + j * NT, pol_stream);
 #pragma unroll
-                        for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad(x[j], sc, lse2));
+                        for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad_scaled(x[j], gref));
                     } else {
 #pragma unroll
                         for (int j = 0; j < U; ++j) {
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                         for (int j = 0; j < U; ++j) {
                             const int vi = v0 + j * NT;
                             if (vi >= n_vec) break;
-                            const uint4 d = B::grad(x[j], sc, lse2);
+                            const uint4 d = B::grad_scaled(x[j], gref);
                             if (vi == tail_vi) store_tail(drow + (int64_t)vi * 8, d, tail_valid);
                             else stg_stream(dst4 + vi, d);
                         }

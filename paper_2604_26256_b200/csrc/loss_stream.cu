@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
         if (!two_pass) continue;
         // ---- pass 2: resident chunks n-R..n-1 (loads base+n-R..), then the re-loads
         const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
+            const auto gref = RowwiseBatch<NT, U>::grad_ref(sc, lse2);
         const int32_t y = __float_as_int(row_scalars[3]);
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
         uint16_t *drow = p.dlogits + row * p.ld;
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
 #pragma unroll
-                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad(x[j], sc, lse2));
+                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gref));
                 }
             } else {
 #pragma unroll
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
                     const int vi = v0 + j * NT;
                     if (vi >= g.n_vec) break;
                     const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
-                                               : RowwiseBatch<NT, U>::grad(chunk[j * NT + threadIdx.x], sc, lse2);
+                                               : RowwiseBatch<NT, U>::grad_scaled(chunk[j * NT + threadIdx.x], gref);
                     if (vi == g.n_vec - 1 && g.tail_valid < 8) store_tail(drow + (int64_t)vi * 8, d, g.tail_valid);
                     else stg_stream(dst4 + vi, d);
                 }

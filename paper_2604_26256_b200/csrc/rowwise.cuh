@@ -27,6 +27,24 @@ struct RowwiseBatch {
         }
         lse2_merge(a, s, va, (t0 + t1) + (t2 + t3));
     }
+    // s * 2^(z*log2e - lse2) = sign(s) * 2^(z*log2e - (lse2 - log2|s|)): the token scale
+    // folds into the exponent's reference, so an element costs one FFMA and one EX2 (no
+    // FMUL) and the sign is applied to the packed bf16 pair
+    struct GradRef {
+        float ref;
+        uint32_t sign;
+    };
+    static __device__ __forceinline__ GradRef grad_ref(float sc, float lse2) {
+        return GradRef{lse2 - log2f(fabsf(sc)), sc < 0.0f ? 0x80008000u : 0u};
+    }
+    static __device__ __forceinline__ uint4 grad_scaled(const uint4 &x, const GradRef &g) {
+        uint4 d;
+        d.x = pack_bf16x2(ex2(fmaf(bf_lo(x.x), kLog2e, -g.ref)), ex2(fmaf(bf_hi(x.x), kLog2e, -g.ref))) ^ g.sign;
+        d.y = pack_bf16x2(ex2(fmaf(bf_lo(x.y), kLog2e, -g.ref)), ex2(fmaf(bf_hi(x.y), kLog2e, -g.ref))) ^ g.sign;
+        d.z = pack_bf16x2(ex2(fmaf(bf_lo(x.z), kLog2e, -g.ref)), ex2(fmaf(bf_hi(x.z), kLog2e, -g.ref))) ^ g.sign;
+        d.w = pack_bf16x2(ex2(fmaf(bf_lo(x.w), kLog2e, -g.ref)), ex2(fmaf(bf_hi(x.w), kLog2e, -g.ref))) ^ g.sign;
+        return d;
+    }
     // s * 2^(z*log2e - lse2) for the 8 elements of one vector, packed to bf16
     static __device__ __forceinline__ uint4 grad(const uint4 &x, float sc, float lse2) {
         uint4 d;

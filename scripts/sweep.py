@@ -38,23 +38,37 @@ plans = [json.loads(p) for p in args.plans.split(";")] if args.plans else [
     {"kernel": 1, "cluster_size": 16, "stages": 2}, {"kernel": 1, "cluster_size": 16, "ctas_per_sm": 3},
 ]
 bytes_row = 4 * V + 25 if not args.fwd_only else 2 * V + 25
-for plan in plans:
+def run_once(plan):
     loss.tune = plan
-    try:
-        times = []
-        for r in range(args.reps + 1 if args.reps > 0 else 1):
-            G.grpo_profile_enable(True); G.grpo_profile_collect()
-            loss.loss_chunk(lg, 0, R, db.target_ids[:R], db.logp_behav[:R], db.cu_seqlens, adv, inv, ts, st,
-                            dlogits=None if args.fwd_only else dl, V=V)
-            torch.cuda.synchronize()
-            n, ms = G.grpo_profile_collect()
+    G.grpo_profile_enable(True); G.grpo_profile_collect()
+    loss.loss_chunk(lg, 0, R, db.target_ids[:R], db.logp_behav[:R], db.cu_seqlens, adv, inv, ts, st,
+                    dlogits=None if args.fwd_only else dl, V=V)
+    torch.cuda.synchronize()
+    n, ms = G.grpo_profile_collect()
+    return ms, G.grpo_async_last_plan()
+
+
+times = {i: [] for i in range(len(plans))}
+plans_used, errors = {}, {}
+n_rounds = args.reps + 1 if args.reps > 0 else 1
+# plans interleaved round by round, so slow drifts (power cap, clocks) hit every plan alike
+for r in range(n_rounds):
+    for i, plan in enumerate(plans):
+        if i in errors:
+            continue
+        try:
+            ms, pl = run_once(plan)
+            plans_used[i] = pl
             if r > 0 or args.reps == 0:
-                times.append(ms)
-        pl = G.grpo_async_last_plan()
-        ms = float(np.median(times))
-        print(json.dumps({"tune": plan, "plan": pl, "ms": round(ms, 3),
-                          "GBps": round(bytes_row * R / ms / 1e6, 1),
-                          "frac": round(bytes_row * R / ms / 1e6 / 6546.6, 3)}), flush=True)
-    except Exception as e:
-        print(json.dumps({"tune": plan, "error": str(e)}), flush=True)
+                times[i].append(ms)
+        except Exception as e:
+            errors[i] = str(e)
+for i, plan in enumerate(plans):
+    if i in errors:
+        print(json.dumps({"tune": plan, "error": errors[i]}), flush=True)
+        continue
+    ms = float(np.median(times[i]))
+    print(json.dumps({"tune": plan, "plan": plans_used[i], "ms": round(ms, 3),
+                      "GBps": round(bytes_row * R / ms / 1e6, 1),
+                      "frac": round(bytes_row * R / ms / 1e6 / 6546.6, 3)}), flush=True)
 G.grpo_profile_enable(False)
