@@ -339,6 +339,12 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
  */
 size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N);
 
+/* Tensor-core mode of the calling thread's later LM-head calls: 1 = one CTA per MMA
+ * (tcgen05.mma.cta_group::1, 128 x 256 tiles), 2 = CTA pairs on one TPC (cta_group::2,
+ * 256 x 256 tiles, each CTA stages half of the W tile; the default).  Same results.
+ * Errors: GRPO_ERR_INVALID_ARG for other values. */
+grpo_status_t grpo_async_lmhead_set_cta_group(int32_t cta_group);
+
 grpo_status_t grpo_async_lmhead_fwd(const uint16_t *hidden, const uint16_t *W, int64_t row_begin,
                                     int64_t n_rows, int32_t d, int32_t V,
                                     const int64_t *target_ids, const float *logp_behav,

@@ -34,7 +34,7 @@ EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advan
             "grpo_async_advantage_ex", "grpo_async_loss_fwd", "grpo_async_loss_fwd_ex",
             "grpo_async_loss_fwd_vp", "grpo_async_loss_bwd", "grpo_async_workspace_size",
             "grpo_async_lmhead_workspace_size", "grpo_async_lmhead_fwd", "grpo_async_lmhead_bwd",
-            "grpo_async_lmhead_logits",
+            "grpo_async_lmhead_logits", "grpo_async_lmhead_set_cta_group",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -121,6 +121,8 @@ def _load():
     lib.grpo_async_lmhead_bwd.restype = st
     lib.grpo_async_lmhead_logits.argtypes = [P, P, i64, i32, i32, P, i64, P]
     lib.grpo_async_lmhead_logits.restype = st
+    lib.grpo_async_lmhead_set_cta_group.argtypes = [i32]
+    lib.grpo_async_lmhead_set_cta_group.restype = st
     lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
     lib.grpo_async_loss_bwd.restype = st
     lib.grpo_async_workspace_size.argtypes = [i64, i32, i32]
@@ -404,3 +406,7 @@ def grpo_async_lmhead_bwd(hidden, W, n_rows, d, V, target_ids, lse, token_scale,
 def grpo_async_lmhead_logits(hidden, W, n_rows, d, V, out, ld_out, stream=None):
     _check(LIB.grpo_async_lmhead_logits(_bf16(hidden, "hidden"), _bf16(W, "W"), n_rows, d, V,
                                         _bf16(out, "out"), ld_out, _stream(stream)))
+
+
+def grpo_async_lmhead_set_cta_group(cta_group: int) -> None:
+    _check(LIB.grpo_async_lmhead_set_cta_group(int(cta_group)))

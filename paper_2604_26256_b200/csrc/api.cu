@@ -489,6 +489,8 @@ grpo_status_t lm_check(const char *fn, const uint16_t *hidden, const uint16_t *W
     return GRPO_OK;
 }
 
+thread_local int g_lm_cta_group = 2;
+
 cublasHandle_t cublas_handle() {
     static thread_local cublasHandle_t h = nullptr;
     static thread_local int h_dev = -1;
@@ -504,6 +506,13 @@ cublasHandle_t cublas_handle() {
 }  // namespace
 
 extern "C" {
+
+grpo_status_t grpo_async_lmhead_set_cta_group(int32_t cta_group) {
+    if (cta_group != 1 && cta_group != 2)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_set_cta_group: %d (1 or 2)", cta_group);
+    g_lm_cta_group = cta_group;
+    return ok(0);
+}
 
 size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N) {
     if (n_rows < 0) n_rows = 0;
@@ -580,7 +589,7 @@ grpo_status_t grpo_async_lmhead_fwd(const uint16_t *hidden, const uint16_t *W, i
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "lmhead_fwd/profile");
     e = grpo::launch_lmhead(0, hidden, W, n_rows, d, V, a.rowinfo, part, zy, nullptr, 0, nullptr, nullptr,
-                            nullptr, 1.0f, s, &launches, &g_last_plan, why, sizeof why);
+                            nullptr, 1.0f, s, &launches, &g_last_plan, why, sizeof why, g_lm_cta_group);
     if (e != cudaSuccess) return cuda_fail(e, "lmhead_fwd/tcgen05", why);
     if (traced && (e = prof_end(s, ev)) != cudaSuccess) return cuda_fail(e, "lmhead_fwd/profile");
     e = grpo::launch_lmhead_combine(part, zy, n_split, a, s, &launches);
@@ -608,7 +617,7 @@ grpo_status_t grpo_async_lmhead_bwd(const uint16_t *hidden, const uint16_t *W, i
     char why[256] = {0};
     cudaError_t e = grpo::launch_lmhead(1, hidden, W, n_rows, d, V, nullptr, nullptr, nullptr, dz, ld_dz,
                                         target_ids, lse, token_scale, grad_scale_mult, s, &launches,
-                                        &g_last_plan, why, sizeof why);
+                                        &g_last_plan, why, sizeof why, g_lm_cta_group);
     if (e != cudaSuccess) return cuda_fail(e, "lmhead_bwd/tcgen05", why);
     if (dhidden || dW) {
         cublasHandle_t h = cublas_handle();
@@ -645,7 +654,7 @@ grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W
     char why[256] = {0};
     cudaError_t e = grpo::launch_lmhead(2, hidden, W, n_rows, d, V, nullptr, nullptr, nullptr, out, ld_out,
                                         nullptr, nullptr, nullptr, 1.0f, (cudaStream_t)stream, &launches,
-                                        &g_last_plan, why, sizeof why);
+                                        &g_last_plan, why, sizeof why, g_lm_cta_group);
     if (e != cudaSuccess) return cuda_fail(e, "lmhead_logits/tcgen05", why);
     return ok(launches);
 }

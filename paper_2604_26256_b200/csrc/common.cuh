@@ -399,7 +399,8 @@ int32_t lmhead_n_split(int64_t n_rows, int32_t V);
 cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows, int32_t d, int32_t V,
                           const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,
                           const int64_t *targets, const float *lse, const float *scale, float mult,
-                          cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len);
+                          cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len,
+                          int cta_group);
 cudaError_t launch_lmhead_combine(const float2 *part, const float *zy, int32_t n_split, const LossArgs &a,
                                   cudaStream_t s, int *launches);
 cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned long long *row_ctr,

@@ -62,37 +62,57 @@ __device__ __forceinline__ void decode(const Params &p, int unit, int &m_tile, i
     m_tile = grp * GROUP_M + (rem - split * gm);
 }
 
-template <int EPI>
+// CG = CTAs per MMA: 1 (one SM, M = 128 per tile) or 2 (a CTA pair on one TPC issuing
+// tcgen05.mma.cta_group::2, M = 256: each CTA stages its own 128 rows of X and half of the
+// 256 vocabulary rows of W, so a pair moves 2 x 32 KB per k-block instead of 2 x 48 KB).
+template <int CG>
+struct Geo {
+    static constexpr int B_ROWS = BN / CG;                 // W rows staged per CTA
+    static constexpr int B_BYTES_CG = B_ROWS * BK * 2;
+    static constexpr int STAGE = A_BYTES + B_BYTES_CG;
+    static constexpr int NSTAGE = CG == 1 ? STAGES : 6;
+    static constexpr int SMEM = NSTAGE * STAGE + 1024 + 256;
+};
+
+template <int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     lmhead_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                   const Params p) {
+    using GG = Geo<CG>;
+    constexpr int NS = GG::NSTAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sA = smem;                             // STAGES x A_BYTES
-    uint8_t *sB = smem + STAGES * A_BYTES;          // STAGES x B_BYTES
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
-    uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES,
-             *tempty = bars + 2 * STAGES + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+    uint8_t *sA = smem;                             // NS x A_BYTES
+    uint8_t *sB = smem + NS * A_BYTES;              // NS x B_BYTES_CG
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * GG::STAGE);
+    uint64_t *full = bars, *empty = bars + NS, *tfull = bars + 2 * NS, *tempty = bars + 2 * NS + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = p.d / BK;
+    const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;        // 0 = the pair's leader
+    const int cta_id = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
+    const int n_ctas = CG == 2 ? (int)ncluster_x() : (int)gridDim.x;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128);
+            mbar_init(tempty + a, 128 * CG);  // every epilogue thread of the pair
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tc::prefetch_tmap(&tmX);
         tc::prefetch_tmap(&tmW);
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 1) {
+        if (CG == 2) tc::tmem_alloc2(tmem_slot, TMEM_COLS);
+        else tc::tmem_alloc(tmem_slot, TMEM_COLS);
+    }
     tc::fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync_all();  // the peer's barriers are initialised before use
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -102,17 +122,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
                 int m_tile, split;
                 decode(p, unit, m_tile, split);
                 const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
+                const int a_row = m_tile * (BM * CG) + (int)crank * BM;
                 for (int vt = vt0; vt < vt1; ++vt)
                     for (int kb = 0; kb < nk; ++kb) {
                         mbar_wait(empty + stage, phase ^ 1u);
-                        mbar_arrive_expect_tx(full + stage, STAGE_BYTES);
-                        tc::tma_load_2d(sA + stage * A_BYTES, &tmX, kb * BK, m_tile * BM, full + stage, pol_a);
-                        tc::tma_load_2d(sB + stage * B_BYTES, &tmW, kb * BK, vt * BN, full + stage, pol_b);
-                        if (++stage == STAGES) {
+                        const int b_row = vt * BN + (int)crank * GG::B_ROWS;
+                        if (CG == 1) {
+                            mbar_arrive_expect_tx(full + stage, GG::STAGE);
+                            tc::tma_load_2d(sA + stage * A_BYTES, &tmX, kb * BK, a_row, full + stage, pol_a);
+                            tc::tma_load_2d(sB + stage * GG::B_BYTES_CG, &tmW, kb * BK, b_row, full + stage, pol_b);
+                        } else {
+                            // the leader's full barrier counts both CTAs' bytes
+                            if (crank == 0) mbar_arrive_expect_tx(full + stage, 2 * GG::STAGE);
+                            tc::tma_load_2d_pair(sA + stage * A_BYTES, &tmX, kb * BK, a_row, full + stage, pol_a);
+                            tc::tma_load_2d_pair(sB + stage * GG::B_BYTES_CG, &tmW, kb * BK, b_row, full + stage,
+                                                 pol_b);
+                        }
+                        if (++stage == NS) {
                             stage = 0;
                             phase ^= 1u;
                         }
@@ -121,11 +151,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
+        if (lane == 0 && crank == 0) {  // one thread of the pair's leader issues every MMA
+            constexpr uint32_t idesc = tc::idesc_bf16_f32(BM * CG, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
                 int m_tile, split;
                 decode(p, unit, m_tile, split);
                 const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
@@ -137,17 +167,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         mbar_wait(full + stage, phase);
                         tc::fence_after();
                         const uint64_t ad = tc::desc_k_sw128(sA + stage * A_BYTES);
-                        const uint64_t bd = tc::desc_k_sw128(sB + stage * B_BYTES);
+                        const uint64_t bd = tc::desc_k_sw128(sB + stage * GG::B_BYTES_CG);
 #pragma unroll
-                        for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the swizzle atom
-                            tc::mma_bf16(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
-                        tc::commit(empty + stage);
-                        if (++stage == STAGES) {
+                        for (int k = 0; k < BK / 16; ++k) {  // +32 B along K inside the swizzle atom
+                            if (CG == 1) tc::mma_bf16(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                            else tc::mma2_bf16(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (kb | k) != 0);
+                        }
+                        if (CG == 1) tc::commit(empty + stage);
+                        else tc::commit2_multicast(empty + stage, 0x3);  // frees the stage in both CTAs
+                        if (++stage == NS) {
                             stage = 0;
                             phase ^= 1u;
                         }
                     }
-                    tc::commit(tfull + acc);
+                    if (CG == 1) tc::commit(tfull + acc);
+                    else tc::commit2_multicast(tfull + acc, 0x3);
                     acc ^= 1;
                     if (acc == 0) acc_phase ^= 1u;
                 }
@@ -159,11 +193,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int r_in_tile = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+        for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
             int m_tile, split;
             decode(p, unit, m_tile, split);
             const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
-            const int row = m_tile * BM + r_in_tile;
+            const int row = m_tile * (BM * CG) + (int)crank * BM + r_in_tile;
             const bool valid = row < p.n_rows;
             int32_t y = -1;
             float lse2 = 0.0f, sc = 0.0f;
@@ -244,7 +278,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
                 tc::fence_before();
-                mbar_arrive(tempty + acc);
+                if (CG == 1) mbar_arrive(tempty + acc);
+                else tc::mbar_arrive_remote(tempty + acc, 0);  // the leader's MMA waits on it
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1u;
             }
@@ -256,7 +291,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2) cluster_sync_all();  // the peer's epilogue is done with the pair's TMEM
+    if (warp == 1) {
+        if (CG == 2) tc::tmem_dealloc2(tmem_base, TMEM_COLS);
+        else tc::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
 }
 
 // per row: merge the n_split partials in split order (deterministic), then the
@@ -328,11 +367,13 @@ int32_t lmhead_n_split(int64_t n_rows, int32_t V) {
 cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows, int32_t d, int32_t V,
                           const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,
                           const int64_t *targets, const float *lse, const float *scale, float mult,
-                          cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len) {
+                          cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len,
+                          int cta_group) {
     using namespace lm;
     if (n_rows == 0) return cudaSuccess;
+    const int CG = cta_group == 1 ? 1 : 2;
     CUtensorMap mx, mw;
-    if (!make_map(&mx, X, n_rows, d, BM) || !make_map(&mw, W, V, d, BN)) {
+    if (!make_map(&mx, X, n_rows, d, BM) || !make_map(&mw, W, V, d, BN / CG)) {
         if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
         return cudaErrorInvalidValue;
     }
@@ -340,7 +381,7 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     p.n_rows = (int32_t)n_rows;
     p.V = V;
     p.d = d;
-    p.m_tiles = (int32_t)((n_rows + BM - 1) / BM);
+    p.m_tiles = (int32_t)((n_rows + BM * CG - 1) / (BM * CG));
     p.n_vt = (V + BN - 1) / BN;
     p.vt_per_unit = lmhead_vt_per_unit(n_rows);
     const int32_t n_split = (p.n_vt + p.vt_per_unit - 1) / p.vt_per_unit;
@@ -357,30 +398,49 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(p.n_units, n_sm);
+    const int groups = std::min(p.n_units, n_sm / CG);  // persistent: one CTA (pair) per SM (pair)
     cudaError_t e;
-#define GRPO_LM_LAUNCH(E)                                                                               \
-    do {                                                                                                \
-        e = cudaFuncSetAttribute(lmhead_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); \
-        if (e != cudaSuccess) return e;                                                                 \
-        lmhead_kernel<E><<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mx, mw, p);                             \
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(groups * CG));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#define GRPO_LM_LAUNCH(E, CG_)                                                                         \
+    do {                                                                                               \
+        cfg.dynamicSmemBytes = Geo<CG_>::SMEM;                                                         \
+        e = cudaFuncSetAttribute(lmhead_kernel<E, CG_>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                 Geo<CG_>::SMEM);                                                      \
+        if (e != cudaSuccess) return e;                                                                \
+        e = cudaLaunchKernelEx(&cfg, lmhead_kernel<E, CG_>, mx, mw, p);                                \
     } while (0)
-    if (epi == EPI_STATS) GRPO_LM_LAUNCH(EPI_STATS);
-    else if (epi == EPI_DZ) GRPO_LM_LAUNCH(EPI_DZ);
-    else GRPO_LM_LAUNCH(EPI_LOGITS);
+    if (CG == 1) {
+        if (epi == EPI_STATS) GRPO_LM_LAUNCH(EPI_STATS, 1);
+        else if (epi == EPI_DZ) GRPO_LM_LAUNCH(EPI_DZ, 1);
+        else GRPO_LM_LAUNCH(EPI_LOGITS, 1);
+    } else {
+        if (epi == EPI_STATS) GRPO_LM_LAUNCH(EPI_STATS, 2);
+        else if (epi == EPI_DZ) GRPO_LM_LAUNCH(EPI_DZ, 2);
+        else GRPO_LM_LAUNCH(EPI_LOGITS, 2);
+    }
 #undef GRPO_LM_LAUNCH
-    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     *launches += 1;
     if (plan) {
         *plan = grpo_plan_t{};
         plan->kernel = 4 + epi;
-        plan->grid = grid;
+        plan->cluster_size = CG;
+        plan->grid = groups * CG;
         plan->ctas_per_sm = 1;
-        plan->stages = STAGES;
+        plan->stages = CG == 1 ? Geo<1>::NSTAGE : Geo<2>::NSTAGE;
         plan->vec_per_thread = p.vt_per_unit;
         plan->max_clusters = p.n_units;
-        plan->smem_bytes = SMEM_BYTES;
+        plan->smem_bytes = CG == 1 ? Geo<1>::SMEM : Geo<2>::SMEM;
     }
     return cudaSuccess;
 }

@@ -286,7 +286,8 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
     // consumer threads (ctas_per_sm 256 / 512), CTAs per SM (row_cache 1 / 2), slot size
     const int nt = (tune && tune->ctas_per_sm == 256) ? 256 : 512;
     const int cps = (tune && tune->row_cache == 2) ? 2 : 1;
-    const int ckb = (tune && (tune->chunk_kb == 32 || tune->chunk_kb == 64)) ? tune->chunk_kb : 16;
+    const int ckb = (tune && (tune->chunk_kb == 24 || tune->chunk_kb == 32 || tune->chunk_kb == 48 ||
+                              tune->chunk_kb == 64)) ? tune->chunk_kb : 16;
     const int max_ns = (cps == 2 ? 96 : 208) / ckb;
     if (!(tune && tune->stages > 0)) p.ns = max_ns;
     if (p.ns < 2 || p.ns > max_ns || p.pf >= p.ns) {
@@ -309,6 +310,10 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
     } while (0)
     if (ckb == 64) {
         GRPO_K3C(512, 1, 4096);
+    } else if (ckb == 48) {
+        GRPO_K3C(512, 1, 3072);
+    } else if (ckb == 24) {
+        GRPO_K3C(512, 1, 1536);
     } else if (ckb == 32) {
         if (nt == 512 && cps == 1) GRPO_K3C(512, 1, 2048);
         else if (nt == 512) GRPO_K3C(512, 2, 2048);

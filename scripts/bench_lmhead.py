@@ -36,7 +36,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--skip-unfused", action="store_true")
+    ap.add_argument("--cta-group", type=int, default=2, help="1 or 2 (tcgen05 cta_group::2 pairs)")
     args = ap.parse_args()
+    L.grpo_async_lmhead_set_cta_group(args.cta_group)
     dev = torch.device("cuda", 0)
     b = make_batch("prod", 0, period=args.rows)
     R, V, d = min(args.rows, b.T), b.V, args.d
@@ -105,6 +107,7 @@ def main():
     ms_bwd = timed(bwd)
     fl = 2.0 * R * V * d
     out = {"workload": f"lmhead prod chunk R={R} d={d} V={V}", "rows": R, "d": d, "V": V,
+           "cta_group": args.cta_group,
            "ms_fwd": ms_fwd, "ms_fwd_tcgen05_kernel": ms_fwd_kernel, "ms_bwd": ms_bwd,
            "fwd_tflops": fl / ms_fwd / 1e9, "fwd_kernel_tflops": fl / ms_fwd_kernel / 1e9,
            "bwd_tflops": 3 * fl / ms_bwd / 1e9, "plan_fwd": plan_fwd,

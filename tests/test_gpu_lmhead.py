@@ -35,7 +35,7 @@ def _check(gpu, ref, b, eps_hi=None):
 
 @pytest.mark.parametrize("d", [64, 256])
 @pytest.mark.parametrize("name", ["tiny", "ragged", "mid32k"])
-def test_lmhead_parity(dev, name, d):
+def test_lmhead_parity(dev, name, d, cta_group):
     b, X, W = lmhead_batch(name, 3, d)
     ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
     gpu = run_gpu_lmhead(b, X, W, dev)
@@ -43,7 +43,7 @@ def test_lmhead_parity(dev, name, d):
     print(name, d, errs)
 
 
-def test_lmhead_parity_152k_chunked(dev):
+def test_lmhead_parity_152k_chunked(dev, cta_group):
     """The metric's vocabulary (V = 152064, 594 tiles of 256) with row chunks that are not
     multiples of the 128-row tile."""
     b, X, W = lmhead_batch("mid152k", 4, 128)
@@ -61,8 +61,16 @@ def test_lmhead_dapo_options(dev):
     _check(gpu, ref, b, eps_hi=0.28)
 
 
-@pytest.mark.parametrize("shape", [(1, 64, 1), (127, 64, 255), (129, 128, 257), (300, 192, 1000)])
-def test_lmhead_logits_gemm(dev, shape):
+@pytest.fixture(params=[1, 2], ids=["cg1", "cg2"])
+def cta_group(request):
+    L.grpo_async_lmhead_set_cta_group(request.param)
+    yield request.param
+    L.grpo_async_lmhead_set_cta_group(2)
+
+
+@pytest.mark.parametrize("shape", [(1, 64, 1), (127, 64, 255), (129, 128, 257), (300, 192, 1000),
+                                   (513, 256, 4099)])
+def test_lmhead_logits_gemm(dev, shape, cta_group):
     """The tcgen05 GEMM alone (ragged n, V; minimum d) against the fp64 product: every
     logit within half a bf16 ulp plus the fp32 accumulation bound d * 2^-23 * sum|x w|."""
     n, d, V = shape
