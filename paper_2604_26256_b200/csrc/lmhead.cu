@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tc.cuh"
@@ -34,7 +35,7 @@ enum { EPI_STATS = 0, EPI_DZ = 1, EPI_LOGITS = 2 };
 
 struct Params {
     int32_t n_rows, V, d;
-    int32_t m_tiles, n_vt, vt_per_unit, n_units;
+    int32_t m_tiles, n_vt, vt_per_unit, n_units, group_m;
     // EPI_STATS
     const RowInfo *rowinfo;
     float2 *part;  // [n_split][n_rows] log2-domain (max, sum)
@@ -51,8 +52,8 @@ struct Params {
 // Units are rastered in groups of GROUP_M row tiles: the CTAs running at the same
 // time cover ~GROUP_M row tiles x ~grid/GROUP_M vocabulary tiles, so the X and W tiles
 // they stream (re-read once per tile of the other operand) stay resident in L2.
-constexpr int GROUP_M = 16;
 __device__ __forceinline__ void decode(const Params &p, int unit, int &m_tile, int &split) {
+    const int GROUP_M = p.group_m;
     const int n_split = (p.n_vt + p.vt_per_unit - 1) / p.vt_per_unit;
     const int per_group = GROUP_M * n_split;
     const int grp = unit / per_group;
@@ -386,6 +387,7 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     p.vt_per_unit = lmhead_vt_per_unit(n_rows);
     const int32_t n_split = (p.n_vt + p.vt_per_unit - 1) / p.vt_per_unit;
     p.n_units = p.m_tiles * n_split;
+    p.group_m = 16 / CG;  // 16 x 128 rows of X per raster group (measured: 2-4 pair tiles is worse)
     p.rowinfo = rowinfo;
     p.part = part;
     p.zy = zy;
