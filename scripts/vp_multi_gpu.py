@@ -88,9 +88,18 @@ def timing(rank, world, dev, rows, steps, warmup):
     stats = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
     tgt, lw = db.target_ids[:R], db.logp_behav[:R]
 
-    def vp():
+    logp_chk = torch.empty(R, device=dev)
+
+    def vp(logp_out=None):
         loss.loss_chunk_vp(comm, [mine], 0, R, tgt, lw, db.cu_seqlens, adv, inv, traj_sum, stats,
-                           dshards=[dmine], V=V)
+                           dshards=[dmine], V=V, logp_out=logp_out)
+
+    # the exchange protocol must give the same bits on the first call and after hundreds of
+    # calls on the same buffers (epoch parity, tags), in every schedule
+    vp(logp_chk)
+    torch.cuda.synchronize(dev)
+    first = logp_chk.clone()
+    d_first = dmine.clone()
 
     def timed(fn):
         for _ in range(warmup):
@@ -115,6 +124,11 @@ def timing(rank, world, dev, rows, steps, warmup):
     comm.lag, comm.dynamic_rows = 0, 0
     ms_vp = timed(vp)
     plan = G.grpo_async_last_plan()
+    vp(logp_chk)
+    torch.cuda.synchronize(dev)
+    same = bool(torch.equal(first, logp_chk) and torch.equal(d_first, dmine))
+    ok = torch.tensor([1 if same else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     # the same per-rank bytes through the single-GPU kernel: a V = shard_cols problem
     tgt_h = tgt % sc
 
@@ -143,6 +157,7 @@ def timing(rank, world, dev, rows, steps, warmup):
     dist.barrier()
     bytes_rank = R * (hi - lo) * 2 * 2
     return dict(rows=R, V=V, shard_cols=sc, ms_vp_step=ms_vp, ms_vp_modes=modes,
+                bitwise_stable_after_epochs=bool(ok.item()), epochs=comm.epoch,
                 ms_single_kernel_on_shard=ms_half,
                 ms_single_gpu=ms_single,
                 vp_GBps_per_rank=bytes_rank / ms_vp / 1e6,
