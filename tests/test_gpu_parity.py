@@ -284,3 +284,19 @@ def test_odd_vocabulary_sizes(dev, V):
                  {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 1}, None):
         gpu = run_gpu(b, bits, dev, tune=tune)
         compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+
+
+def test_auto_plan_choice(dev):
+    """The auto plan (tune kernel 0) runs K3b below V = 90000 and K3c (32 KB slots) from
+    there on (DESIGN.md §8 measurements); an explicitly tuned call is never redirected."""
+    import paper_2604_26256_b200 as Gp
+    for V, kernel in ((76032, 2), (90000, 3), (152064, 3)):
+        rows = [(np.random.default_rng(V).normal(size=V), 3) for _ in range(4)]
+        b, bits = _adversarial_batch(V, rows)
+        run_gpu(b, bits, dev)
+        plan = Gp.grpo_async_last_plan()
+        assert plan["kernel"] == kernel, (V, plan)
+        if kernel == 3:
+            assert plan["stages"] == 6 and plan["smem_bytes"] >= 6 * 32768
+    run_gpu(b, bits, dev, tune={"kernel": 2, "stages": 8})
+    assert Gp.grpo_async_last_plan()["kernel"] == 2
