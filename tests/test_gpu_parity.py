@@ -300,3 +300,13 @@ def test_auto_plan_choice(dev):
             assert plan["stages"] == 6 and plan["smem_bytes"] >= 6 * 32768
     run_gpu(b, bits, dev, tune={"kernel": 2, "stages": 8})
     assert Gp.grpo_async_last_plan()["kernel"] == 2
+
+
+@pytest.mark.parametrize("name", ["mid152k", "large_small"])
+def test_inplace_auto_plan_long_rows(dev, name):
+    """In-place dlogits (dlogits == logits) with the auto plan on long rows (K3c, 32 KB slots:
+    pass 2 writes the resident chunks while the re-loads of the row's head are in flight)."""
+    b, bits = _case(name, 4)
+    ref = run_oracle(b, bits)
+    gpu = run_gpu(b, bits, dev, inplace=True, chunks=2)
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
