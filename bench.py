@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--lag", type=int, default=0, help="grpo_tune_t.lag (kernel 3: free ring slots)")
+    ap.add_argument("--chunk-kb", type=int, default=0, help="grpo_tune_t.chunk_kb (kernel 3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -258,9 +260,10 @@ def main():
     SG.fill_logits(logits, spec, 0, R, V)
 
     tune = None
-    if args.kernel or args.cluster or args.ctas_per_sm or args.stages:
+    if args.kernel or args.cluster or args.ctas_per_sm or args.stages or args.lag or args.chunk_kb:
         tune = {"kernel": args.kernel, "cluster_size": args.cluster,
-                "ctas_per_sm": args.ctas_per_sm, "stages": args.stages}
+                "ctas_per_sm": args.ctas_per_sm, "stages": args.stages, "lag": args.lag,
+                "chunk_kb": args.chunk_kb}
     loss = G.GrpoAsyncLoss(eps=cfg.eps, std_floor=cfg.std_floor, tune=tune)
     vo = G.ValidateOut(batch.N, batch.P, batch.K, dev)
     adv = torch.empty(batch.N, dtype=torch.float32, device=dev)
