@@ -197,6 +197,42 @@ grpo_status_t grpo_async_advantage_ex(const float *rewards, const int32_t *group
                                       grpo_stream_t stream);
 
 /*
+ * Sharded rewards (the north_star "group reward statistics" all-reduce): when a
+ * rank holds only its own trajectories' rewards, eq:group_advantage needs the
+ * group statistics of all ranks.  Three calls around two all-reduces of the caller's
+ * collective library (NCCL):
+ *   grpo_async_group_partials   part[P*4 + 1] (double) <- per group p of the local
+ *       trajectories: part[4p] = count, part[4p+1] = sum of rewards (ascending local index),
+ *       part[4p+2] = max and part[4p+3] = -min of the rewards' float32 bit patterns (as
+ *       exact doubles), and part[4P] = the local kept tokens (token-mean normalisation).
+ *       Combine entries 4p, 4p+1 and 4P with SUM and 4p+2, 4p+3 with MAX over ranks.
+ *   grpo_async_group_sq_partials  ss[P] (double) <- sum over local members of (R - mean)^2
+ *       with mean = glob[4p+1] / glob[4p] from the combined partials; combine with SUM.
+ *   grpo_async_advantage_from_stats  A_i and inv_norm_i of the local trajectories from the
+ *       combined partials: A_i = 0 when the group's rewards are bitwise equal (max == min),
+ *       else (R_i - mean) / max(std, std_floor) (population std, or n - 1 with
+ *       opts->std_unbiased); inv_norm_i = 1/(P * count_p * L_i) or 1/T_kept (opts->norm)
+ *       and 0 for masked / invalid trajectories -- the same readings as grpo_async_advantage_ex.
+ * The sums are fp64; across ranks they are added in the collective's order, so A_i agrees
+ * with the single-rank result to fp64 rounding (bit-identical for rewards whose partial sums
+ * are exact, e.g. 0/1 rewards).  N may be 0 on a rank.  All pointers are device pointers.
+ * Errors: GRPO_ERR_INVALID_ARG (NULL pointers, P <= 0, N < 0, std_floor <= 0, bad opts),
+ * GRPO_ERR_CUDA.
+ */
+grpo_status_t grpo_async_group_partials(const float *rewards, const int32_t *group_ids,
+                                        const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                        const grpo_loss_opts_t *opts, double *part,
+                                        grpo_stream_t stream);
+grpo_status_t grpo_async_group_sq_partials(const float *rewards, const int32_t *group_ids,
+                                           int32_t N, int32_t P, const double *glob, double *ss,
+                                           grpo_stream_t stream);
+grpo_status_t grpo_async_advantage_from_stats(const float *rewards, const int32_t *group_ids,
+                                              const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                              float std_floor, const grpo_loss_opts_t *opts,
+                                              const double *glob, const double *ss, float *adv,
+                                              float *inv_norm, grpo_stream_t stream);
+
+/*
  * grpo_async_loss_fwd -- fused log-softmax + target gather + ratio + clip +
  * min + segmented mean, and (if dlogits != NULL) the backward in the same pass.
  * The chunk is rows [row_begin, row_begin + n_rows) of this rank's packing.

@@ -35,6 +35,8 @@ EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advan
             "grpo_async_loss_fwd_vp", "grpo_async_loss_bwd", "grpo_async_workspace_size",
             "grpo_async_lmhead_workspace_size", "grpo_async_lmhead_fwd", "grpo_async_lmhead_bwd",
             "grpo_async_lmhead_logits", "grpo_async_lmhead_set_cta_group",
+            "grpo_async_group_partials", "grpo_async_group_sq_partials",
+            "grpo_async_advantage_from_stats",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -121,6 +123,12 @@ def _load():
     lib.grpo_async_lmhead_bwd.restype = st
     lib.grpo_async_lmhead_logits.argtypes = [P, P, i64, i32, i32, P, i64, P]
     lib.grpo_async_lmhead_logits.restype = st
+    lib.grpo_async_group_partials.argtypes = [P, P, P, i32, i32, P, P, P]
+    lib.grpo_async_group_partials.restype = st
+    lib.grpo_async_group_sq_partials.argtypes = [P, P, i32, i32, P, P, P]
+    lib.grpo_async_group_sq_partials.restype = st
+    lib.grpo_async_advantage_from_stats.argtypes = [P, P, P, i32, i32, f32, P, P, P, P, P, P]
+    lib.grpo_async_advantage_from_stats.restype = st
     lib.grpo_async_lmhead_set_cta_group.argtypes = [i32]
     lib.grpo_async_lmhead_set_cta_group.restype = st
     lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
@@ -410,3 +418,29 @@ def grpo_async_lmhead_logits(hidden, W, n_rows, d, V, out, ld_out, stream=None):
 
 def grpo_async_lmhead_set_cta_group(cta_group: int) -> None:
     _check(LIB.grpo_async_lmhead_set_cta_group(int(cta_group)))
+
+
+# ---- sharded rewards: group statistics through the caller's all-reduce
+def grpo_async_group_partials(rewards, group_ids, cu_seqlens, N, P, part, traj_mask=None,
+                              stream=None):
+    o = _opts(0.2, 0.2, NORM_SEQ, traj_mask)
+    _check(LIB.grpo_async_group_partials(
+        _ptr(rewards, torch.float32, "rewards"), _ptr(group_ids, torch.int32, "group_ids"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, P, C.byref(o),
+        _ptr(part, torch.float64, "part"), _stream(stream)))
+
+
+def grpo_async_group_sq_partials(rewards, group_ids, N, P, glob, ss, stream=None):
+    _check(LIB.grpo_async_group_sq_partials(
+        _ptr(rewards, torch.float32, "rewards"), _ptr(group_ids, torch.int32, "group_ids"), N, P,
+        _ptr(glob, torch.float64, "glob"), _ptr(ss, torch.float64, "ss"), _stream(stream)))
+
+
+def grpo_async_advantage_from_stats(rewards, group_ids, cu_seqlens, N, P, std_floor, norm,
+                                    traj_mask, std_unbiased, glob, ss, adv, inv_norm, stream=None):
+    o = _opts(0.2, 0.2, norm, traj_mask, std_unbiased)
+    _check(LIB.grpo_async_advantage_from_stats(
+        _ptr(rewards, torch.float32, "rewards"), _ptr(group_ids, torch.int32, "group_ids"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, P, float(std_floor), C.byref(o),
+        _ptr(glob, torch.float64, "glob"), _ptr(ss, torch.float64, "ss"),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"), _stream(stream)))

@@ -119,6 +119,45 @@ class GrpoAsyncLoss:
         self.launches += L.grpo_last_launch_count()
         return adv, inv
 
+    # ---- advantages from sharded rewards (SURVEY §8e "group reward statistics" variant)
+    def advantage_sharded(self, rewards, group_ids, cu_seqlens, P, allreduce=None, stream=None):
+        """This rank's trajectories only (rewards, group_ids, local cu_seqlens); the group
+        statistics of all ranks are combined with two rounds of all-reduce.  `allreduce(t, op)`
+        reduces a float64 device tensor in place over the ranks ("sum" or "max"); the default
+        uses torch.distributed (NCCL).  Returns (adv, inv_norm) of the local trajectories."""
+        if allreduce is None:
+            import torch.distributed as dist
+
+            def allreduce(t, op):
+                dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX)
+        dev = rewards.device
+        N = int(rewards.numel())
+        part = torch.empty(4 * P + 1, dtype=torch.float64, device=dev)
+        L.grpo_async_group_partials(rewards, group_ids, cu_seqlens, N, P, part, self.traj_mask,
+                                    stream)
+        self.launches += L.grpo_last_launch_count()
+        p4 = part[:4 * P].view(P, 4)
+        summed = torch.cat([p4[:, :2].reshape(-1), part[4 * P:]])
+        maxed = p4[:, 2:].reshape(-1).contiguous()
+        allreduce(summed, "sum")
+        allreduce(maxed, "max")
+        glob = torch.empty_like(part)
+        g4 = glob[:4 * P].view(P, 4)
+        g4[:, :2] = summed[:2 * P].view(P, 2)
+        g4[:, 2:] = maxed.view(P, 2)
+        glob[4 * P] = summed[2 * P]
+        ss = torch.empty(P, dtype=torch.float64, device=dev)
+        L.grpo_async_group_sq_partials(rewards, group_ids, N, P, glob, ss, stream)
+        self.launches += L.grpo_last_launch_count()
+        allreduce(ss, "sum")
+        adv = torch.empty(max(N, 1), dtype=torch.float32, device=dev)
+        inv = torch.empty(max(N, 1), dtype=torch.float32, device=dev)
+        L.grpo_async_advantage_from_stats(rewards, group_ids, cu_seqlens, N, P, self.std_floor,
+                                          self.norm, self.traj_mask, self.std_unbiased, glob, ss,
+                                          adv, inv, stream)
+        self.launches += L.grpo_last_launch_count()
+        return adv[:N], inv[:N]
+
     def _default_opts(self):
         return (self.eps_hi == self.eps and self.norm == L.NORM_SEQ and self.traj_mask is None
                 and not self.std_unbiased)

@@ -212,6 +212,54 @@ grpo_status_t grpo_async_advantage(const float *rewards, const int32_t *group_id
     return ok(launches);
 }
 
+grpo_status_t grpo_async_group_partials(const float *rewards, const int32_t *group_ids,
+                                        const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                        const grpo_loss_opts_t *opts, double *part,
+                                        grpo_stream_t stream) {
+    if (N < 0 || P <= 0) return fail(GRPO_ERR_INVALID_ARG, "group_partials: N=%d P=%d", N, P);
+    if (!part || (N > 0 && (!rewards || !group_ids || !cu_seqlens)))
+        return fail(GRPO_ERR_INVALID_ARG, "group_partials: NULL pointer");
+    int launches = 0;
+    cudaError_t e = grpo::launch_group_partials(rewards, group_ids, cu_seqlens, N, P,
+                                                opts ? opts->traj_mask : nullptr, part,
+                                                (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "group_partials");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_group_sq_partials(const float *rewards, const int32_t *group_ids,
+                                           int32_t N, int32_t P, const double *glob, double *ss,
+                                           grpo_stream_t stream) {
+    if (N < 0 || P <= 0) return fail(GRPO_ERR_INVALID_ARG, "group_sq_partials: N=%d P=%d", N, P);
+    if (!glob || !ss || (N > 0 && (!rewards || !group_ids)))
+        return fail(GRPO_ERR_INVALID_ARG, "group_sq_partials: NULL pointer");
+    int launches = 0;
+    cudaError_t e = grpo::launch_group_sq(rewards, group_ids, N, P, glob, ss, (cudaStream_t)stream,
+                                          &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "group_sq_partials");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_advantage_from_stats(const float *rewards, const int32_t *group_ids,
+                                              const int64_t *cu_seqlens, int32_t N, int32_t P,
+                                              float std_floor, const grpo_loss_opts_t *opts,
+                                              const double *glob, const double *ss, float *adv,
+                                              float *inv_norm, grpo_stream_t stream) {
+    if (N < 0 || P <= 0) return fail(GRPO_ERR_INVALID_ARG, "advantage_from_stats: N=%d P=%d", N, P);
+    if (!(std_floor > 0.0f)) return fail(GRPO_ERR_INVALID_ARG, "advantage_from_stats: std_floor must be > 0");
+    if (opts && opts->norm != GRPO_NORM_SEQ && opts->norm != GRPO_NORM_TOKEN)
+        return fail(GRPO_ERR_INVALID_ARG, "advantage_from_stats: norm %d", opts->norm);
+    if (!glob || !ss || (N > 0 && (!rewards || !group_ids || !cu_seqlens || !adv || !inv_norm)))
+        return fail(GRPO_ERR_INVALID_ARG, "advantage_from_stats: NULL pointer");
+    int launches = 0;
+    cudaError_t e = grpo::launch_advantage_from_stats(
+        rewards, group_ids, cu_seqlens, N, P, std_floor, opts ? opts->norm : GRPO_NORM_SEQ,
+        opts && opts->std_unbiased ? 1 : 0, opts ? opts->traj_mask : nullptr, glob, ss, adv, inv_norm,
+        (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "advantage_from_stats");
+    return ok(launches);
+}
+
 grpo_status_t grpo_async_advantage_ex(const float *rewards, const int32_t *group_ids,
                                       const int64_t *cu_seqlens, int32_t N, int32_t P,
                                       float std_floor, const grpo_loss_opts_t *opts, float *adv,

@@ -388,6 +388,16 @@ struct LossArgs {
 };
 
 cudaError_t launch_rowinfo(const LossArgs &a, cudaStream_t s, int *launches);
+cudaError_t launch_group_partials(const float *rewards, const int32_t *group_ids, const int64_t *cu,
+                                  int32_t N, int32_t P, const uint8_t *traj_mask, double *part,
+                                  cudaStream_t s, int *launches);
+cudaError_t launch_group_sq(const float *rewards, const int32_t *group_ids, int32_t N, int32_t P,
+                            const double *glob, double *ss, cudaStream_t s, int *launches);
+cudaError_t launch_advantage_from_stats(const float *rewards, const int32_t *group_ids, const int64_t *cu,
+                                        int32_t N, int32_t P, float std_floor, int32_t norm,
+                                        int32_t unbiased, const uint8_t *traj_mask, const double *glob,
+                                        const double *ss, float *adv, float *inv_norm, cudaStream_t s,
+                                        int *launches);
 cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
                                  int *launches, char *why, size_t why_len, grpo_plan_t *plan);
 cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
