@@ -415,6 +415,7 @@ def main():
                                  "chunk buffer (DESIGN.md input recipe)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac_of_spec_8000_gbs": achieved / 8000.0,
                          "kernel": {1: "fused_cluster_kernel", 2: "rowwise_kernel",
                                     3: "stream_kernel"}.get(
                              plan["kernel"], str(plan["kernel"])),
