@@ -461,11 +461,7 @@ cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cud
     }
     if (auto_lag && stages < lag + 2) lag = stages - 2 >= 1 ? stages - 2 : 1;
     fp.lag = lag;
-    {
-        const char *pc = getenv("GRPO_FUSED_PIECE");
-        fp.piece = pc ? (uint32_t)atoi(pc) : 0u;
-        fp.piece = fp.piece ? (fp.piece + 15u) / 16u * 16u : fp.stage_bytes;
-    }
+    fp.piece = fp.stage_bytes;  // one bulk copy per slice
     if (stages > kMaxStages) {
         if (why) snprintf(why, why_len, "stages %d > %d", stages, kMaxStages);
         return cudaErrorInvalidValue;
