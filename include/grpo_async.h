@@ -375,6 +375,41 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
  */
 size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N);
 
+/*
+ * Tensor-parallel LM head (NEXT(2) in the trainer's Megatron layout; NEXT(3)'s
+ * vocabulary split): rank q holds W rows [col_offset, col_offset + Vs) and the full hidden
+ * states.  Forward: grpo_async_lmhead_tp_partials computes this shard's per-row partial
+ *   row_part[4*row .. 4*row+3] = (max, sum 2^(t - max) in log2 units, z_y, 1 if this shard
+ *   holds y_t else 0)   (float; workspace: grpo_async_lmhead_workspace_size(n_rows, Vs, 1));
+ * the caller all-gathers the R ranks' row_part arrays in rank order ([R][n_rows][4]) and
+ * grpo_async_lmhead_tp_fwd finishes logp / lse / token_scale / traj_sum / stats identically on
+ * every rank (arguments as grpo_async_lmhead_fwd; workspace grpo_async_workspace_size).
+ * Backward: grpo_async_lmhead_tp_bwd writes this shard's dz columns and, with dhidden_partial
+ * (float [n_rows, d]), this shard's dz_q W_q -- the caller all-reduces (SUM) the partials
+ * over the ranks -- and dW_q += dz_q^T hidden (float [Vs, d]).
+ * Errors: as the single-GPU LM-head calls; GRPO_ERR_INVALID_ARG for R < 1 or col_offset < 0.
+ */
+grpo_status_t grpo_async_lmhead_tp_partials(const uint16_t *hidden, const uint16_t *W_shard,
+                                            int64_t n_rows, int32_t d, int32_t Vs,
+                                            int32_t col_offset, const int64_t *target_ids,
+                                            float *row_part, void *workspace,
+                                            size_t workspace_bytes, grpo_stream_t stream);
+grpo_status_t grpo_async_lmhead_tp_fwd(const float *row_parts, int32_t R, int64_t row_begin,
+                                       int64_t n_rows, int32_t V, const int64_t *target_ids,
+                                       const float *logp_behav, const int64_t *cu_seqlens,
+                                       int32_t N, const int32_t *traj_index, const float *adv,
+                                       const float *inv_norm, const grpo_loss_opts_t *opts,
+                                       float grad_scale, float *logp_out, float *lse_out,
+                                       float *token_scale_out, double *traj_sum, double *stats,
+                                       void *workspace, size_t workspace_bytes,
+                                       grpo_stream_t stream);
+grpo_status_t grpo_async_lmhead_tp_bwd(const uint16_t *hidden, const uint16_t *W_shard,
+                                       int64_t n_rows, int32_t d, int32_t Vs, int32_t col_offset,
+                                       const int64_t *target_ids, const float *lse,
+                                       const float *token_scale, float grad_scale_mult,
+                                       uint16_t *dz, int64_t ld_dz, float *dhidden_partial,
+                                       float *dW_shard, grpo_stream_t stream);
+
 /* Tensor-core mode of the calling thread's later LM-head calls: 1 = one CTA per MMA
  * (tcgen05.mma.cta_group::1, 128 x 256 tiles), 2 = CTA pairs on one TPC (cta_group::2,
  * 256 x 256 tiles, each CTA stages half of the W tile; the default).  Same results.

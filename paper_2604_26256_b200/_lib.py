@@ -36,7 +36,8 @@ EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advan
             "grpo_async_lmhead_workspace_size", "grpo_async_lmhead_fwd", "grpo_async_lmhead_bwd",
             "grpo_async_lmhead_logits", "grpo_async_lmhead_set_cta_group",
             "grpo_async_group_partials", "grpo_async_group_sq_partials",
-            "grpo_async_advantage_from_stats",
+            "grpo_async_advantage_from_stats", "grpo_async_lmhead_tp_partials",
+            "grpo_async_lmhead_tp_fwd", "grpo_async_lmhead_tp_bwd",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -129,6 +130,13 @@ def _load():
     lib.grpo_async_group_sq_partials.restype = st
     lib.grpo_async_advantage_from_stats.argtypes = [P, P, P, i32, i32, f32, P, P, P, P, P, P]
     lib.grpo_async_advantage_from_stats.restype = st
+    lib.grpo_async_lmhead_tp_partials.argtypes = [P, P, i64, i32, i32, i32, P, P, P, sz, P]
+    lib.grpo_async_lmhead_tp_partials.restype = st
+    lib.grpo_async_lmhead_tp_fwd.argtypes = [P, i32, i64, i64, i32, P, P, P, i32, P, P, P, P, f32,
+                                             P, P, P, P, P, P, sz, P]
+    lib.grpo_async_lmhead_tp_fwd.restype = st
+    lib.grpo_async_lmhead_tp_bwd.argtypes = [P, P, i64, i32, i32, i32, P, P, P, f32, P, i64, P, P, P]
+    lib.grpo_async_lmhead_tp_bwd.restype = st
     lib.grpo_async_lmhead_set_cta_group.argtypes = [i32]
     lib.grpo_async_lmhead_set_cta_group.restype = st
     lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
@@ -444,3 +452,39 @@ def grpo_async_advantage_from_stats(rewards, group_ids, cu_seqlens, N, P, std_fl
         _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, P, float(std_floor), C.byref(o),
         _ptr(glob, torch.float64, "glob"), _ptr(ss, torch.float64, "ss"),
         _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"), _stream(stream)))
+
+
+# ---- tensor-parallel LM head (NEXT(2) x NEXT(3))
+def grpo_async_lmhead_tp_partials(hidden, W_shard, n_rows, d, Vs, col_offset, target_ids, row_part,
+                                  workspace, stream=None):
+    _check(LIB.grpo_async_lmhead_tp_partials(
+        _bf16(hidden, "hidden"), _bf16(W_shard, "W_shard"), n_rows, d, Vs, col_offset,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(row_part, torch.float32, "row_part"),
+        _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
+
+
+def grpo_async_lmhead_tp_fwd(row_parts, R, row_begin, n_rows, V, target_ids, logp_behav,
+                             cu_seqlens, N, traj_index, adv, inv_norm, eps_lo, eps_hi, norm,
+                             traj_mask, grad_scale, logp_out, lse_out, token_scale_out, traj_sum,
+                             stats, workspace, stream=None):
+    o = _opts(eps_lo, eps_hi, norm, traj_mask)
+    _check(LIB.grpo_async_lmhead_tp_fwd(
+        _ptr(row_parts, torch.float32, "row_parts"), R, row_begin, n_rows, V,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(logp_behav, torch.float32, "logp_behav"),
+        _ptr(cu_seqlens, torch.int64, "cu_seqlens"), N, _ptr(traj_index, torch.int32, "traj_index"),
+        _ptr(adv, torch.float32, "adv"), _ptr(inv_norm, torch.float32, "inv_norm"), C.byref(o),
+        float(grad_scale), _ptr(logp_out, torch.float32, "logp_out"),
+        _ptr(lse_out, torch.float32, "lse_out"), _ptr(token_scale_out, torch.float32, "token_scale_out"),
+        _ptr(traj_sum, torch.float64, "traj_sum"), _ptr(stats, torch.float64, "stats"),
+        _ptr(workspace, torch.uint8, "workspace"), workspace.numel(), _stream(stream)))
+
+
+def grpo_async_lmhead_tp_bwd(hidden, W_shard, n_rows, d, Vs, col_offset, target_ids, lse,
+                             token_scale, grad_scale_mult, dz, ld_dz, dhidden_partial, dW_shard,
+                             stream=None):
+    _check(LIB.grpo_async_lmhead_tp_bwd(
+        _bf16(hidden, "hidden"), _bf16(W_shard, "W_shard"), n_rows, d, Vs, col_offset,
+        _ptr(target_ids, torch.int64, "target_ids"), _ptr(lse, torch.float32, "lse"),
+        _ptr(token_scale, torch.float32, "token_scale"), float(grad_scale_mult), _bf16(dz, "dz"),
+        ld_dz, _ptr(dhidden_partial, torch.float32, "dhidden_partial"),
+        _ptr(dW_shard, torch.float32, "dW_shard"), _stream(stream)))

@@ -218,6 +218,48 @@ class GrpoAsyncLoss:
                                 dz.shape[1], dhidden, dW, stream)
         self.launches += L.grpo_last_launch_count()
 
+    # ---- tensor-parallel LM head: W split by vocabulary rows over the ranks of a group
+    def lmhead_tp_fwd(self, hidden, W_shard, col_offset, V, row_begin, n_rows, target_ids,
+                      logp_behav, cu_seqlens, adv, inv_norm, traj_sum, stats, allgather=None,
+                      R=None, logp_out=None, lse_out=None, scale_out=None, traj_index=None,
+                      stream=None):
+        """allgather(t) returns the ranks' copies of the float32 device tensor t stacked in
+        rank order (default: torch.distributed.all_gather_into_tensor over NCCL)."""
+        Vs, d = W_shard.shape
+        dev = W_shard.device
+        ws = torch.empty(L.grpo_async_lmhead_workspace_size(n_rows, Vs, 1), dtype=torch.uint8,
+                         device=dev)
+        part = torch.empty((max(n_rows, 1), 4), dtype=torch.float32, device=dev)
+        L.grpo_async_lmhead_tp_partials(hidden, W_shard, n_rows, d, Vs, col_offset, target_ids,
+                                        part, ws, stream)
+        self.launches += L.grpo_last_launch_count()
+        if allgather is None:
+            import torch.distributed as dist
+
+            def allgather(t):
+                out = torch.empty((dist.get_world_size(),) + tuple(t.shape), dtype=t.dtype,
+                                  device=t.device)
+                dist.all_gather_into_tensor(out, t.contiguous())
+                return out
+        parts = allgather(part).contiguous()
+        R = parts.shape[0]
+        N = cu_seqlens.numel() - 1
+        ws2 = self.workspace(n_rows, V, N, dev)
+        L.grpo_async_lmhead_tp_fwd(parts, R, row_begin, n_rows, V, target_ids, logp_behav,
+                                   cu_seqlens, N, traj_index, adv, inv_norm, self.eps, self.eps_hi,
+                                   self.norm, self.traj_mask, self.grad_scale, logp_out, lse_out,
+                                   scale_out, traj_sum, stats, ws2, stream)
+        self.launches += L.grpo_last_launch_count()
+
+    def lmhead_tp_bwd(self, hidden, W_shard, col_offset, n_rows, target_ids, lse, token_scale, dz,
+                      dhidden_partial=None, dW_shard=None, mult=1.0, stream=None):
+        """dhidden_partial (float32) is this shard's dz W_shard: sum it over the ranks."""
+        Vs, d = W_shard.shape
+        L.grpo_async_lmhead_tp_bwd(hidden, W_shard, n_rows, d, Vs, col_offset, target_ids, lse,
+                                   token_scale, mult, dz, dz.shape[1], dhidden_partial, dW_shard,
+                                   stream)
+        self.launches += L.grpo_last_launch_count()
+
     # ---- fused loss over vocabulary-parallel logits (SURVEY NEXT(3), P:282)
     def loss_chunk_vp(self, comm, shards, row_begin, n_rows, target_ids, logp_behav, cu_seqlens,
                       adv, inv_norm, traj_sum, stats, dshards=None, traj_index=None,

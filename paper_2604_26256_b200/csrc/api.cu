@@ -689,6 +689,145 @@ grpo_status_t grpo_async_lmhead_bwd(const uint16_t *hidden, const uint16_t *W, i
     return ok(launches);
 }
 
+grpo_status_t grpo_async_lmhead_tp_partials(const uint16_t *hidden, const uint16_t *W_shard,
+                                            int64_t n_rows, int32_t d, int32_t Vs,
+                                            int32_t col_offset, const int64_t *target_ids,
+                                            float *row_part, void *workspace,
+                                            size_t workspace_bytes, grpo_stream_t stream) {
+    grpo_status_t st = lm_check("lmhead_tp_partials", hidden, W_shard, n_rows, d, Vs);
+    if (st != GRPO_OK) return st;
+    if (col_offset < 0) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_partials: col_offset %d", col_offset);
+    if (n_rows > 0 && (!target_ids || !row_part))
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_partials: NULL target_ids/row_part");
+    const size_t need = grpo_async_lmhead_workspace_size(n_rows, Vs, 1);
+    if (!workspace || workspace_bytes < need)
+        return fail(GRPO_ERR_WORKSPACE, "lmhead_tp_partials: workspace %zu B < required %zu B",
+                    workspace_bytes, need);
+    if (n_rows == 0) return ok(0);
+    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
+    const int32_t n_split = grpo::lmhead_n_split(n_rows, Vs);
+    float2 *part = reinterpret_cast<float2 *>(w);
+    w += align256((size_t)n_split * (size_t)n_rows * 8);
+    float *zy = reinterpret_cast<float *>(w);
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_lmhead(0, hidden, W_shard, n_rows, d, Vs, nullptr, part, zy, nullptr, 0,
+                                        target_ids, nullptr, nullptr, 1.0f, s, &launches, &g_last_plan, why,
+                                        sizeof why, g_lm_cta_group, col_offset);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_partials/tcgen05", why);
+    e = grpo::launch_lmhead_rowpart(part, zy, n_split, n_rows, target_ids, col_offset, Vs,
+                                    reinterpret_cast<float4 *>(row_part), s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_partials/rowpart");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_lmhead_tp_fwd(const float *row_parts, int32_t R, int64_t row_begin,
+                                       int64_t n_rows, int32_t V, const int64_t *target_ids,
+                                       const float *logp_behav, const int64_t *cu_seqlens,
+                                       int32_t N, const int32_t *traj_index, const float *adv,
+                                       const float *inv_norm, const grpo_loss_opts_t *opts,
+                                       float grad_scale, float *logp_out, float *lse_out,
+                                       float *token_scale_out, double *traj_sum, double *stats,
+                                       void *workspace, size_t workspace_bytes,
+                                       grpo_stream_t stream) {
+    if (R < 1) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_fwd: R=%d", R);
+    if (!opts) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_fwd: NULL opts");
+    if (!(opts->eps_lo > 0.0f && opts->eps_lo < 1.0f) || !(opts->eps_hi > 0.0f))
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_fwd: eps_lo not in (0,1) or eps_hi <= 0");
+    if (n_rows < 0 || N <= 0 || V <= 0 || row_begin < 0)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_fwd: n_rows/N/V/row_begin");
+    if (!cu_seqlens || !adv || !inv_norm || !traj_sum || !stats)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_fwd: NULL cu_seqlens/adv/inv_norm/traj_sum/stats");
+    if (n_rows > 0 && (!target_ids || !logp_behav || !row_parts))
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_fwd: NULL target_ids/logp_behav/row_parts");
+    const size_t need = grpo_async_workspace_size(n_rows, V, N);
+    if (!workspace || workspace_bytes < need)
+        return fail(GRPO_ERR_WORKSPACE, "lmhead_tp_fwd: workspace %zu B < required %zu B", workspace_bytes,
+                    need);
+    grpo::LossArgs a{};
+    a.V = V;
+    a.row_begin = row_begin;
+    a.n_rows = n_rows;
+    a.target_ids = target_ids;
+    a.logp_behav = logp_behav;
+    a.cu_seqlens = cu_seqlens;
+    a.N = N;
+    a.traj_index = traj_index;
+    a.adv = adv;
+    a.inv_norm = inv_norm;
+    a.eps_lo = opts->eps_lo;
+    a.eps_hi = opts->eps_hi;
+    a.grad_scale = grad_scale;
+    a.logp_out = logp_out;
+    a.lse_out = lse_out;
+    a.scale_out = token_scale_out;
+    a.traj_sum = traj_sum;
+    a.stats = stats;
+    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
+    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
+    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
+    a.term_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.logp_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.flag_ws = w;
+    w += align256((size_t)n_rows);
+    a.part_ws = reinterpret_cast<double *>(w);
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    cudaError_t e = grpo::launch_rowinfo(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_fwd/rowinfo");
+    e = grpo::launch_lmhead_tp_combine(reinterpret_cast<const float4 *>(row_parts), R, a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_fwd/combine");
+    e = grpo::launch_segment_reduce(a, s, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_fwd/segment_reduce");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_lmhead_tp_bwd(const uint16_t *hidden, const uint16_t *W_shard,
+                                       int64_t n_rows, int32_t d, int32_t Vs, int32_t col_offset,
+                                       const int64_t *target_ids, const float *lse,
+                                       const float *token_scale, float grad_scale_mult,
+                                       uint16_t *dz, int64_t ld_dz, float *dhidden_partial,
+                                       float *dW_shard, grpo_stream_t stream) {
+    grpo_status_t st = lm_check("lmhead_tp_bwd", hidden, W_shard, n_rows, d, Vs);
+    if (st != GRPO_OK) return st;
+    if (col_offset < 0) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_bwd: col_offset %d", col_offset);
+    if (n_rows > 0 && (!target_ids || !lse || !token_scale || !dz))
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_bwd: NULL target_ids/lse/token_scale/dz");
+    if (ld_dz < Vs || ld_dz % 8 != 0 || (dz && !aligned16(dz)))
+        return fail(GRPO_ERR_ALIGNMENT, "lmhead_tp_bwd: ld_dz=%lld must be >= Vs, a multiple of 8, dz aligned",
+                    (long long)ld_dz);
+    if (n_rows == 0) return ok(0);
+    cudaStream_t s = (cudaStream_t)stream;
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_lmhead(1, hidden, W_shard, n_rows, d, Vs, nullptr, nullptr, nullptr, dz, ld_dz,
+                                        target_ids, lse, token_scale, grad_scale_mult, s, &launches,
+                                        &g_last_plan, why, sizeof why, g_lm_cta_group, col_offset);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_bwd/tcgen05", why);
+    if (dhidden_partial || dW_shard) {
+        cublasHandle_t h = cublas_handle();
+        if (!h) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: cublasCreate failed");
+        if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: cublasSetStream");
+        const float one = 1.0f, zero = 0.0f;
+        if (dhidden_partial) {  // f32 partial (summed over the ranks by the caller)
+            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, d, (int)n_rows, Vs, &one, W_shard,
+                                             CUDA_R_16BF, d, dz, CUDA_R_16BF, (int)ld_dz, &zero, dhidden_partial,
+                                             CUDA_R_32F, d, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: dhidden GEMM status %d", (int)cs);
+        }
+        if (dW_shard) {
+            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, d, Vs, (int)n_rows, &one, hidden,
+                                             CUDA_R_16BF, d, dz, CUDA_R_16BF, (int)ld_dz, &one, dW_shard, CUDA_R_32F,
+                                             d, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: dW GEMM status %d", (int)cs);
+        }
+    }
+    return ok(launches);
+}
+
 grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
                                        int32_t d, int32_t V, uint16_t *out, int64_t ld_out,
                                        grpo_stream_t stream) {

@@ -429,7 +429,12 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
                           const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,
                           const int64_t *targets, const float *lse, const float *scale, float mult,
                           cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len,
-                          int cta_group);
+                          int cta_group, int32_t col_offset = 0);
+cudaError_t launch_lmhead_rowpart(const float2 *part, const float *zy, int32_t n_split, int64_t n_rows,
+                                  const int64_t *targets, int32_t col_offset, int32_t Vs, float4 *out,
+                                  cudaStream_t s, int *launches);
+cudaError_t launch_lmhead_tp_combine(const float4 *parts, int32_t R, const LossArgs &a, cudaStream_t s,
+                                     int *launches);
 cudaError_t launch_lmhead_combine(const float2 *part, const float *zy, int32_t n_split, const LossArgs &a,
                                   cudaStream_t s, int *launches);
 cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned long long *row_ctr,

@@ -36,6 +36,7 @@ enum { EPI_STATS = 0, EPI_DZ = 1, EPI_LOGITS = 2 };
 struct Params {
     int32_t n_rows, V, d;
     int32_t m_tiles, n_vt, vt_per_unit, n_units, group_m;
+    int32_t col_offset;  // first vocabulary id of this W shard (tensor-parallel head), else 0
     // EPI_STATS
     const RowInfo *rowinfo;
     float2 *part;  // [n_split][n_rows] log2-domain (max, sum)
@@ -203,10 +204,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int32_t y = -1;
             float lse2 = 0.0f, sc = 0.0f;
             if (EPI == EPI_STATS) {
-                y = valid ? p.rowinfo[row].target : -1;
+                // the target's column in this W shard (-1: another shard holds it)
+                const int64_t t = !valid ? -1 : (p.rowinfo ? (int64_t)p.rowinfo[row].target : p.targets[row]);
+                y = (t >= p.col_offset && t - p.col_offset < p.V) ? (int32_t)(t - p.col_offset) : -1;
             } else if (EPI == EPI_DZ && valid) {
                 const int64_t t = p.targets[row];
-                y = (t >= 0 && t < p.V) ? (int32_t)t : -1;
+                y = (t >= p.col_offset && t - p.col_offset < p.V) ? (int32_t)(t - p.col_offset) : -1;
                 lse2 = p.lse[row] * kLog2e;
                 sc = p.scale[row] * p.mult;
             }
@@ -326,6 +329,53 @@ __global__ void __launch_bounds__(256) lmhead_combine_kernel(const float2 *__res
     a.flag_ws[row] = o.flags;
 }
 
+// tensor-parallel head: this shard's per-row partial (log2-domain max, sum, z_y, holds-y)
+// from its n_split unit partials, merged in unit order
+__global__ void __launch_bounds__(256) lmhead_rowpart_kernel(const float2 *__restrict__ part,
+                                                             const float *__restrict__ zy_ws,
+                                                             int32_t n_split, int64_t n_rows,
+                                                             const int64_t *__restrict__ targets,
+                                                             int32_t col_offset, int32_t Vs,
+                                                             float4 *__restrict__ out) {
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= n_rows) return;
+    float M = -INFINITY, S = 0.0f;
+    for (int s = 0; s < n_split; ++s) {
+        const float2 v = part[(int64_t)s * n_rows + row];
+        lse2_merge(M, S, v.x, v.y);
+    }
+    const int64_t t = targets[row];
+    const bool mine = t >= col_offset && t - col_offset < Vs;
+    out[row] = make_float4(M, S, mine ? zy_ws[row] : 0.0f, mine ? 1.0f : 0.0f);
+}
+
+// the R shards' partials of each row merged in rank order (identical on every rank), then
+// the per-token epilogue of the logits kernels
+__global__ void __launch_bounds__(256) lmhead_tp_combine_kernel(const float4 *__restrict__ parts,
+                                                                int32_t R, LossArgs a) {
+    const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (row >= a.n_rows) return;
+    float M = -INFINITY, S = 0.0f, zy = __int_as_float(0x7FC00000);
+    for (int q = 0; q < R; ++q) {
+        const float4 v = parts[(int64_t)q * a.n_rows + row];
+        lse2_merge(M, S, v.x, v.y);
+        if (v.w != 0.0f) zy = v.z;
+    }
+    const RowInfo ri = a.rowinfo[row];
+    const bool y_valid = ri.target >= 0 && ri.target < a.V;
+    const float zyv = y_valid ? zy : __int_as_float(0x7FC00000);
+    const float l2s = log2f(S);
+    const double logp_d = row_logp(zyv, M, l2s);
+    const RowOut o = row_epilogue(logp_d, ri, a.eps_lo, a.eps_hi, a.grad_scale);
+    const float logp = (float)logp_d;
+    if (a.logp_out) a.logp_out[row] = logp;
+    if (a.lse_out) a.lse_out[row] = (M + l2s) * kLn2;
+    if (a.scale_out) a.scale_out[row] = o.s;
+    a.term_ws[row] = o.term;
+    a.logp_ws[row] = logp;
+    a.flag_ws[row] = o.flags;
+}
+
 // ---------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -369,7 +419,7 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
                           const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,
                           const int64_t *targets, const float *lse, const float *scale, float mult,
                           cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len,
-                          int cta_group) {
+                          int cta_group, int32_t col_offset) {
     using namespace lm;
     if (n_rows == 0) return cudaSuccess;
     const int CG = cta_group == 1 ? 1 : 2;
@@ -397,6 +447,7 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     p.lse = lse;
     p.scale = scale;
     p.mult = mult;
+    p.col_offset = col_offset;
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -445,6 +496,24 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
         plan->smem_bytes = CG == 1 ? Geo<1>::SMEM : Geo<2>::SMEM;
     }
     return cudaSuccess;
+}
+
+cudaError_t launch_lmhead_rowpart(const float2 *part, const float *zy, int32_t n_split, int64_t n_rows,
+                                  const int64_t *targets, int32_t col_offset, int32_t Vs, float4 *out,
+                                  cudaStream_t s, int *launches) {
+    if (n_rows == 0) return cudaSuccess;
+    lm::lmhead_rowpart_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(part, zy, n_split, n_rows,
+                                                                               targets, col_offset, Vs, out);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lmhead_tp_combine(const float4 *parts, int32_t R, const LossArgs &a, cudaStream_t s,
+                                     int *launches) {
+    if (a.n_rows == 0) return cudaSuccess;
+    lm::lmhead_tp_combine_kernel<<<(unsigned)((a.n_rows + 255) / 256), 256, 0, s>>>(parts, R, a);
+    *launches += 1;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_lmhead_combine(const float2 *part, const float *zy, int32_t n_split, const LossArgs &a,
