@@ -322,3 +322,23 @@ def run_batch_lmhead(batch, hidden_bits, W_bits, eps=0.2, grad_scale=1.0, std_fl
         out["dhidden"] = rr.dlogits @ _bf16_to_f64(W_bits)
         out["dW"] = rr.dlogits.T @ _bf16_to_f64(hidden_bits)
     return out
+
+
+def lmhead_logits_rows(hidden_rows_bits, W_bits, block=16384):
+    """lmhead_logits for a few rows of X against a large W, W widened block by block (the same
+    definition, bounded memory: full-size parity tests)."""
+    Xr = _bf16_to_f64(hidden_rows_bits)
+    V = W_bits.shape[0]
+    out = np.empty((Xr.shape[0], V), np.float64)
+    for v0 in range(0, V, block):
+        out[:, v0:v0 + block] = Xr @ _bf16_to_f64(W_bits[v0:v0 + block]).T
+    return out
+
+
+def matmul_rows_W(rows_f64, W_bits, block=16384):
+    """rows [k, V] (fp64) times W [V, d] (bf16, widened block by block): dJ/dX of the rows."""
+    V, d = W_bits.shape
+    out = np.zeros((rows_f64.shape[0], d), np.float64)
+    for v0 in range(0, V, block):
+        out += rows_f64[:, v0:v0 + block] @ _bf16_to_f64(W_bits[v0:v0 + block])
+    return out

@@ -12,6 +12,7 @@ import torch
 
 import oracle.oracle as O
 import paper_2604_26256_b200 as G
+from synth.gen import make_batch
 from paper_2604_26256_b200 import _lib as L
 from tests.gpu_util import compare, lmhead_batch, run_gpu_lmhead, to_dev_bits
 
@@ -192,3 +193,59 @@ def test_lmhead_tensor_parallel(dev, name, d, R, cta_group):
     assert abs(J - ref["J"]) / max(abs(ref["J"]), 1e-2 * S_abs) <= 1e-5
     for k, rk in (("dz", rr.dlogits), ("dX", ref["dhidden"]), ("dW", ref["dW"])):
         assert _rel_l2(g[k], rk) <= 1e-2, k
+
+
+@pytest.mark.parametrize("cg", [2])
+def test_lmhead_fullsize_sampled_rows(dev, cg):
+    """The LM-head bench workload at full size (8190 rows of `prod`, d = 5120, V = 152064) in
+    the launch configuration scripts/bench_lmhead.py times, checked on 12 sampled rows that
+    the oracle computes one by one: logp, lse, token scale, the dz row and the dX row."""
+    import dataclasses
+
+    from synth.gen import lmhead_inputs
+    L.grpo_async_lmhead_set_cta_group(cg)
+    b0 = make_batch("prod", 0)
+    n = int(b0.cu_seqlens[int(np.searchsorted(b0.cu_seqlens, 8192, side="right") - 1)])
+    d, V = 5120, b0.V
+    X, W = lmhead_inputs(n, V, d, 11)
+    rng = np.random.default_rng(5)
+    rows = np.sort(rng.choice(n, 12, replace=False))
+    z = O.lmhead_logits_rows(X[rows], W)
+    m = z.max(1, keepdims=True)
+    lse_rows = (m + np.log(np.exp(z - m).sum(1, keepdims=True)))[:, 0]
+    tgt = b0.target_ids[:n]
+    logp_rows = z[np.arange(len(rows)), tgt[rows]] - lse_rows
+    # test-side inputs: behaviour log-probs of the sampled rows near the oracle's own logp
+    lw = np.array(b0.logp_behav[:n], np.float32)
+    lw[rows] = (logp_rows - rng.normal(size=len(rows)) * 0.05).astype(np.float32)
+    full_lw = np.array(b0.logp_behav, np.float32)
+    full_lw[:n] = lw
+    b = dataclasses.replace(b0, logp_behav=full_lw)
+    db = G.DeviceBatch.from_host(b, dev)
+    loss = G.GrpoAsyncLoss()
+    adv, inv = loss.advantage(db)
+    Xd = to_dev_bits(X, dev).view(torch.bfloat16)
+    Wd = to_dev_bits(W, dev).view(torch.bfloat16)
+    logp = torch.empty(n, device=dev)
+    lse = torch.empty(n, device=dev)
+    scale = torch.empty(n, device=dev)
+    ts = torch.zeros(b.N, dtype=torch.float64, device=dev)
+    st = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
+    loss.lmhead_fwd(Xd, Wd, 0, n, db.target_ids[:n], db.logp_behav[:n], db.cu_seqlens, adv, inv, ts,
+                    st, logp_out=logp, lse_out=lse, scale_out=scale)
+    dz = torch.empty((n, V), dtype=torch.bfloat16, device=dev)
+    dX = torch.empty((n, d), dtype=torch.bfloat16, device=dev)
+    loss.lmhead_bwd(Xd, Wd, n, db.target_ids[:n], lse, scale, dz, dhidden=dX)
+    torch.cuda.synchronize()
+    ref_adv, ref_inv, _ = O.advantage(b.rewards, b.group_ids, b.cu_seqlens, b.P, float(np.float32(1e-8)))
+    rr = O.rows_f64(rows, z, tgt[rows], lw[rows], b.cu_seqlens, ref_adv, ref_inv, 0.2)  # row-local
+    r_idx = torch.from_numpy(rows).to(dev)
+    g_logp = logp[r_idx].cpu().numpy()
+    assert np.max(np.abs(g_logp - rr.logp)) <= 2e-3
+    assert np.max(np.abs(lse[r_idx].cpu().numpy() - rr.lse)) <= 2e-3
+    assert np.allclose(scale[r_idx].cpu().numpy(), rr.s, rtol=1e-3, atol=1e-12)
+    g_dz = dz[r_idx].float().cpu().numpy().astype(np.float64)
+    assert _rel_l2(g_dz, rr.dlogits) <= 1e-2
+    ref_dX = O.matmul_rows_W(rr.dlogits, W)
+    assert _rel_l2(dX[r_idx].float().cpu().numpy().astype(np.float64), ref_dX) <= 1e-2
+    L.grpo_async_lmhead_set_cta_group(2)

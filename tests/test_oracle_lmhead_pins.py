@@ -87,3 +87,17 @@ def test_lmhead_gradients_finite_differences(seed):
                 num[i, j] = -(Jp - Jm) / (2 * h)
         err = np.abs(num - grad).max() / max(np.abs(grad).max(), 1e-12)
         assert err < 1e-6, (which, err)
+
+
+def test_blockwise_helpers():
+    """The block-wise full-size helpers are the same definitions: lmhead_logits_rows equals
+    lmhead_logits bit for bit (each block holds the whole d-sum of its columns), and
+    matmul_rows_W of one-hot rows returns rows of W exactly."""
+    rng = np.random.default_rng(3)
+    X = f32_to_bf16_bits(rng.normal(size=(5, 24)).astype(np.float32))
+    W = f32_to_bf16_bits(rng.normal(size=(70, 24)).astype(np.float32))
+    assert np.array_equal(O.lmhead_logits_rows(X, W, block=16), O.lmhead_logits(X, W))
+    onehot = np.zeros((3, 70))
+    onehot[0, 5] = onehot[1, 69] = onehot[2, 33] = 1.0
+    got = O.matmul_rows_W(onehot, W, block=16)
+    assert np.array_equal(got, O._bf16_to_f64(W)[[5, 69, 33]])
