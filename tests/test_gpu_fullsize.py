@@ -75,3 +75,48 @@ def test_fullsize_chunk_sampled_rows(dev, name, R):
     assert abs(st[G.STAT_J]) <= st[G.STAT_ABS]
     ts = traj_sum.cpu().numpy()
     assert abs(np.sum(inv_ref * ts) - st[G.STAT_J]) <= 1e-6 * st[G.STAT_ABS]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_vocab_parallel_fullsize_sampled_rows(dev, world):
+    """NEXT(3) at the metric's size: a 65536-row chunk of `prod` (V = 152064) cut into `world`
+    column shards, all ranks in one cooperative launch (the peer-memory protocol of the
+    multi-GPU run), sampled rows against the oracle and the J invariants."""
+    R = 65536
+    b = make_batch("prod", 0, period=R)
+    V, ld = b.V, b.ld
+    lg = torch.empty((R, ld), dtype=torch.int16, device=dev)
+    SG.fill_logits(lg, b.logits, 0, R, V)
+    comm = G.VpGroup.local(world, V, R, dev)
+    sc = comm.shard_cols
+    shards = []
+    for q in range(world):
+        sh = torch.full((R, sc), 0x7FC1, dtype=torch.int16, device=dev)
+        lo, hi = q * sc, min((q + 1) * sc, V)
+        sh[:, :hi - lo] = lg[:, lo:hi]
+        shards.append(sh)
+    del lg
+    dsh = [torch.empty_like(s) for s in shards]
+    db = G.DeviceBatch.from_host(b, dev)
+    loss = G.GrpoAsyncLoss()
+    adv, inv = loss.advantage(db)
+    logp = torch.empty(R, device=dev)
+    scale = torch.empty(R, device=dev)
+    ts = torch.zeros(b.N, dtype=torch.float64, device=dev)
+    st = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
+    loss.loss_chunk_vp(comm, shards, 0, R, db.target_ids[:R], db.logp_behav[:R], db.cu_seqlens, adv,
+                       inv, ts, st, dshards=dsh, logp_out=logp, scale_out=scale, V=V)
+    torch.cuda.synchronize()
+    adv_ref, inv_ref, _ = O.advantage(b.rewards, b.group_ids, b.cu_seqlens, b.P, float(np.float32(1e-8)))
+    rows = np.sort(np.random.default_rng(world).choice(R, size=12, replace=False))
+    bits = b.logits_bits(rows)
+    rr = O.rows(rows, bits, V, b.target_ids[rows], b.logp_behav[rows], b.cu_seqlens, adv_ref,
+                inv_ref, 0.2, want_dlogits=True)
+    r_idx = torch.from_numpy(rows).to(dev)
+    assert np.max(np.abs(logp[r_idx].cpu().numpy() - rr.logp)) < 1e-4
+    got = np.concatenate([bf16_bits_to_f32(d[r_idx].cpu().numpy().view(np.uint16)) for d in dsh],
+                         axis=1)[:, :V].astype(np.float64)
+    den = np.linalg.norm(rr.dlogits)
+    assert np.linalg.norm(got - rr.dlogits) / den < 1e-2
+    s = st.cpu().numpy()
+    assert s[G.STAT_ROWS] == R and abs(s[G.STAT_J]) <= s[G.STAT_ABS]
