@@ -410,6 +410,14 @@ grpo_status_t grpo_async_lmhead_tp_bwd(const uint16_t *hidden, const uint16_t *W
                                        uint16_t *dz, int64_t ld_dz, float *dhidden_partial,
                                        float *dW_shard, grpo_stream_t stream);
 
+/* dW (+)= dz^T hidden from an existing dz (bf16 [n_rows, ld_dz], as written by
+ * grpo_async_lmhead_bwd / _tp_bwd), f32 [V, d] accumulated: lets a caller run the dW GEMM
+ * while the tensor-parallel dhidden all-reduce is in flight.  cuBLAS GEMM (bf16 in, f32 out).
+ * Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_CUDA. */
+grpo_status_t grpo_async_lmhead_dw(const uint16_t *hidden, int64_t n_rows, int32_t d, int32_t V,
+                                   const uint16_t *dz, int64_t ld_dz, float *dW,
+                                   grpo_stream_t stream);
+
 /* Tensor-core mode of the calling thread's later LM-head calls: 1 = one CTA per MMA
  * (tcgen05.mma.cta_group::1, 128 x 256 tiles), 2 = CTA pairs on one TPC (cta_group::2,
  * 256 x 256 tiles, each CTA stages half of the W tile; the default).  Same results.

@@ -37,7 +37,7 @@ EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advan
             "grpo_async_lmhead_logits", "grpo_async_lmhead_set_cta_group",
             "grpo_async_group_partials", "grpo_async_group_sq_partials",
             "grpo_async_advantage_from_stats", "grpo_async_lmhead_tp_partials",
-            "grpo_async_lmhead_tp_fwd", "grpo_async_lmhead_tp_bwd",
+            "grpo_async_lmhead_tp_fwd", "grpo_async_lmhead_tp_bwd", "grpo_async_lmhead_dw",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -137,6 +137,8 @@ def _load():
     lib.grpo_async_lmhead_tp_fwd.restype = st
     lib.grpo_async_lmhead_tp_bwd.argtypes = [P, P, i64, i32, i32, i32, P, P, P, f32, P, i64, P, P, P]
     lib.grpo_async_lmhead_tp_bwd.restype = st
+    lib.grpo_async_lmhead_dw.argtypes = [P, i64, i32, i32, P, i64, P, P]
+    lib.grpo_async_lmhead_dw.restype = st
     lib.grpo_async_lmhead_set_cta_group.argtypes = [i32]
     lib.grpo_async_lmhead_set_cta_group.restype = st
     lib.grpo_async_loss_bwd.argtypes = [P, i64, i32, i64, P, P, P, f32, P, P]
@@ -488,3 +490,8 @@ def grpo_async_lmhead_tp_bwd(hidden, W_shard, n_rows, d, Vs, col_offset, target_
         _ptr(token_scale, torch.float32, "token_scale"), float(grad_scale_mult), _bf16(dz, "dz"),
         ld_dz, _ptr(dhidden_partial, torch.float32, "dhidden_partial"),
         _ptr(dW_shard, torch.float32, "dW_shard"), _stream(stream)))
+
+
+def grpo_async_lmhead_dw(hidden, n_rows, d, V, dz, ld_dz, dW, stream=None):
+    _check(LIB.grpo_async_lmhead_dw(_bf16(hidden, "hidden"), n_rows, d, V, _bf16(dz, "dz"), ld_dz,
+                                    _ptr(dW, torch.float32, "dW"), _stream(stream)))

@@ -252,13 +252,26 @@ class GrpoAsyncLoss:
         self.launches += L.grpo_last_launch_count()
 
     def lmhead_tp_bwd(self, hidden, W_shard, col_offset, n_rows, target_ids, lse, token_scale, dz,
-                      dhidden_partial=None, dW_shard=None, mult=1.0, stream=None):
-        """dhidden_partial (float32) is this shard's dz W_shard: sum it over the ranks."""
+                      dhidden_partial=None, dW_shard=None, mult=1.0, stream=None,
+                      allreduce_async=None):
+        """dhidden_partial (float32) is this shard's dz W_shard: sum it over the ranks.  With
+        allreduce_async(t) -> handle (e.g. torch.distributed.all_reduce(t, async_op=True)) the
+        all-reduce of dhidden_partial is started right after its GEMM and overlaps the dW GEMM;
+        the handle is returned (wait() before using dhidden_partial)."""
         Vs, d = W_shard.shape
+        if allreduce_async is None:
+            L.grpo_async_lmhead_tp_bwd(hidden, W_shard, n_rows, d, Vs, col_offset, target_ids, lse,
+                                       token_scale, mult, dz, dz.shape[1], dhidden_partial,
+                                       dW_shard, stream)
+            self.launches += L.grpo_last_launch_count()
+            return None
         L.grpo_async_lmhead_tp_bwd(hidden, W_shard, n_rows, d, Vs, col_offset, target_ids, lse,
-                                   token_scale, mult, dz, dz.shape[1], dhidden_partial, dW_shard,
-                                   stream)
+                                   token_scale, mult, dz, dz.shape[1], dhidden_partial, None, stream)
         self.launches += L.grpo_last_launch_count()
+        handle = allreduce_async(dhidden_partial)
+        if dW_shard is not None:
+            L.grpo_async_lmhead_dw(hidden, n_rows, d, Vs, dz, dz.shape[1], dW_shard, stream)
+        return handle
 
     # ---- fused loss over vocabulary-parallel logits (SURVEY NEXT(3), P:282)
     def loss_chunk_vp(self, comm, shards, row_begin, n_rows, target_ids, logp_behav, cu_seqlens,

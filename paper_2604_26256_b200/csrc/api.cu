@@ -828,6 +828,26 @@ grpo_status_t grpo_async_lmhead_tp_bwd(const uint16_t *hidden, const uint16_t *W
     return ok(launches);
 }
 
+grpo_status_t grpo_async_lmhead_dw(const uint16_t *hidden, int64_t n_rows, int32_t d, int32_t V,
+                                   const uint16_t *dz, int64_t ld_dz, float *dW,
+                                   grpo_stream_t stream) {
+    if (n_rows < 0 || V <= 0 || d <= 0 || n_rows > INT32_MAX)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_dw: n_rows/V/d");
+    if (n_rows > 0 && (!hidden || !dz || !dW)) return fail(GRPO_ERR_INVALID_ARG, "lmhead_dw: NULL pointer");
+    if (ld_dz < V || ld_dz % 8 != 0) return fail(GRPO_ERR_ALIGNMENT, "lmhead_dw: ld_dz=%lld", (long long)ld_dz);
+    if (n_rows == 0) return ok(0);
+    cublasHandle_t h = cublas_handle();
+    if (!h) return fail(GRPO_ERR_CUDA, "lmhead_dw: cublasCreate failed");
+    if (cublasSetStream(h, (cudaStream_t)stream) != CUBLAS_STATUS_SUCCESS)
+        return fail(GRPO_ERR_CUDA, "lmhead_dw: cublasSetStream");
+    const float one = 1.0f;
+    cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, d, V, (int)n_rows, &one, hidden, CUDA_R_16BF,
+                                     d, dz, CUDA_R_16BF, (int)ld_dz, &one, dW, CUDA_R_32F, d,
+                                     CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_dw: GEMM status %d", (int)cs);
+    return ok(0);
+}
+
 grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
                                        int32_t d, int32_t V, uint16_t *out, int64_t ld_out,
                                        grpo_stream_t stream) {

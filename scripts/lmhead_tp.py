@@ -22,7 +22,7 @@ import paper_2604_26256_b200 as G  # noqa: E402
 from synth.gen import make_batch  # noqa: E402
 
 
-def run(loss, db, X, W, V, R0, n, rank, world, lw=None):
+def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False):
     d = X.shape[1]
     Vs = -(-V // world)
     off = rank * Vs
@@ -41,9 +41,15 @@ def run(loss, db, X, W, V, R0, n, rank, world, lw=None):
     dz = torch.empty((n, (Vq + 7) // 8 * 8), dtype=torch.bfloat16, device=X.device)
     dX = torch.empty((n, d), dtype=torch.float32, device=X.device)
     dW = torch.zeros((Vq, d), dtype=torch.float32, device=X.device)
-    loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz, dhidden_partial=dX,
-                       dW_shard=dW)
-    dist.all_reduce(dX)
+    if overlap:  # the dhidden all-reduce overlaps the dW GEMM
+        h = loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz,
+                               dhidden_partial=dX, dW_shard=dW,
+                               allreduce_async=lambda t: dist.all_reduce(t, async_op=True))
+        h.wait()
+    else:
+        loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz,
+                           dhidden_partial=dX, dW_shard=dW)
+        dist.all_reduce(dX)
     return logp, st, dX, dW, dz
 
 
@@ -86,23 +92,26 @@ def main():
     dbb = G.DeviceBatch.from_host(bb, dev)
     loss = G.GrpoAsyncLoss()
 
-    def step():
-        run(loss, dbb, Xt, Wq, V, 0, n, rank, world)
+    def timed(overlap):
+        for _ in range(2):
+            run(loss, dbb, Xt, Wq, V, 0, n, rank, world, overlap=overlap)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            run(loss, dbb, Xt, Wq, V, 0, n, rank, world, overlap=overlap)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = torch.tensor([e0.elapsed_time(e1) / 5], device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
 
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize(dev)
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(5):
-        step()
-    e1.record()
-    torch.cuda.synchronize(dev)
-    ms = torch.tensor([e0.elapsed_time(e1) / 5], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    out["timing"] = {"rows": n, "d": d, "V": V, "shard_cols": Vs, "ms_fwd_bwd_step": float(ms.item()),
-                     "tflops_per_gpu": 8.0 * n * Vs * d / float(ms.item()) / 1e9}
+    ms_seq = timed(False)
+    ms = timed(True)
+    out["timing"] = {"rows": n, "d": d, "V": V, "shard_cols": Vs, "ms_fwd_bwd_step": ms,
+                     "ms_fwd_bwd_step_no_overlap": ms_seq,
+                     "tflops_per_gpu": 8.0 * n * Vs * d / ms / 1e9}
     if rank == 0:
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()
