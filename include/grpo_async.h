@@ -410,6 +410,27 @@ grpo_status_t grpo_async_lmhead_tp_bwd(const uint16_t *hidden, const uint16_t *W
                                        uint16_t *dz, int64_t ld_dz, float *dhidden_partial,
                                        float *dW_shard, grpo_stream_t stream);
 
+/*
+ * The tensor-parallel dhidden as one kernel that computes and communicates (GEMM ->
+ * reduce-scatter over NVLink peer memory): rank `rank` of `world` multiplies its dz shard
+ * (bf16 [n_rows, ld_dz], columns [0, Vs)) by its W shard (bf16 [Vs, d]) on the tensor cores
+ * and its epilogue stores each f32 tile of rows r into slot `rank` of the rank that owns r
+ * (rows_per_rank = ceil(n_rows / world); rank q owns rows [q*rpr, (q+1)*rpr)).
+ *   slots[q]  device pointer (peer mapping) of rank q's slot buffer, f32
+ *             [world][rows_per_rank][d], for q < world (host array of world pointers)
+ * After every rank's grpo_async_lmhead_tp_dx has completed (a group barrier, e.g. a NCCL
+ * collective on the same stream), grpo_async_lmhead_tp_dx_reduce sums this rank's world slots
+ * in rank order into out [rows owned, d] (f32, or bf16 with out_bf16 = 1): deterministic.
+ * d % 128 == 0, world <= GRPO_VP_MAX_RANKS.  Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT,
+ * GRPO_ERR_CUDA.
+ */
+grpo_status_t grpo_async_lmhead_tp_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W_shard,
+                                      int64_t n_rows, int32_t d, int32_t Vs, int32_t world,
+                                      int32_t rank, float *const *slots, grpo_stream_t stream);
+grpo_status_t grpo_async_lmhead_tp_dx_reduce(const float *own_slots, int32_t world, int64_t n_rows,
+                                             int32_t d, int32_t rank, void *out, int32_t out_bf16,
+                                             grpo_stream_t stream);
+
 /* dW (+)= dz^T hidden from an existing dz (bf16 [n_rows, ld_dz], as written by
  * grpo_async_lmhead_bwd / _tp_bwd), f32 [V, d] accumulated: lets a caller run the dW GEMM
  * while the tensor-parallel dhidden all-reduce is in flight.  cuBLAS GEMM (bf16 in, f32 out).

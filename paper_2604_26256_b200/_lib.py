@@ -38,6 +38,7 @@ EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advan
             "grpo_async_group_partials", "grpo_async_group_sq_partials",
             "grpo_async_advantage_from_stats", "grpo_async_lmhead_tp_partials",
             "grpo_async_lmhead_tp_fwd", "grpo_async_lmhead_tp_bwd", "grpo_async_lmhead_dw",
+            "grpo_async_lmhead_tp_dx", "grpo_async_lmhead_tp_dx_reduce",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -137,6 +138,10 @@ def _load():
     lib.grpo_async_lmhead_tp_fwd.restype = st
     lib.grpo_async_lmhead_tp_bwd.argtypes = [P, P, i64, i32, i32, i32, P, P, P, f32, P, i64, P, P, P]
     lib.grpo_async_lmhead_tp_bwd.restype = st
+    lib.grpo_async_lmhead_tp_dx.argtypes = [P, i64, P, i64, i32, i32, i32, i32, P, P]
+    lib.grpo_async_lmhead_tp_dx.restype = st
+    lib.grpo_async_lmhead_tp_dx_reduce.argtypes = [P, i32, i64, i32, i32, P, i32, P]
+    lib.grpo_async_lmhead_tp_dx_reduce.restype = st
     lib.grpo_async_lmhead_dw.argtypes = [P, i64, i32, i32, P, i64, P, P]
     lib.grpo_async_lmhead_dw.restype = st
     lib.grpo_async_lmhead_set_cta_group.argtypes = [i32]
@@ -495,3 +500,17 @@ def grpo_async_lmhead_tp_bwd(hidden, W_shard, n_rows, d, Vs, col_offset, target_
 def grpo_async_lmhead_dw(hidden, n_rows, d, V, dz, ld_dz, dW, stream=None):
     _check(LIB.grpo_async_lmhead_dw(_bf16(hidden, "hidden"), n_rows, d, V, _bf16(dz, "dz"), ld_dz,
                                     _ptr(dW, torch.float32, "dW"), _stream(stream)))
+
+
+def grpo_async_lmhead_tp_dx(dz, ld_dz, W_shard, n_rows, d, Vs, world, rank, slots, stream=None):
+    """slots: `world` device addresses (ints or float32 tensors) of every rank's slot buffer."""
+    arr = (C.c_void_p * world)(*[_addr(x, "slots") for x in slots])
+    _check(LIB.grpo_async_lmhead_tp_dx(_bf16(dz, "dz"), ld_dz, _bf16(W_shard, "W_shard"), n_rows, d,
+                                       Vs, world, rank, arr, _stream(stream)))
+
+
+def grpo_async_lmhead_tp_dx_reduce(own_slots, world, n_rows, d, rank, out, stream=None):
+    out_bf16 = 1 if out.element_size() == 2 else 0
+    _check(LIB.grpo_async_lmhead_tp_dx_reduce(_ptr(own_slots, torch.float32, "own_slots"), world,
+                                              n_rows, d, rank, _ptr(out, None, "out"), out_bf16,
+                                              _stream(stream)))

@@ -848,6 +848,41 @@ grpo_status_t grpo_async_lmhead_dw(const uint16_t *hidden, int64_t n_rows, int32
     return ok(0);
 }
 
+grpo_status_t grpo_async_lmhead_tp_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W_shard,
+                                      int64_t n_rows, int32_t d, int32_t Vs, int32_t world,
+                                      int32_t rank, float *const *slots, grpo_stream_t stream) {
+    if (n_rows < 0 || n_rows > INT32_MAX || Vs <= 0 || d < 128 || d % 128 != 0)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx: n_rows=%lld d=%d Vs=%d (d a multiple of 128)",
+                    (long long)n_rows, d, Vs);
+    if (world < 1 || world > GRPO_VP_MAX_RANKS || rank < 0 || rank >= world || !slots)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx: world=%d rank=%d", world, rank);
+    for (int q = 0; q < world; ++q)
+        if (!slots[q] || !aligned16(slots[q])) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx: slots[%d]", q);
+    if (n_rows > 0 && (!dz || !W_shard)) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx: NULL dz/W_shard");
+    if (ld_dz < Vs || ld_dz % 8 != 0 || (dz && !aligned16(dz)) || (W_shard && !aligned16(W_shard)))
+        return fail(GRPO_ERR_ALIGNMENT, "lmhead_tp_dx: ld_dz=%lld (>= Vs, multiple of 8), 16-byte aligned",
+                    (long long)ld_dz);
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_lmhead_dx(dz, ld_dz, W_shard, n_rows, d, Vs, world, rank, slots,
+                                           (cudaStream_t)stream, &launches, why, sizeof why);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_dx", why);
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_lmhead_tp_dx_reduce(const float *own_slots, int32_t world, int64_t n_rows,
+                                             int32_t d, int32_t rank, void *out, int32_t out_bf16,
+                                             grpo_stream_t stream) {
+    if (n_rows < 0 || d < 4 || d % 4 != 0 || world < 1 || world > GRPO_VP_MAX_RANKS || rank < 0 || rank >= world)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx_reduce: n_rows/d/world/rank");
+    if (n_rows > 0 && (!own_slots || !out)) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx_reduce: NULL");
+    int launches = 0;
+    cudaError_t e = grpo::launch_lmhead_dx_reduce(own_slots, world, n_rows, d, rank, out, out_bf16,
+                                                  (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_dx_reduce");
+    return ok(launches);
+}
+
 grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W, int64_t n_rows,
                                        int32_t d, int32_t V, uint16_t *out, int64_t ld_out,
                                        grpo_stream_t stream) {

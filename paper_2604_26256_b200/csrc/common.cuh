@@ -433,6 +433,11 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
 cudaError_t launch_lmhead_rowpart(const float2 *part, const float *zy, int32_t n_split, int64_t n_rows,
                                   const int64_t *targets, int32_t col_offset, int32_t Vs, float4 *out,
                                   cudaStream_t s, int *launches);
+cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W, int64_t n_rows, int32_t d,
+                             int32_t Vs, int32_t world, int32_t rank, float *const *slots, cudaStream_t s,
+                             int *launches, char *why, size_t why_len);
+cudaError_t launch_lmhead_dx_reduce(const float *own_slots, int32_t world, int64_t n_rows, int32_t d,
+                                    int32_t rank, void *out, int out_bf16, cudaStream_t s, int *launches);
 cudaError_t launch_lmhead_tp_combine(const float4 *parts, int32_t R, const LossArgs &a, cudaStream_t s,
                                      int *launches);
 cudaError_t launch_lmhead_combine(const float2 *part, const float *zy, int32_t n_split, const LossArgs &a,

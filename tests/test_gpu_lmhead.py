@@ -249,3 +249,52 @@ def test_lmhead_fullsize_sampled_rows(dev, cg):
     ref_dX = O.matmul_rows_W(rr.dlogits, W)
     assert _rel_l2(dX[r_idx].float().cpu().numpy().astype(np.float64), ref_dX) <= 1e-2
     L.grpo_async_lmhead_set_cta_group(2)
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4])
+@pytest.mark.parametrize("name,d", [("ragged", 128), ("mid32k", 256)])
+def test_lmhead_tp_dx_gemm_reduce_scatter(dev, name, d, R):
+    """grpo_async_lmhead_tp_dx: dz_q W_q on the tensor cores (B read MN-major from the
+    row-major W shard) with the f32 tiles stored straight into the owner rank's slot; then
+    the owner's rank-order sum.  R ranks emulated on one GPU (the slot buffers are local).
+    Against the oracle's dhidden and against the cuBLAS partials summed."""
+    b, X, W = lmhead_batch(name, 9, d)
+    ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
+    T, V = b.T, b.V
+    Vs = -(-V // R)
+    db = G.DeviceBatch.from_host(b, dev)
+    loss = G.GrpoAsyncLoss()
+    adv, inv = loss.advantage(db)
+    Xd = to_dev_bits(X, dev).view(torch.bfloat16)
+    Wd = to_dev_bits(W, dev).view(torch.bfloat16)
+    lse = torch.empty(T, device=dev)
+    scale = torch.empty(T, device=dev)
+    ts = torch.zeros(b.N, dtype=torch.float64, device=dev)
+    st = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
+    loss.lmhead_fwd(Xd, Wd, 0, T, db.target_ids, db.logp_behav, db.cu_seqlens, adv, inv, ts, st,
+                    lse_out=lse, scale_out=scale)
+    rpr = -(-T // R)
+    bufs = [torch.full((R, rpr, d), float("nan"), device=dev) for _ in range(R)]
+    cublas_sum = torch.zeros((T, d), device=dev)
+    for q in range(R):
+        off = q * Vs
+        Wq = Wd[off:min(off + Vs, V)].contiguous()
+        Vq = Wq.shape[0]
+        ld = (Vq + 7) // 8 * 8
+        dz = torch.zeros((T, ld), dtype=torch.bfloat16, device=dev)
+        part = torch.empty((T, d), device=dev)
+        loss.lmhead_tp_bwd(Xd, Wq, off, T, db.target_ids, lse, scale, dz, dhidden_partial=part)
+        cublas_sum += part
+        L.grpo_async_lmhead_tp_dx(dz, ld, Wq, T, d, Vq, R, q, bufs)
+    outs = []
+    for q in range(R):
+        rows = max(0, min(rpr, T - q * rpr))
+        o = torch.empty((max(rows, 1), d), device=dev)
+        L.grpo_async_lmhead_tp_dx_reduce(bufs[q], R, T, d, q, o)
+        outs.append(o[:rows])
+    torch.cuda.synchronize()
+    dX = torch.cat(outs).cpu().numpy().astype(np.float64)
+    assert dX.shape == (T, d) and np.isfinite(dX).all()
+    assert _rel_l2(dX, ref["dhidden"]) <= 1e-2
+    # two f32 GEMMs summing ~V products in different orders
+    assert _rel_l2(dX, cublas_sum.cpu().numpy().astype(np.float64)) <= 1e-3
