@@ -22,7 +22,19 @@ import paper_2604_26256_b200 as G  # noqa: E402
 from synth.gen import make_batch  # noqa: E402
 
 
-def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False):
+class FusedDX:
+    """Slot buffers for grpo_async_lmhead_tp_dx in torch symmetric memory (peer pointers)."""
+
+    def __init__(self, n, d, world, dev):
+        import torch.distributed._symmetric_memory as symm
+        self.rpr = -(-n // world)
+        self.buf = symm.empty(world * self.rpr * d, dtype=torch.float32, device=dev)
+        self.h = symm.rendezvous(self.buf, dist.group.WORLD)
+        self.ptrs = [self.h.get_buffer(q, (world * self.rpr * d,), torch.float32).data_ptr()
+                     for q in range(world)]
+
+
+def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False, fused=None):
     d = X.shape[1]
     Vs = -(-V // world)
     off = rank * Vs
@@ -41,6 +53,16 @@ def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False):
     dz = torch.empty((n, (Vq + 7) // 8 * 8), dtype=torch.bfloat16, device=X.device)
     dX = torch.empty((n, d), dtype=torch.float32, device=X.device)
     dW = torch.zeros((Vq, d), dtype=torch.float32, device=X.device)
+    if fused is not None:  # one GEMM -> reduce-scatter kernel over peer memory, then dW
+        from paper_2604_26256_b200 import _lib as L
+        loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz)
+        L.grpo_async_lmhead_tp_dx(dz, dz.shape[1], Wq, n, d, Vq, world, rank, fused.ptrs)
+        L.grpo_async_lmhead_dw(X, n, d, Vq, dz, dz.shape[1], dW)
+        dist.barrier()  # every rank's tiles have landed in their owners' slots
+        rows = max(0, min(fused.rpr, n - rank * fused.rpr))
+        mine = torch.empty((max(rows, 1), d), dtype=torch.float32, device=X.device)
+        L.grpo_async_lmhead_tp_dx_reduce(fused.buf, world, n, d, rank, mine)
+        return logp, st, mine[:rows], dW, dz
     if overlap:  # the dhidden all-reduce overlaps the dW GEMM
         h = loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz,
                                dhidden_partial=dX, dW_shard=dW,
@@ -92,25 +114,37 @@ def main():
     dbb = G.DeviceBatch.from_host(bb, dev)
     loss = G.GrpoAsyncLoss()
 
-    def timed(overlap):
+    fused = FusedDX(n, d, world, dev)
+    # the fused dhidden (this rank's rows) against the NCCL all-reduce path
+    _, _, dx_ref, _, _ = run(loss, dbb, Xt, Wq, V, 0, n, rank, world)
+    _, _, dx_f, _, _ = run(loss, dbb, Xt, Wq, V, 0, n, rank, world, fused=fused)
+    r0 = rank * fused.rpr
+    rel = (torch.linalg.norm(dx_f - dx_ref[r0:r0 + dx_f.shape[0]]) /
+           torch.linalg.norm(dx_ref[r0:r0 + dx_f.shape[0]])).reshape(1)
+    dist.all_reduce(rel, op=dist.ReduceOp.MAX)
+    out["fused_dx_vs_nccl_rel_l2"] = float(rel.item())
+
+    def timed(overlap, fz=None):
         for _ in range(2):
-            run(loss, dbb, Xt, Wq, V, 0, n, rank, world, overlap=overlap)
+            run(loss, dbb, Xt, Wq, V, 0, n, rank, world, overlap=overlap, fused=fz)
         torch.cuda.synchronize(dev)
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(5):
-            run(loss, dbb, Xt, Wq, V, 0, n, rank, world, overlap=overlap)
+            run(loss, dbb, Xt, Wq, V, 0, n, rank, world, overlap=overlap, fused=fz)
         e1.record()
         torch.cuda.synchronize(dev)
         ms = torch.tensor([e0.elapsed_time(e1) / 5], device=dev)
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
-    ms_seq = timed(False)
-    ms = timed(True)
+    ms = timed(False)
+    ms_ovl = timed(True)
+    ms_fused = timed(False, fused)
     out["timing"] = {"rows": n, "d": d, "V": V, "shard_cols": Vs, "ms_fwd_bwd_step": ms,
-                     "ms_fwd_bwd_step_no_overlap": ms_seq,
+                     "ms_fwd_bwd_step_allreduce_overlap_dw": ms_ovl,
+                     "ms_fwd_bwd_step_fused_dx_reduce_scatter": ms_fused,
                      "tflops_per_gpu": 8.0 * n * Vs * d / ms / 1e9}
     if rank == 0:
         print(json.dumps(out), flush=True)
