@@ -27,6 +27,20 @@ struct Params {
     float *slots[GRPO_VP_MAX_RANKS];  // slot buffers of every rank: [world][rows_per_rank][d]
 };
 
+// Units (m_tile, n_tile) rastered in groups of GM row tiles (row tile fastest): the pairs
+// running at the same time cover ~GM row tiles x ~grid/GM column tiles and, moving through
+// K at about the same pace, share each A and B k-block in L2 instead of re-reading dz
+// (K = the shard's vocabulary, tens of MB per row tile) from HBM.
+constexpr int GM = 8;
+__device__ __forceinline__ void dx_decode(const Params &p, int unit, int &m_tile, int &n_tile) {
+    const int per_group = GM * p.n_tiles;
+    const int grp = unit / per_group;
+    const int rem = unit - grp * per_group;
+    const int gm = min(GM, p.m_tiles - grp * GM);
+    m_tile = grp * GM + rem % gm;
+    n_tile = rem / gm;
+}
+
 // Shared-memory matrix descriptor, MN-major, 128-byte swizzle: 64-element rows along N,
 // 8 K-rows per 1 KB atom (SBO = 1024 B between K atoms), N atoms of 64 elements LBO apart.
 __device__ __forceinline__ uint64_t desc_mn_sw128(const void *smem_tile, uint32_t lbo_bytes) {
@@ -40,39 +54,49 @@ __host__ __device__ constexpr uint32_t idesc_kmn(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int BN>
+// CG = 2: a CTA pair (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each CTA stages
+// its own 128 rows of dz and half of the tile's BN columns of W; the leader issues the MMA.
+template <int BN, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dx_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
     constexpr int A_BYTES = BM * BK * 2;          // 16 KB
-    constexpr int NB = BN / 64;                   // 64-wide N atoms per tile
+    constexpr int NB = BN / 64 / CG;              // 64-wide N atoms staged per CTA
     constexpr int B_ATOM = BK * 64 * 2;           // 8 KB: 64 K-rows x 64 N elements
     constexpr int STAGE = A_BYTES + NB * B_ATOM;
+    constexpr int NS = CG == 1 ? STAGES : 6;
     constexpr uint32_t TMEM_COLS = 2 * BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sA = smem, *sB = smem + STAGES * A_BYTES;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE);
-    uint64_t *full = bars, *empty = bars + STAGES, *tfull = bars + 2 * STAGES, *tempty = bars + 2 * STAGES + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+    uint8_t *sA = smem, *sB = smem + NS * A_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * STAGE);
+    uint64_t *full = bars, *empty = bars + NS, *tfull = bars + 2 * NS, *tempty = bars + 2 * NS + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (p.Vs + BK - 1) / BK;
+    const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
+    const int cta_id = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
+    const int n_ctas = CG == 2 ? (int)ncluster_x() : (int)gridDim.x;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
-            mbar_init(tempty + a, 128);
+            mbar_init(tempty + a, 128 * CG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tc::prefetch_tmap(&tmA);
         tc::prefetch_tmap(&tmB);
     }
-    if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+    if (warp == 1) {
+        if (CG == 2) tc::tmem_alloc2(tmem_slot, TMEM_COLS);
+        else tc::tmem_alloc(tmem_slot, TMEM_COLS);
+    }
     tc::fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync_all();
     tc::fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -81,17 +105,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t pol = policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
-                const int m_tile = unit % p.m_tiles, n_tile = unit / p.m_tiles;
+            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+                int m_tile, n_tile;
+                dx_decode(p, unit, m_tile, n_tile);
+                const int a_row = m_tile * BM * CG + (int)crank * BM;
+                const int b_col = n_tile * BN + (int)crank * (BN / CG);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1u);
-                    mbar_arrive_expect_tx(full + stage, STAGE);
-                    tc::tma_load_2d(sA + stage * A_BYTES, &tmA, kb * BK, m_tile * BM, full + stage, pol);
+                    if (CG == 1) {
+                        mbar_arrive_expect_tx(full + stage, STAGE);
+                        tc::tma_load_2d(sA + stage * A_BYTES, &tmA, kb * BK, a_row, full + stage, pol);
 #pragma unroll
-                    for (int j = 0; j < NB; ++j)  // 64 vocabulary rows x 64 columns of W each
-                        tc::tma_load_2d(sB + stage * NB * B_ATOM + j * B_ATOM, &tmB, n_tile * BN + j * 64, kb * BK,
-                                        full + stage, pol);
-                    if (++stage == STAGES) {
+                        for (int j = 0; j < NB; ++j)
+                            tc::tma_load_2d(sB + stage * NB * B_ATOM + j * B_ATOM, &tmB, b_col + j * 64, kb * BK,
+                                            full + stage, pol);
+                    } else {
+                        if (crank == 0) mbar_arrive_expect_tx(full + stage, 2 * STAGE);
+                        tc::tma_load_2d_pair(sA + stage * A_BYTES, &tmA, kb * BK, a_row, full + stage, pol);
+#pragma unroll
+                        for (int j = 0; j < NB; ++j)
+                            tc::tma_load_2d_pair(sB + stage * NB * B_ATOM + j * B_ATOM, &tmB, b_col + j * 64,
+                                                 kb * BK, full + stage, pol);
+                    }
+                    if (++stage == NS) {
                         stage = 0;
                         phase ^= 1u;
                     }
@@ -99,11 +135,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer
-            constexpr uint32_t idesc = idesc_kmn(BM, BN);
+        if (lane == 0 && crank == 0) {  // ---- MMA issuer (the pair's leader)
+            constexpr uint32_t idesc = idesc_kmn(BM * CG, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
+            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
                 mbar_wait(tempty + acc, acc_phase ^ 1u);
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -113,15 +149,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const uint64_t ad = tc::desc_k_sw128(sA + stage * A_BYTES);
                     const uint64_t bd = desc_mn_sw128(sB + stage * NB * B_ATOM, B_ATOM);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)  // A: +32 B inside its atom; B: +16 K-rows = 2 KB
-                        tc::mma_bf16(d_tmem, ad + 2u * k, bd + 128u * k, idesc, (kb | k) != 0);
-                    tc::commit(empty + stage);
-                    if (++stage == STAGES) {
+                    for (int k = 0; k < BK / 16; ++k) {  // A: +32 B inside its atom; B: +16 K-rows = 2 KB
+                        if (CG == 1) tc::mma_bf16(d_tmem, ad + 2u * k, bd + 128u * k, idesc, (kb | k) != 0);
+                        else tc::mma2_bf16(d_tmem, ad + 2u * k, bd + 128u * k, idesc, (kb | k) != 0);
+                    }
+                    if (CG == 1) tc::commit(empty + stage);
+                    else tc::commit2_multicast(empty + stage, 0x3);
+                    if (++stage == NS) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                tc::commit(tfull + acc);
+                if (CG == 1) tc::commit(tfull + acc);
+                else tc::commit2_multicast(tfull + acc, 0x3);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1u;
             }
@@ -131,9 +171,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int r_in_tile = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int unit = blockIdx.x; unit < p.n_units; unit += gridDim.x) {
-            const int m_tile = unit % p.m_tiles, n_tile = unit / p.m_tiles;
-            const int row = m_tile * BM + r_in_tile;
+        for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+            int m_tile, n_tile;
+            dx_decode(p, unit, m_tile, n_tile);
+            const int row = m_tile * BM * CG + (int)crank * BM + r_in_tile;
             mbar_wait(tfull + acc, acc_phase);
             tc::fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
@@ -154,14 +195,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
             }
             tc::fence_before();
-            mbar_arrive(tempty + acc);
+            if (CG == 1) mbar_arrive(tempty + acc);
+            else tc::mbar_arrive_remote(tempty + acc, 0);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1u;
         }
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2) cluster_sync_all();
+    if (warp == 1) {
+        if (CG == 2) tc::tmem_dealloc2(tmem_base, TMEM_COLS);
+        else tc::tmem_dealloc(tmem_base, TMEM_COLS);
+    }
 }
 
 // this rank's rows: the world slots summed in rank order (f32 -> out type)
@@ -222,6 +268,7 @@ cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *
     using namespace lmdx;
     if (n_rows == 0) return cudaSuccess;
     const int BN = d % 256 == 0 ? 256 : 128;
+    const int CG = 2;  // CTA pairs (tcgen05.mma.cta_group::2), as the LM-head kernel
     CUtensorMap ma, mb;
     if (!make_map(&ma, dz, n_rows, Vs, ld_dz, BM) || !make_map(&mb, W, Vs, d, d, BK)) {
         if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
@@ -231,7 +278,7 @@ cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *
     p.n_rows = (int32_t)n_rows;
     p.d = d;
     p.Vs = Vs;
-    p.m_tiles = (int32_t)((n_rows + BM - 1) / BM);
+    p.m_tiles = (int32_t)((n_rows + BM * CG - 1) / (BM * CG));
     p.n_tiles = d / BN;
     p.n_units = p.m_tiles * p.n_tiles;
     p.world = world;
@@ -241,19 +288,33 @@ cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(p.n_units, n_sm);
+    const int groups = std::min(p.n_units, n_sm / CG);
     cudaError_t e;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(groups * CG));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (BN == 256) {
-        constexpr int SMEM = STAGES * (BM * BK * 2 + 4 * BK * 64 * 2) + 1024 + 256;
-        e = cudaFuncSetAttribute(dx_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        constexpr int SMEM = 6 * (BM * BK * 2 + 2 * BK * 64 * 2) + 1024 + 256;
+        cfg.dynamicSmemBytes = SMEM;
+        e = cudaFuncSetAttribute(dx_kernel<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         if (e != cudaSuccess) return e;
-        dx_kernel<256><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, p);
+        e = cudaLaunchKernelEx(&cfg, dx_kernel<256, 2>, ma, mb, p);
     } else {
-        constexpr int SMEM = STAGES * (BM * BK * 2 + 2 * BK * 64 * 2) + 1024 + 256;
-        e = cudaFuncSetAttribute(dx_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        constexpr int SMEM = 6 * (BM * BK * 2 + 1 * BK * 64 * 2) + 1024 + 256;
+        cfg.dynamicSmemBytes = SMEM;
+        e = cudaFuncSetAttribute(dx_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         if (e != cudaSuccess) return e;
-        dx_kernel<128><<<grid, NUM_THREADS, SMEM, s>>>(ma, mb, p);
+        e = cudaLaunchKernelEx(&cfg, dx_kernel<128, 2>, ma, mb, p);
     }
+    if (e != cudaSuccess) return e;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     *launches += 1;

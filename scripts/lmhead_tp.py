@@ -22,6 +22,11 @@ import paper_2604_26256_b200 as G  # noqa: E402
 from synth.gen import make_batch  # noqa: E402
 
 
+from paper_2604_26256_b200 import _lib as L_  # noqa: E402
+
+TIMERS = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+
+
 class FusedDX:
     """Slot buffers for grpo_async_lmhead_tp_dx in torch symmetric memory (peer pointers)."""
 
@@ -32,6 +37,7 @@ class FusedDX:
         self.h = symm.rendezvous(self.buf, dist.group.WORLD)
         self.ptrs = [self.h.get_buffer(q, (world * self.rpr * d,), torch.float32).data_ptr()
                      for q in range(world)]
+        self.flag = torch.zeros(1, device=dev)
 
 
 def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False, fused=None):
@@ -55,13 +61,22 @@ def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False, fused=Non
     dW = torch.zeros((Vq, d), dtype=torch.float32, device=X.device)
     if fused is not None:  # one GEMM -> reduce-scatter kernel over peer memory, then dW
         from paper_2604_26256_b200 import _lib as L
+        tm = TIMERS
+        tm[0].record()
         loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz)
+        tm[1].record()
         L.grpo_async_lmhead_tp_dx(dz, dz.shape[1], Wq, n, d, Vq, world, rank, fused.ptrs)
+        tm[2].record()
         L.grpo_async_lmhead_dw(X, n, d, Vq, dz, dz.shape[1], dW)
-        dist.barrier()  # every rank's tiles have landed in their owners' slots
+        tm[3].record()
+        # every rank's tiles have landed in their owners' slots: a 1-element all-reduce is
+        # stream-ordered after the GEMM (dist.barrier() would synchronize the host)
+        dist.all_reduce(fused.flag)
+        tm[4].record()
         rows = max(0, min(fused.rpr, n - rank * fused.rpr))
         mine = torch.empty((max(rows, 1), d), dtype=torch.float32, device=X.device)
         L.grpo_async_lmhead_tp_dx_reduce(fused.buf, world, n, d, rank, mine)
+        tm[5].record()
         return logp, st, mine[:rows], dW, dz
     if overlap:  # the dhidden all-reduce overlaps the dW GEMM
         h = loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz,
@@ -142,6 +157,12 @@ def main():
     ms = timed(False)
     ms_ovl = timed(True)
     ms_fused = timed(False, fused)
+    torch.cuda.synchronize(dev)
+    out["ms_fused_path_parts"] = {"dz": TIMERS[0].elapsed_time(TIMERS[1]),
+                                  "dx_gemm_reduce_scatter": TIMERS[1].elapsed_time(TIMERS[2]),
+                                  "cublas_dW": TIMERS[2].elapsed_time(TIMERS[3]),
+                                  "flag_allreduce": TIMERS[3].elapsed_time(TIMERS[4]),
+                                  "slot_sum": TIMERS[4].elapsed_time(TIMERS[5])}
     out["timing"] = {"rows": n, "d": d, "V": V, "shard_cols": Vs, "ms_fwd_bwd_step": ms,
                      "ms_fwd_bwd_step_allreduce_overlap_dw": ms_ovl,
                      "ms_fwd_bwd_step_fused_dx_reduce_scatter": ms_fused,
