@@ -310,3 +310,14 @@ def test_inplace_auto_plan_long_rows(dev, name):
     ref = run_oracle(b, bits)
     gpu = run_gpu(b, bits, dev, inplace=True, chunks=2)
     compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+
+
+@pytest.mark.parametrize("name", ["mid152k", "ragged", "large_small"])
+def test_run_to_run_bitwise_determinism(dev, name):
+    """Every reduction has a fixed order (per-thread partials, fixed block/warp trees, fp64
+    segment sums in row order): two runs give identical bits for every output."""
+    b, bits = _case(name, 11)
+    g1 = run_gpu(b, bits, dev, chunks=3)
+    g2 = run_gpu(b, bits, dev, chunks=3)
+    for k in ("adv", "inv_norm", "logp", "lse", "scale", "traj_sum", "stats", "dlogits_raw"):
+        assert np.array_equal(g1[k], g2[k], equal_nan=True), k
