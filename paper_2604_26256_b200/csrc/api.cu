@@ -77,6 +77,45 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
+// The fields every fused-loss entry shares, and the chunk's scratch carved from the caller's
+// workspace in the layout grpo_async_workspace_size sizes (row info, term / logp / flag per
+// row, 5 doubles per trajectory).  Returns the first byte past that carve-up.
+uint8_t *fill_loss_args(grpo::LossArgs &a, int64_t row_begin, int64_t n_rows, int32_t V,
+                        const int64_t *target_ids, const float *logp_behav, const int64_t *cu_seqlens,
+                        int32_t N, const int32_t *traj_index, const float *adv, const float *inv_norm,
+                        float eps_lo, float eps_hi, float grad_scale, float *logp_out, float *lse_out,
+                        float *token_scale_out, double *traj_sum, double *stats, void *workspace) {
+    a.V = V;
+    a.row_begin = row_begin;
+    a.n_rows = n_rows;
+    a.target_ids = target_ids;
+    a.logp_behav = logp_behav;
+    a.cu_seqlens = cu_seqlens;
+    a.N = N;
+    a.traj_index = traj_index;
+    a.adv = adv;
+    a.inv_norm = inv_norm;
+    a.eps_lo = eps_lo;
+    a.eps_hi = eps_hi;
+    a.grad_scale = grad_scale;
+    a.logp_out = logp_out;
+    a.lse_out = lse_out;
+    a.scale_out = token_scale_out;
+    a.traj_sum = traj_sum;
+    a.stats = stats;
+    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
+    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
+    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
+    a.term_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.logp_ws = reinterpret_cast<float *>(w);
+    w += align256((size_t)n_rows * 4);
+    a.flag_ws = w;
+    w += align256((size_t)n_rows);
+    a.part_ws = reinterpret_cast<double *>(w);
+    return w + align256((size_t)N * 5 * sizeof(double));
+}
+
 }  // namespace
 
 // shared with the host control plane (transfer_queue.cu)
@@ -329,39 +368,13 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     if (tune && (tune->kernel < 0 || tune->kernel > 3))
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: tune->kernel %d", tune->kernel);
 
-    grpo::LossArgs a;
+    grpo::LossArgs a{};
+    fill_loss_args(a, row_begin, n_rows, V, target_ids, logp_behav, cu_seqlens, N, traj_index, adv,
+                   inv_norm, opts->eps_lo, opts->eps_hi, grad_scale, logp_out, lse_out, token_scale_out,
+                   traj_sum, stats, workspace);
     a.logits = logits;
     a.dlogits = dlogits;
     a.ld = ld;
-    a.V = V;
-    a.row_begin = row_begin;
-    a.n_rows = n_rows;
-    a.target_ids = target_ids;
-    a.logp_behav = logp_behav;
-    a.cu_seqlens = cu_seqlens;
-    a.N = N;
-    a.traj_index = traj_index;
-    a.adv = adv;
-    a.inv_norm = inv_norm;
-    a.eps_lo = opts->eps_lo;
-    a.eps_hi = opts->eps_hi;
-    a.grad_scale = grad_scale;
-    a.logp_out = logp_out;
-    a.lse_out = lse_out;
-    a.scale_out = token_scale_out;
-    a.traj_sum = traj_sum;
-    a.stats = stats;
-    uint8_t *w = static_cast<uint8_t *>(workspace);
-    w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(w)));
-    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
-    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
-    a.term_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.logp_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.flag_ws = w;
-    w += align256((size_t)n_rows);
-    a.part_ws = reinterpret_cast<double *>(w);
 
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
@@ -452,36 +465,10 @@ grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_beg
         return fail(GRPO_ERR_WORKSPACE, "loss_fwd_vp: workspace %zu B < required %zu B",
                     workspace_bytes, need);
     grpo::LossArgs a{};
+    uint8_t *w = fill_loss_args(a, row_begin, n_rows, V, target_ids, logp_behav, cu_seqlens, N, traj_index,
+                                adv, inv_norm, opts->eps_lo, opts->eps_hi, grad_scale, logp_out, lse_out,
+                                token_scale_out, traj_sum, stats, workspace);
     a.ld = ld;
-    a.V = V;
-    a.row_begin = row_begin;
-    a.n_rows = n_rows;
-    a.target_ids = target_ids;
-    a.logp_behav = logp_behav;
-    a.cu_seqlens = cu_seqlens;
-    a.N = N;
-    a.traj_index = traj_index;
-    a.adv = adv;
-    a.inv_norm = inv_norm;
-    a.eps_lo = opts->eps_lo;
-    a.eps_hi = opts->eps_hi;
-    a.grad_scale = grad_scale;
-    a.logp_out = logp_out;
-    a.lse_out = lse_out;
-    a.scale_out = token_scale_out;
-    a.traj_sum = traj_sum;
-    a.stats = stats;
-    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
-    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
-    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
-    a.term_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.logp_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.flag_ws = w;
-    w += align256((size_t)n_rows);
-    a.part_ws = reinterpret_cast<double *>(w);
-    w += align256((size_t)N * 5 * sizeof(double));
     unsigned long long *row_ctr = reinterpret_cast<unsigned long long *>(w);
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
@@ -594,36 +581,12 @@ grpo_status_t grpo_async_lmhead_fwd(const uint16_t *hidden, const uint16_t *W, i
         return fail(GRPO_ERR_WORKSPACE, "lmhead_fwd: workspace %zu B < required %zu B", workspace_bytes,
                     need);
     grpo::LossArgs a{};
-    a.V = V;
-    a.row_begin = row_begin;
-    a.n_rows = n_rows;
-    a.target_ids = target_ids;
-    a.logp_behav = logp_behav;
-    a.cu_seqlens = cu_seqlens;
-    a.N = N;
-    a.traj_index = traj_index;
-    a.adv = adv;
-    a.inv_norm = inv_norm;
-    a.eps_lo = opts->eps_lo;
-    a.eps_hi = opts->eps_hi;
-    a.grad_scale = grad_scale;
-    a.logp_out = logp_out;
-    a.lse_out = lse_out;
-    a.scale_out = token_scale_out;
-    a.traj_sum = traj_sum;
-    a.stats = stats;
-    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
-    uint8_t *const w0 = w;
-    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
-    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
-    a.term_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.logp_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.flag_ws = w;
-    w += align256((size_t)n_rows);
-    a.part_ws = reinterpret_cast<double *>(w);
-    w = w0 + grpo_async_workspace_size(n_rows, V, N) - 256;  // past the standard carve-up
+    fill_loss_args(a, row_begin, n_rows, V, target_ids, logp_behav, cu_seqlens, N, traj_index, adv, inv_norm,
+                   opts->eps_lo, opts->eps_hi, grad_scale, logp_out, lse_out, token_scale_out, traj_sum, stats,
+                   workspace);
+    // past the standard carve-up (grpo_async_workspace_size's layout, incl. its trailing slack)
+    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace))) +
+                 grpo_async_workspace_size(n_rows, V, N) - 256;
     const int32_t n_split = grpo::lmhead_n_split(n_rows, V);
     float2 *part = reinterpret_cast<float2 *>(w);
     w += align256((size_t)n_split * (size_t)n_rows * 8);
@@ -746,34 +709,9 @@ grpo_status_t grpo_async_lmhead_tp_fwd(const float *row_parts, int32_t R, int64_
         return fail(GRPO_ERR_WORKSPACE, "lmhead_tp_fwd: workspace %zu B < required %zu B", workspace_bytes,
                     need);
     grpo::LossArgs a{};
-    a.V = V;
-    a.row_begin = row_begin;
-    a.n_rows = n_rows;
-    a.target_ids = target_ids;
-    a.logp_behav = logp_behav;
-    a.cu_seqlens = cu_seqlens;
-    a.N = N;
-    a.traj_index = traj_index;
-    a.adv = adv;
-    a.inv_norm = inv_norm;
-    a.eps_lo = opts->eps_lo;
-    a.eps_hi = opts->eps_hi;
-    a.grad_scale = grad_scale;
-    a.logp_out = logp_out;
-    a.lse_out = lse_out;
-    a.scale_out = token_scale_out;
-    a.traj_sum = traj_sum;
-    a.stats = stats;
-    uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
-    a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
-    w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
-    a.term_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.logp_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
-    a.flag_ws = w;
-    w += align256((size_t)n_rows);
-    a.part_ws = reinterpret_cast<double *>(w);
+    fill_loss_args(a, row_begin, n_rows, V, target_ids, logp_behav, cu_seqlens, N, traj_index, adv, inv_norm,
+                   opts->eps_lo, opts->eps_hi, grad_scale, logp_out, lse_out, token_scale_out, traj_sum, stats,
+                   workspace);
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
     cudaError_t e = grpo::launch_rowinfo(a, s, &launches);
