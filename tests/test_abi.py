@@ -147,3 +147,46 @@ def test_host_side_errors_new_entry_points():
                                  0.2, 1.0, None, None, None, fake, fake, None, fake, ws2,
                                  C.byref(t), None)
     assert st == L.GRPO_ERR_INVALID_ARG
+
+
+def test_host_side_errors_tensor_parallel_and_sharded_entry_points():
+    import paper_2604_26256_b200._lib as L
+    lib = L.LIB
+    fake = C.c_void_p(16)
+    assert lib.grpo_async_lmhead_set_cta_group(3) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_lmhead_set_cta_group(2) == L.GRPO_OK
+    ws = lib.grpo_async_lmhead_workspace_size(10, 1000, 1)
+    # tp partials: negative col_offset, d % 64
+    assert lib.grpo_async_lmhead_tp_partials(fake, fake, 10, 128, 1000, -1, fake, fake, fake, ws,
+                                             None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_lmhead_tp_partials(fake, fake, 10, 100, 1000, 0, fake, fake, fake, ws,
+                                             None) == L.GRPO_ERR_INVALID_ARG
+    # tp fwd: R < 1, NULL opts
+    opts = L.LossOpts(0.2, 0.2, 0, None, 0)
+    vws = lib.grpo_async_workspace_size(10, 1000, 4)
+    assert lib.grpo_async_lmhead_tp_fwd(fake, 0, 0, 10, 1000, fake, fake, fake, 4, None, fake, fake,
+                                        C.byref(opts), 1.0, None, None, None, fake, fake, fake, vws,
+                                        None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_lmhead_tp_fwd(fake, 2, 0, 10, 1000, fake, fake, fake, 4, None, fake, fake,
+                                        None, 1.0, None, None, None, fake, fake, fake, vws,
+                                        None) == L.GRPO_ERR_INVALID_ARG
+    # tp bwd: ld_dz < Vs
+    assert lib.grpo_async_lmhead_tp_bwd(fake, fake, 10, 128, 1000, 0, fake, fake, fake, 1.0, fake, 992,
+                                        None, None, None) == L.GRPO_ERR_ALIGNMENT
+    # fused dhidden: d % 128, rank >= world, NULL slot
+    slots = (C.c_void_p * 2)(16, 32)
+    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 192, 1000, 2, 0, slots,
+                                       None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 256, 1000, 2, 2, slots,
+                                       None) == L.GRPO_ERR_INVALID_ARG
+    bad = (C.c_void_p * 2)(16, None)
+    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 256, 1000, 2, 0, bad,
+                                       None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_lmhead_tp_dx_reduce(fake, 9, 10, 256, 0, fake, 0, None) == L.GRPO_ERR_INVALID_ARG
+    # dW from dz: ld_dz not a multiple of 8
+    assert lib.grpo_async_lmhead_dw(fake, 10, 128, 1000, fake, 1001, fake, None) == L.GRPO_ERR_ALIGNMENT
+    # sharded rewards: P <= 0, std_floor <= 0
+    assert lib.grpo_async_group_partials(fake, fake, fake, 4, 0, None, fake, None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_group_sq_partials(fake, fake, 4, 2, None, fake, None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_advantage_from_stats(fake, fake, fake, 4, 2, 0.0, None, fake, fake, fake, fake,
+                                               None) == L.GRPO_ERR_INVALID_ARG
