@@ -321,3 +321,50 @@ def test_run_to_run_bitwise_determinism(dev, name):
     g2 = run_gpu(b, bits, dev, chunks=3)
     for k in ("adv", "inv_norm", "logp", "lse", "scale", "traj_sum", "stats", "dlogits_raw"):
         assert np.array_equal(g1[k], g2[k], equal_nan=True), k
+
+
+def test_step_captures_into_a_cuda_graph(dev):
+    """One step of the path (validate, advantage, fused loss over row chunks) is stream-ordered
+    with no host synchronisation, so it captures into a CUDA graph; replays reproduce the
+    eager outputs bit for bit."""
+    import paper_2604_26256_b200 as Gp
+    b, bits = _case("mid152k", 12)
+    eager = run_gpu(b, bits, dev, chunks=2)
+    db = Gp.DeviceBatch.from_host(b, dev)
+    loss = Gp.GrpoAsyncLoss()
+    T, ld, V = b.T, b.ld, b.V
+    lg = torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).to(dev)
+    dl = torch.full((T, ld), 0x7FC3, dtype=torch.int16, device=dev)
+    logp = torch.empty(T, device=dev)
+    traj_sum = torch.zeros(b.N, dtype=torch.float64, device=dev)
+    stats = torch.zeros(Gp.NUM_STATS, dtype=torch.float64, device=dev)
+    vo = Gp.ValidateOut(b.N, b.P, b.K, dev)
+    adv = torch.empty(b.N, device=dev)
+    inv = torch.empty(b.N, device=dev)
+    loss.workspace(T - T // 2, V, b.N, dev)  # allocate outside the capture
+
+    def step():
+        traj_sum.zero_()
+        stats.zero_()
+        loss.validate(db, vo)
+        loss.advantage(db, adv, inv)
+        for r0, r1 in ((0, T // 2), (T // 2, T)):
+            loss.loss_chunk(lg[r0:r1], r0, r1 - r0, db.target_ids[r0:r1], db.logp_behav[r0:r1],
+                            db.cu_seqlens, adv, inv, traj_sum, stats, dlogits=dl[r0:r1],
+                            logp_out=logp[r0:r1], V=V)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()  # warm-up on the side stream (function attributes, tensor maps)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(logp.cpu().numpy().astype(np.float64), eager["logp"])
+    assert np.array_equal(stats.cpu().numpy(), eager["stats"])
+    assert np.array_equal(traj_sum.cpu().numpy(), eager["traj_sum"])
+    assert np.array_equal(dl.cpu().numpy().view(np.uint16), eager["dlogits_raw"])
