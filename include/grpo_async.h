@@ -111,11 +111,12 @@ typedef struct {
 
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
-    int32_t kernel;        /* 0 auto (2 for V < 90000, else 3 with 32 KB slots), 1 cluster-resident, 2 row-wise, */
-                           /* 3 one row per SM streamed through a bulk-copy ring (K3c)       */
+    int32_t kernel;        /* 0 auto: 2 for V < 90000, else 3 with 6 x 32 KB slots (an explicit */
+                           /* tune with other fields set is never redirected); 1 cluster-    */
+                           /* resident; 2 row-wise; 3 one row per SM through a bulk-copy ring */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
     int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1); 1,2,4,8 (kernel 2: 1024/512/256/256 threads); */
-                           /* kernel 3: 256 / 1024 consumer threads (default 512)              */
+                           /* kernel 3: 256 consumer threads (default 512)                     */
     int32_t stages;        /* 0 auto, else lag+2..8 shared-memory row stages per CTA (kernel 1); */
                            /* kernel 2: 4, 8 or 16 vectors in flight per thread; kernel 3:  */
                            /* ring slots (0 = as many as fit: 13 of 16 KB, 6 of 32 KB)       */
@@ -126,7 +127,7 @@ typedef struct {
     int32_t row_cache;     /* kernel 2: leading vectors per thread of each row kept in shared */
                            /* memory for the second pass (0 auto = 160 KB per SM, -1 none); */
                            /* kernel 3: CTAs per SM, 1 (default) or 2                        */
-    int32_t chunk_kb;      /* kernel 3: ring slot size in KB, 16 (default) or 32              */
+    int32_t chunk_kb;      /* kernel 3: ring slot size in KB: 16 (default), 24, 32, 48 or 64   */
 } grpo_tune_t;
 
 /*
@@ -470,14 +471,18 @@ typedef struct {
     int32_t kernel;        /* 1 cluster-resident, 2 row-wise, 3 streamed ring, 4/5/6 LM-head */
                            /* (tcgen05) loss partials / logits gradient / logits, 7 vocab-  */
                            /* parallel                                                      */
-    int32_t cluster_size;  /* CTAs per row (kernel 1)                                 */
-    int32_t ctas_per_sm;   /* requested residency (kernel 1)                          */
-    int32_t stages;        /* shared-memory row stages per CTA (kernel 1)             */
-    int32_t vec_per_thread;/* 8-element vectors held in registers per thread          */
-    int32_t grid;          /* CTAs launched                                           */
-    int32_t max_clusters;  /* co-resident clusters the occupancy query allows         */
-    int32_t smem_bytes;    /* dynamic shared memory per CTA                           */
-    int32_t lag;           /* reduction-to-backward lag in rows (kernel 1)            */
+    int32_t cluster_size;  /* CTAs per row (kernel 1); CTAs per MMA (4-6)                     */
+    int32_t ctas_per_sm;   /* requested residency                                            */
+    int32_t stages;        /* kernel 1: row stages per CTA; 2: cached vectors per thread;   */
+                           /* 3: ring slots; 4-6: pipeline stages                            */
+    int32_t vec_per_thread;/* kernels 1-3, 7: threads per CTA (consumer threads for 3);      */
+                           /* 4-6: vocabulary tiles per work unit                            */
+    int32_t grid;          /* CTAs launched                                                  */
+    int32_t max_clusters;  /* kernels 1, 2, 7: co-resident CTAs / clusters per SM the        */
+                           /* occupancy query allows; 4-6: work units                        */
+    int32_t smem_bytes;    /* dynamic shared memory per CTA                                  */
+    int32_t lag;           /* kernel 1: reduction-to-backward lag in rows; 3: free ring     */
+                           /* slots at the end of pass 1; 7: deferred exchange wait          */
 } grpo_plan_t;
 
 grpo_status_t grpo_async_last_plan(grpo_plan_t *out);
