@@ -368,3 +368,24 @@ def test_step_captures_into_a_cuda_graph(dev):
     assert np.array_equal(stats.cpu().numpy(), eager["stats"])
     assert np.array_equal(traj_sum.cpu().numpy(), eager["traj_sum"])
     assert np.array_equal(dl.cpu().numpy().view(np.uint16), eager["dlogits_raw"])
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_shapes_and_plans(dev, seed):
+    """Fuzz: random vocabulary size, row count, row padding and launch plan (row-wise,
+    streamed ring with random slot size / count / free slots) against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    V = int(rng.choice([int(rng.integers(2, 600)), int(rng.integers(600, 40000)),
+                        int(rng.integers(40000, 200000))]))
+    n = int(rng.integers(4, 48))
+    rows = [(rng.normal(size=V) * float(rng.uniform(0.5, 4)), int(rng.integers(0, V))) for _ in range(n)]
+    b, bits = _adversarial_batch(V, rows)
+    ref = run_oracle(b, bits)
+    kb = int(rng.choice([16, 24, 32, 48]))
+    ns = int(rng.integers(2, 208 // kb + 1))
+    plans = [None, {"kernel": 2}, {"kernel": 3, "chunk_kb": kb, "stages": ns,
+                                   "lag": int(rng.integers(1, ns))}]
+    for tune in plans:
+        gpu = run_gpu(b, bits, dev, tune=tune, chunks=int(rng.integers(1, 4)),
+                      inplace=bool(rng.integers(0, 2)))
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
