@@ -11,6 +11,10 @@ import paper_2604_26256_b200 as G
 from synth.gen import bf16_bits_to_f32
 
 EPS32 = float(np.float32(0.2))
+# DESIGN.md Z17: the relative loss criterion is taken against max(|J|, Z17_GUARD * S_abs).  The
+# fp32 per-token path carries |d logp| ~ 1e-6 (7e-7 observed at worst on the fuzz), i.e.
+# |dJ| <~ 1e-6 * S_abs whatever the cancellation in J; 1e-5 of 0.1 * S_abs is that floor.
+Z17_GUARD = 0.1
 
 
 def to_dev_bits(bits: np.ndarray, device) -> torch.Tensor:
@@ -105,7 +109,7 @@ def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5,
                          np.abs(rr.term)))
     J_gpu = gpu["stats"][G.STAT_J]
     errs["J_ref"], errs["J_gpu"] = J_ref, J_gpu
-    errs["J_rel_guarded"] = abs(J_gpu - J_ref) / max(abs(J_ref), 1e-2 * S_abs, 1e-300)
+    errs["J_rel_guarded"] = abs(J_gpu - J_ref) / max(abs(J_ref), Z17_GUARD * S_abs, 1e-300)
     errs["J_rel_raw"] = abs(J_gpu - J_ref) / max(abs(J_ref), 1e-300)
     assert errs["J_rel_guarded"] <= loss_rtol, errs
     assert abs(gpu["stats"][G.STAT_ABS] - S_abs) <= 1e-5 * S_abs + 1e-300

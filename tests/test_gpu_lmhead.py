@@ -190,7 +190,7 @@ def test_lmhead_tensor_parallel(dev, name, d, R, cta_group):
     assert np.max(np.abs(g["logp"] - rr.logp)) <= 2e-3
     S_abs = float(np.sum(ref["inv_norm"][np.repeat(np.arange(b.N), b.lengths)] * np.abs(rr.term)))
     J = g["stats"][G.STAT_J]
-    assert abs(J - ref["J"]) / max(abs(ref["J"]), 1e-2 * S_abs) <= 1e-5
+    assert abs(J - ref["J"]) / max(abs(ref["J"]), 0.1 * S_abs) <= 1e-5  # DESIGN.md Z17
     for k, rk in (("dz", rr.dlogits), ("dX", ref["dhidden"]), ("dW", ref["dW"])):
         assert _rel_l2(g[k], rk) <= 1e-2, k
 
