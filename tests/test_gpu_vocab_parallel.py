@@ -71,3 +71,24 @@ def test_vp_forward_only_and_empty_shards(dev):
     ref = run_oracle(b, bits)
     gpu = run_gpu_vp(b, bits, dev, 4, shard_cols=512)
     compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_vp_random_shapes(dev, seed):
+    """Fuzz: random vocabulary, group size 1-8, shard width (incl. empty trailing shards),
+    chunking and schedule, against the oracle."""
+    from tests.test_gpu_parity import _adversarial_batch
+    rng = np.random.default_rng(500 + seed)
+    V = int(rng.choice([int(rng.integers(8, 2000)), int(rng.integers(2000, 80000))]))
+    world = int(rng.integers(1, 9))
+    n = int(rng.integers(4, 40))
+    rows = [(rng.normal(size=V) * float(rng.uniform(0.5, 3)), int(rng.integers(0, V))) for _ in range(n)]
+    b, bits = _adversarial_batch(V, rows)
+    ref = run_oracle(b, bits)
+    base = -(-V // (world * 8)) * 8
+    sc = base if rng.integers(0, 2) else base + 8 * int(rng.integers(1, 64))
+    gpu = run_gpu_vp(b, bits, dev, world, chunks=int(rng.integers(1, 3)), shard_cols=sc,
+                     lag=int(rng.integers(0, 2)), dynamic_rows=int(rng.integers(0, 2)),
+                     calls=int(rng.integers(1, 3)))
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+    assert gpu["shard_pad_untouched"]
