@@ -298,3 +298,27 @@ def test_lmhead_tp_dx_gemm_reduce_scatter(dev, name, d, R):
     assert _rel_l2(dX, ref["dhidden"]) <= 1e-2
     # two f32 GEMMs summing ~V products in different orders
     assert _rel_l2(dX, cublas_sum.cpu().numpy().astype(np.float64)) <= 1e-3
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_lmhead_random_shapes(dev, seed, cta_group):
+    """Fuzz: random row count (ragged 128/256-row tiles), d (multiples of 64), V (ragged 256
+    tiles) and chunking for the fused forward + backward against the oracle."""
+    import dataclasses
+
+    from synth.gen import lmhead_inputs
+    rng = np.random.default_rng(900 + seed)
+    d = 64 * int(rng.integers(1, 7))
+    V = int(rng.integers(3, 5000))
+    base = make_batch("ragged", seed)
+    b = dataclasses.replace(base, V=V, ld=(V + 7) // 8 * 8,
+                            target_ids=(base.target_ids % V).astype(np.int64))
+    X, W = lmhead_inputs(b.T, V, d, seed)
+    z = O.lmhead_logits(X, W)
+    m = z.max(1, keepdims=True)
+    lse = (m + np.log(np.exp(z - m).sum(1, keepdims=True)))[:, 0]
+    lw = (z[np.arange(b.T), b.target_ids] - lse - rng.normal(size=b.T) * 0.05).astype(np.float32)
+    b = dataclasses.replace(b, logp_behav=lw)
+    ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
+    gpu = run_gpu_lmhead(b, X, W, dev, chunks=int(rng.integers(1, 4)))
+    _check(gpu, ref, b)
