@@ -160,15 +160,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
             }
             // with a = -inf every element so far is -inf: reference 0 keeps the terms 0
             const float ref = a == -INFINITY ? 0.0f : a;
-            float t0 = 0.f, t1 = 0.f;
-#pragma unroll
-            for (int j = 0; j < U; ++j) {
-                t0 += ex2(fmaf(bf_lo(x[j].x), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].x), kLog2e, -ref)) +
-                      ex2(fmaf(bf_lo(x[j].y), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].y), kLog2e, -ref));
-                t1 += ex2(fmaf(bf_lo(x[j].z), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].z), kLog2e, -ref)) +
-                      ex2(fmaf(bf_lo(x[j].w), kLog2e, -ref)) + ex2(fmaf(bf_hi(x[j].w), kLog2e, -ref));
-            }
-            s += t0 + t1;
+            s += RowwiseBatch<NT, U>::sum_exp2(x, ref);
             if (c < g.n - g.R) {  // not resident: release now
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + sl);
@@ -235,7 +227,8 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
 #pragma unroll
-                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gref));
+                    for (int j = 0; j < U; ++j)
+                        stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gref));
                 }
             } else {
 #pragma unroll

@@ -39,6 +39,9 @@ plans = [json.loads(p) for p in args.plans.split(";")] if args.plans else [
 ]
 bytes_row = 4 * V + 25 if not args.fwd_only else 2 * V + 25
 def run_once(plan):
+    plan = dict(plan)
+    for k, v in plan.pop("env", {}).items():  # launch-time environment knobs (experiments)
+        os.environ[k] = str(v)
     loss.tune = plan
     G.grpo_profile_enable(True); G.grpo_profile_collect()
     loss.loss_chunk(lg, 0, R, db.target_ids[:R], db.logp_behav[:R], db.cu_seqlens, adv, inv, ts, st,
@@ -58,6 +61,8 @@ for r in range(n_rounds):
             continue
         try:
             ms, pl = run_once(plan)
+            for k in plan.get("env", {}):
+                os.environ.pop(k, None)
             plans_used[i] = pl
             if r > 0 or args.reps == 0:
                 times[i].append(ms)
