@@ -353,10 +353,14 @@ struct RowOut {
 // logp_t = z_y - lse from the row's log2-domain reference M and l2s = log2(S):
 //   logp = (z_y*log2e - M - l2s) * ln2,
 // formed in fp64 (a few DFMA per row) so the ratio r = exp(logp - logp_w) keeps
-// full fp32 accuracy even for very unlikely tokens (|logp| ~ 100).
+// full fp32 accuracy even for very unlikely tokens (|logp| ~ 100).  z_y is scaled by
+// the same fp32 log2e the exponents of S used: the kernels compute the softmax of
+// z*(1+d), d = fl32(log2e)*ln2 - 1 = 1.4e-8, and logp must be that softmax's log at y
+// -- error d*(z_y - E_p[z]) -- not a mix of the two scalings, which leaves d*E_p[z]
+// (1.4e-4 for logits near 1e4; tests/test_gpu_parity.py::test_scale_jumps_along_the_row).
 __device__ __forceinline__ double row_logp(float zy, float M, float l2s) {
-    const double kLog2eD = 1.4426950408889634074, kLn2D = 0.69314718055994530942;
-    return (fma((double)zy, kLog2eD, -(double)M) - (double)l2s) * kLn2D;
+    const double kLn2D = 0.69314718055994530942;
+    return (fma((double)zy, (double)kLog2e, -(double)M) - (double)l2s) * kLn2D;
 }
 
 __device__ __forceinline__ RowOut row_epilogue(double logp, const RowInfo &ri, float eps_lo,

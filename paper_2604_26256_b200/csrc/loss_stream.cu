@@ -149,18 +149,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
                     else if (vi == g.n_vec - 1 && g.tail_valid < 8) x[j] = mask_tail(x[j], g.tail_valid);
                 }
             }
-            // running max as the exponent reference: one extra ex2 only when it grows
-            uint32_t mx2 = bmax2(bmax2(x[0].x, x[0].y), bmax2(x[0].z, x[0].w));
-#pragma unroll
-            for (int j = 1; j < U; ++j) mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
-            const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
-            if (va > a) {
-                s = (a == -INFINITY) ? 0.0f : s * ex2(a - va);
-                a = va;
-            }
-            // with a = -inf every element so far is -inf: reference 0 keeps the terms 0
-            const float ref = a == -INFINITY ? 0.0f : a;
-            s += RowwiseBatch<NT, U>::sum_exp2(x, ref);
+            RowwiseBatch<NT, U>::reduce(x, a, s);  // lazy exponent reference (rowwise.cuh)
             if (c < g.n - g.R) {  // not resident: release now
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + sl);

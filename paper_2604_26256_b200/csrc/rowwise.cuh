@@ -11,20 +11,40 @@ namespace grpo {
 template <int NT, int U>
 struct RowwiseBatch {
     // sum of 2^(z*log2e - ref) over U vectors (already loaded and masked): paired fp32
-    // arithmetic (FFMA2 / FADD2), one bf16 pair in four on the FMA-pipe polynomial and
-    // the rest on MUFU (ex2x2.cuh) -- measured 3 % faster than all-MUFU on K3c
+    // arithmetic (FFMA2 / FADD2), every exponential on MUFU.  x2::sum_exp2<U, K> can move
+    // K pairs to the FMA-pipe polynomial instead: +2.5 % for a single K3c launch, but
+    // -0.6 % in the sustained, power-capped loop (a polynomial exponential costs more
+    // energy than a MUFU one), so K = 0
     static __device__ __forceinline__ float sum_exp2(const uint4 (&x)[U], float ref) {
-        return x2::sum_exp2<U, U>(x, ref);
+        return x2::sum_exp2<U, 0>(x, ref);
     }
-    // log2-domain partial of U vectors (already loaded and masked)
+    // log2-domain partial of U vectors (already loaded and masked) into (a, s), with a lazy
+    // reference: a is set by the first batch holding a finite element (its max, rounded up,
+    // so every exponent of that batch is <= 0) and raised only when the partial sum passes
+    // 2^64, i.e. when a later element lies more than ~2^64 / (terms so far) above it; the
+    // common batch then costs no max reduction and no rescale.  Terms that fall below
+    // 2^-126 of the reference underflow exactly as they would against the running max
+    // (they are < 2^-126 of the max element, which a contributes at 2^0).  Any value of
+    // the row lands in a <= 2^64 sum, so the per-thread partials combine without overflow.
     static __device__ __forceinline__ void reduce(const uint4 (&x)[U], float &a, float &s) {
+        if (a != -INFINITY) {
+            const float t = s + sum_exp2(x, a);
+            if (t <= 1.8446744e19f) {  // 2^64; false for inf and NaN
+                s = t;
+                return;
+            }
+        }
         uint32_t mx2 = kBf16NegInfPair;
 #pragma unroll
         for (int j = 0; j < U; ++j)
             mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
         const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
-        if (va == -INFINITY) return;
-        lse2_merge(a, s, va, sum_exp2(x, va));
+        if (va > a) {
+            s = (a == -INFINITY) ? 0.0f : s * ex2(a - va);
+            a = va;
+        }
+        // with a = -inf every element so far is -inf: reference 0 keeps the terms 0
+        s += sum_exp2(x, a == -INFINITY ? 0.0f : a);
     }
     // s * 2^(z*log2e - lse2) = sign(s) * 2^(z*log2e - (lse2 - log2|s|)): the token scale
     // folds into the exponent's reference, so an element costs one FFMA and one EX2 (no

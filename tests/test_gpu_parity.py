@@ -167,6 +167,31 @@ def test_adversarial_rows(dev):
         compare(gpu, ref, b, logits_pad=bits[:, b.V:])
 
 
+@pytest.mark.parametrize("V", [40000, 152064])
+def test_scale_jumps_along_the_row(dev, V):
+    """Rows whose later chunks lie far above their first ones: the row-wise kernels keep
+    the first finite batch's max as the exponent reference and raise it only when a
+    thread's partial sum passes 2^64 (rowwise.cuh), so jumps below, at and above that
+    threshold and above fp32's exp2 range (2^128) must all match the oracle."""
+    rng = np.random.default_rng(11)
+    rows = []
+    for jump in (20.0, 40.0, 85.0, 200.0, 1e4):  # nats; 2^64 ~ e^44.4, 2^128 ~ e^88.7
+        if jump < 1e4:  # (a target 1e4 below the max: logp = -1e4, DESIGN.md Z23)
+            z = rng.normal(size=V); z[V // 2:] += jump
+            rows.append((z, int(rng.integers(0, V // 2))))  # target in the low half
+        z = rng.normal(size=V); z[V // 2:] += jump
+        rows.append((z, int(rng.integers(V // 2, V))))  # target in the high half
+    z = np.linspace(-150.0, 150.0, V); rows.append((z, V - 3))  # steady climb
+    z = np.full(V, -np.inf); z[-5:] = rng.normal(size=5); rows.append((z, V - 1))  # finite only at the end
+    z = rng.normal(size=V) * 40; rows.append((z, 9))
+    z = rng.normal(size=V); z[-1] = 120.0; rows.append((z, 0))  # one late dominant entry
+    b, bits = _adversarial_batch(V, rows)
+    ref = run_oracle(b, bits)
+    for tune in KERNELS:
+        gpu = run_gpu(b, bits, dev, tune=tune)
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+
+
 def test_single_token_trajectories_and_empty_chunk(dev):
     rng = np.random.default_rng(3)
     V, P, G = 300, 2, 4
