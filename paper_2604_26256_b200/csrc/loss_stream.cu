@@ -130,7 +130,9 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
         }
         // ---- pass 1: log2-domain running (max, sum) per thread
         float a = -INFINITY, s = 0.0f;
-        for (int c = 0; c < g.n; ++c) {
+        // the full chunks 0..n-2 run without masking (no register merges in the hot loop),
+        // the ragged last chunk after them
+        auto pass1_chunk = [&](int c, bool last) {
             const int sl = slot;
             mbar_wait(full + sl, par);
             if (++slot == p.ns) {
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
             uint4 x[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
-            if (c == g.n - 1) {  // the ragged end of the row (uniform branch)
+            if (last) {
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
                     const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
@@ -154,7 +156,10 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(empty + sl);
             }
-        }
+        };
+#pragma unroll 1
+        for (int c = 0; c < g.n - 1; ++c) pass1_chunk(c, false);
+        pass1_chunk(g.n - 1, true);
         // ---- block reduction and the per-row epilogue
         warp_lse2_combine(a, s);
         if (lane == 0) red[warp] = make_float2(a, s);
