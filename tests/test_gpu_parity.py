@@ -11,11 +11,14 @@ from tests.gpu_util import compare, run_gpu, run_oracle, to_dev_bits
 pytestmark = pytest.mark.gpu
 
 KERNELS = [{"kernel": 1}, {"kernel": 2}, {"kernel": 3}]
-STREAM_PLANS = [{"kernel": 3, "stages": st, "lag": lg, "ctas_per_sm": nt, "chunk_kb": kb}
-                for st, lg, nt, kb in ((13, 3, 0, 16), (13, 1, 0, 16), (13, 12, 0, 16), (2, 1, 0, 16),
-                                       (5, 2, 0, 16), (8, 3, 256, 16), (13, 3, 256, 16),
-                                       (6, 3, 0, 32), (6, 1, 0, 32), (2, 1, 0, 32), (6, 5, 0, 32),
-                                       (3, 1, 256, 32))]
+STREAM_PLANS = [{"kernel": 3, "stages": st, "lag": lg, "ctas_per_sm": nt, "chunk_kb": kb, "row_cache": cps}
+                for st, lg, nt, kb, cps in ((13, 3, 0, 16, 0), (13, 1, 0, 16, 0), (13, 12, 0, 16, 0),
+                                            (2, 1, 0, 16, 0), (5, 2, 0, 16, 0), (8, 3, 256, 16, 0),
+                                            (13, 3, 256, 16, 0), (6, 3, 0, 32, 0), (6, 1, 0, 32, 0),
+                                            (2, 1, 0, 32, 0), (6, 5, 0, 32, 0), (3, 1, 256, 32, 0),
+                                            # two CTAs per SM (the auto plan for 34000 <= V < 90000)
+                                            (6, 3, 256, 16, 2), (6, 1, 0, 16, 2), (3, 1, 0, 32, 2),
+                                            (2, 1, 256, 32, 2))]
 ROWWISE_PLANS = [{"kernel": 2, "ctas_per_sm": c, "stages": u, "row_cache": rc, "cluster_size": cl}
                  for c, u, rc, cl in ((1, 4, -1, 1), (1, 2, 0, 1), (1, 8, 1, 1), (2, 4, -1, 1),
                                       (2, 4, 0, 1), (2, 8, 1, 1), (2, 8, 0, 1), (2, 2, 0, 1),
@@ -282,6 +285,7 @@ def test_sharded_equals_unsharded(dev, R):
 
 @pytest.mark.parametrize("plan", STREAM_PLANS,
                          ids=lambda d: f"ns{d['stages']}pf{d['lag']}nt{d['ctas_per_sm'] or 512}"
+                                       f"kb{d['chunk_kb']}cps{d['row_cache'] or 1}"
                                        f"kb{d['chunk_kb']}")
 def test_stream_plans(dev, plan):
     """K3c (one row per SM through the bulk-copy ring) for ring sizes from 2 slots (every
@@ -297,7 +301,7 @@ def test_stream_plans(dev, plan):
     compare(gpu, ref, b, check_dlogits=False)
 
 
-@pytest.mark.parametrize("V", [2, 7, 8, 9, 100, 16391, 32776, 90007])
+@pytest.mark.parametrize("V", [2, 7, 8, 9, 100, 16391, 32776, 34003, 50689, 90007])
 def test_odd_vocabulary_sizes(dev, V):
     """Small and ragged vocabularies (V % 8 != 0; one vector past a 16 KB / 32 KB ring slot;
     the K3b/K3c switch point) for the row-wise and both ring geometries."""
@@ -312,17 +316,23 @@ def test_odd_vocabulary_sizes(dev, V):
 
 
 def test_auto_plan_choice(dev):
-    """The auto plan (tune kernel 0) runs K3b below V = 90000 and K3c (32 KB slots) from
-    there on (DESIGN.md §8 measurements); an explicitly tuned call is never redirected."""
+    """The auto plan (tune kernel 0): K3b below V = 34000, K3c with two 256-thread CTAs per
+    SM and 16 KB slots up to V = 90000, K3c with one CTA per SM and 32 KB slots from there
+    on (DESIGN.md section 8 measurements); an explicitly tuned call is never redirected."""
     import paper_2604_26256_b200 as Gp
-    for V, kernel in ((76032, 2), (90000, 3), (152064, 3)):
+    for V, kernel, cps in ((30000, 2, None), (34000, 3, 2), (76032, 3, 2), (89990, 3, 2),
+                           (90000, 3, 1), (152064, 3, 1)):
         rows = [(np.random.default_rng(V).normal(size=V), 3) for _ in range(4)]
         b, bits = _adversarial_batch(V, rows)
-        run_gpu(b, bits, dev)
+        ref = run_oracle(b, bits)
+        gpu = run_gpu(b, bits, dev)
         plan = Gp.grpo_async_last_plan()
         assert plan["kernel"] == kernel, (V, plan)
         if kernel == 3:
-            assert plan["stages"] == 6 and plan["smem_bytes"] >= 6 * 32768
+            assert plan["stages"] == 6 and plan["ctas_per_sm"] == cps, (V, plan)
+            assert plan["smem_bytes"] >= 6 * (32768 if cps == 1 else 16384)
+            assert plan["vec_per_thread"] == (512 if cps == 1 else 256), (V, plan)
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
     run_gpu(b, bits, dev, tune={"kernel": 2, "stages": 8})
     assert Gp.grpo_async_last_plan()["kernel"] == 2
 
