@@ -111,7 +111,8 @@ typedef struct {
 
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
-    int32_t kernel;        /* 0 auto: 2 for V < 90000, else 3 with 6 x 32 KB slots (an explicit */
+    int32_t kernel;        /* 0 auto: 2 for V < 34000; 3 with 2 CTAs x 6 x 16 KB up to 90000, */
+                           /* else 3 with 1 CTA x 6 x 32 KB slots per SM (an explicit        */
                            /* tune with other fields set is never redirected); 1 cluster-    */
                            /* resident; 2 row-wise; 3 one row per SM through a bulk-copy ring */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1)       */
@@ -291,9 +292,11 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
  * grpo_async_loss_fwd_vp -- the fused loss for vocabulary-parallel logits (
  * Megatron-style tensor parallelism of the LM head): rank q of a group of R
  * GPUs holds the columns [q*shard_cols, (q+1)*shard_cols) of every row of the chunk.
- * The per-row logsumexp needs all R shards: the kernel exchanges one 16-byte partial
- * per row and rank through peer memory (NVLink P2P stores + system-scope arrival
- * counters) inside the loss kernel, then writes this rank's slice of dlogits.  Every
+ * The per-row logsumexp needs all R shards: the kernel exchanges one 32-byte partial
+ * per row and rank through peer memory (NVLink P2P stores of 64-bit words tagged with
+ * the call's epoch) inside the loss kernel, then writes this rank's slice of dlogits.
+ * Shards of >= 60000 columns with lag 0 and static rows run the streamed ring kernel
+ * (plan kernel 8), others the row-wise one (plan kernel 7); same results.  Every
  * rank computes identical per-row outputs, traj_sum and stats (no further reduction).
  * comm describes the group (host struct of device pointers):
  *   world R <= GRPO_VP_MAX_RANKS; the call computes ranks [rank_begin, rank_begin+n_local)
@@ -470,19 +473,19 @@ grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W
 typedef struct {
     int32_t kernel;        /* 1 cluster-resident, 2 row-wise, 3 streamed ring, 4/5/6 LM-head */
                            /* (tcgen05) loss partials / logits gradient / logits, 7 vocab-  */
-                           /* parallel                                                      */
+                           /* parallel row-wise, 8 vocab-parallel streamed ring              */
     int32_t cluster_size;  /* CTAs per row (kernel 1); CTAs per MMA (4-6)                     */
     int32_t ctas_per_sm;   /* requested residency                                            */
     int32_t stages;        /* kernel 1: row stages per CTA; 2: cached vectors per thread;   */
-                           /* 3: ring slots; 4-6: pipeline stages                            */
-    int32_t vec_per_thread;/* kernels 1-3, 7: threads per CTA (consumer threads for 3);      */
+                           /* 3, 8: ring slots; 4-6: pipeline stages                         */
+    int32_t vec_per_thread;/* kernels 1-3, 7, 8: threads per CTA (consumer threads for 3, 8); */
                            /* 4-6: vocabulary tiles per work unit                            */
     int32_t grid;          /* CTAs launched                                                  */
     int32_t max_clusters;  /* kernels 1, 2, 7: co-resident CTAs / clusters per SM the        */
                            /* occupancy query allows; 4-6: work units                        */
     int32_t smem_bytes;    /* dynamic shared memory per CTA                                  */
     int32_t lag;           /* kernel 1: reduction-to-backward lag in rows; 3: free ring     */
-                           /* slots at the end of pass 1; 7: deferred exchange wait          */
+                           /* slots at the end of pass 1 (also 8); 7: deferred exchange wait */
 } grpo_plan_t;
 
 grpo_status_t grpo_async_last_plan(grpo_plan_t *out);

@@ -285,6 +285,289 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
     }
 }
 
+// The same exchange inside the streamed ring kernel (K3c, loss_stream.cu): one producer
+// thread per CTA moves the local shard's rows with bulk copies into a FIFO ring of NS
+// slots; the consumers run pass 1, post the row's partial to every rank and wait for the
+// group's partials (warp 0) while the producer already streams the next row into the
+// free slots, then run pass 2 over the resident chunks and the re-loads.  Static rows
+// only (CTA g of every rank takes rows g, g + g_per, ...); lag and dynamic_rows select
+// vp_kernel above.
+template <int NT, int MINB, int CHUNK_VECS>
+__global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams p, const int ns,
+                                                                   const int pf) {
+    constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
+    constexpr int U = CHUNK_VECS / NT;
+    constexpr int NW = NT / 32;
+    using B = RowwiseBatch<NT, U>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint4 *ring = reinterpret_cast<uint4 *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)ns * CHUNK_BYTES);
+    uint64_t *empty = full + ns;
+    __shared__ float2 red[NW];
+    __shared__ float row_scalars[4];
+    const int g_per = gridDim.x / p.n_local;
+    const int lr = blockIdx.x / g_per;  // local rank of this CTA
+    const int g = blockIdx.x - lr * g_per;
+    const int rank = p.rank_begin + lr;
+    const int32_t c0 = rank * p.shard_cols;  // first vocabulary column of this shard
+    const int32_t vc = max(0, min(p.shard_cols, p.V - c0));
+    const int n_vec = (vc + 7) / 8;
+    const int n = (n_vec + CHUNK_VECS - 1) / CHUNK_VECS;  // chunks per row
+    const uint16_t *shard = p.logits[lr];
+    uint16_t *dshard = p.dlogits[lr];
+    const bool two_pass = dshard != nullptr;
+    const int R = two_pass ? min(n, max(0, ns - pf)) : 0;  // chunks resident after pass 1
+    const int loads = two_pass ? 2 * n - R : n;
+    const int tail_valid = vc - (n_vec - 1) * 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < ns; ++q) {
+            mbar_init(full + q, 1);
+            mbar_init(empty + q, NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            const uint64_t pol_keep = policy_evict_last(), pol_once = policy_evict_first();
+            const int64_t row_bytes = (int64_t)n_vec * 16;
+            int slot = 0;
+            uint32_t par = 0;
+            for (int64_t row = g; row < p.n_rows; row += g_per) {
+                const uint8_t *src = reinterpret_cast<const uint8_t *>(shard + row * p.ld);
+                for (int i = 0; i < loads; ++i) {
+                    const int c = i < n ? i : i - n;
+                    mbar_wait(empty + slot, par ^ 1u);
+                    const int64_t off = (int64_t)c * CHUNK_BYTES;
+                    const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
+                    const uint64_t pol = (i < n && c < n - R && two_pass) ? pol_keep : pol_once;
+                    mbar_arrive_expect_tx(full + slot, bytes);
+                    bulk_g2s(ring + (size_t)slot * CHUNK_VECS, src + off, bytes, full + slot, pol);
+                    if (++slot == ns) {
+                        slot = 0;
+                        par ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
+    int slot = 0;
+    uint32_t par = 0;
+    for (int64_t row = g; row < p.n_rows; row += g_per) {
+        const int base_slot = slot;
+        // the epilogue's dependent global reads, issued before pass 1
+        RowInfo ri;
+        uint16_t zy_bits = 0;
+        bool mine = false;
+        int32_t y_loc = -1;
+        if (threadIdx.x == 0) {
+            ri = p.rowinfo[row];
+            y_loc = ri.target - c0;
+            mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
+            if (mine) zy_bits = shard[row * p.ld + y_loc];
+        }
+        // ---- pass 1 over the local shard (full chunks, then the ragged last one)
+        float a = -INFINITY, s = 0.0f;
+        auto pass1_chunk = [&](int c, bool last) {
+            const int sl = slot;
+            mbar_wait(full + sl, par);
+            if (++slot == ns) {
+                slot = 0;
+                par ^= 1u;
+            }
+            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            uint4 x[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+            if (last) {
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
+                    if (vi >= n_vec) x[j] = neg_inf;
+                    else if (vi == n_vec - 1 && tail_valid < 8) x[j] = mask_tail(x[j], tail_valid);
+                }
+            }
+            B::reduce(x, a, s);
+            if (c < n - R) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + sl);
+            }
+        };
+#pragma unroll 1
+        for (int c = 0; c < n - 1; ++c) pass1_chunk(c, false);
+        if (n > 0) pass1_chunk(n - 1, true);
+        warp_lse2_combine(a, s);
+        if (lane == 0) red[warp] = make_float2(a, s);
+        named_bar_sync(1, NT);
+        if (warp == 0) {
+            float cm = lane < NW ? red[lane].x : -INFINITY, cs = lane < NW ? red[lane].y : 0.0f;
+            warp_lse2_combine(cm, cs);
+            const bool own_y = __shfl_sync(0xFFFFFFFFu, mine, 0);
+            const float zy = own_y ? __uint_as_float(((uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)zy_bits, 0)) << 16)
+                                   : 0.0f;
+            // ---- the exchange (tagged 64-bit words, see vp_kernel)
+            if (lane < p.world) {
+                const uint64_t hi = (uint64_t)p.tag << 32;
+                ulonglong2 *dst = p.xbuf[lane] + ((p.half + row) * p.world + rank) * 2;
+                st_relaxed_sys_v2(dst, hi | __float_as_uint(cm), hi | __float_as_uint(cs));
+                st_relaxed_sys_v2(dst + 1, hi | __float_as_uint(zy), hi | (own_y ? 1u : 0u));
+            }
+            float M = -INFINITY, S = 0.0f, zsrc = 0.0f;
+            bool own = false;
+            if (lane < p.world) {
+                const ulonglong2 *src = p.xbuf[rank] + ((p.half + row) * p.world + lane) * 2;
+                ulonglong2 w0, w1;
+                long long spins = 0;
+                for (;;) {
+                    w0 = ld_relaxed_sys_v2(src);
+                    w1 = ld_relaxed_sys_v2(src + 1);
+                    if ((uint32_t)(w0.x >> 32) == p.tag && (uint32_t)(w0.y >> 32) == p.tag &&
+                        (uint32_t)(w1.x >> 32) == p.tag && (uint32_t)(w1.y >> 32) == p.tag)
+                        break;
+                    __nanosleep(32);
+                    if (++spins > (1ll << 27)) __trap();  // a peer never arrived: fail, don't hang
+                }
+                M = __uint_as_float((uint32_t)w0.x);
+                S = __uint_as_float((uint32_t)w0.y);
+                zsrc = __uint_as_float((uint32_t)w1.x);
+                own = (uint32_t)w1.y != 0u;
+            }
+            warp_lse2_combine(M, S);  // same inputs in the same lanes on every rank
+            const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
+            const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
+            if (lane == 0) {
+                const float zyv = own_mask != 0u ? zsh : __int_as_float(0x7FC00000);
+                const float l2s = log2f(S);
+                const float lse2 = M + l2s;
+                const double logp_d = row_logp(zyv, M, l2s);
+                const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
+                if (lr == 0) {  // per-row outputs: identical on every rank, written once per call
+                    const float logp = (float)logp_d;
+                    if (p.logp_out) p.logp_out[row] = logp;
+                    if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
+                    if (p.scale_out) p.scale_out[row] = o.s;
+                    p.term_ws[row] = o.term;
+                    p.logp_ws[row] = logp;
+                    p.flag_ws[row] = o.flags;
+                }
+                row_scalars[0] = lse2;
+                row_scalars[1] = o.s;
+                row_scalars[2] = zyv;
+                row_scalars[3] = __int_as_float(mine ? y_loc : -1);
+            }
+        }
+        named_bar_sync(1, NT);
+        if (!two_pass) continue;
+        // ---- pass 2: resident chunks n-R..n-1, then the re-loads
+        const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
+        const auto gref = B::grad_ref(sc, lse2);
+        const int32_t y = __float_as_int(row_scalars[3]);
+        const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
+        uint16_t *drow = dshard + row * p.ld;
+        uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
+        for (int i = 0; i < n; ++i) {
+            const bool resident = i < R;
+            const int c = resident ? n - R + i : i - R;
+            int sl;
+            if (resident) {
+                sl = (base_slot + c) % ns;
+            } else {
+                sl = slot;
+                mbar_wait(full + sl, par);
+                if (++slot == ns) {
+                    slot = 0;
+                    par ^= 1u;
+                }
+            }
+            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            const int v0 = c * CHUNK_VECS + threadIdx.x;
+            if (c != n - 1) {
+                if (sc == 0.0f) {
+#pragma unroll
+                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, make_uint4(0u, 0u, 0u, 0u));
+                } else {
+                    uint4 x[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad_scaled(x[j], gref));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int vi = v0 + j * NT;
+                    if (vi >= n_vec) break;
+                    const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
+                                               : B::grad_scaled(chunk[j * NT + threadIdx.x], gref);
+                    if (vi == n_vec - 1 && tail_valid < 8) store_tail(drow + (int64_t)vi * 8, d, tail_valid);
+                    else stg_stream(dst4 + vi, d);
+                }
+            }
+            if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
+                const float py = ex2(fmaf(zy, kLog2e, -lse2));
+                drow[y] = f2bf(sc * (py - 1.0f));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + sl);
+        }
+    }
+}
+
+template <int NT, int MINB, int CV>
+static cudaError_t launch_vp_stream(VpParams p, const grpo_vp_comm_t *comm, int ns, int pf,
+                                    int64_t n_rows, cudaStream_t s, int *launches, grpo_plan_t *plan,
+                                    char *why, size_t why_len) {
+    const size_t smem = (size_t)ns * CV * 16 + 2 * (size_t)ns * 8;
+    auto kern = vp_stream_kernel<NT, MINB, CV>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, n_sm = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 32, smem);
+    if (e != cudaSuccess) return e;
+    // every CTA must be resident (a CTA may wait for a peer rank's CTA of the same index)
+    int64_t g_per = (int64_t)n_sm * (occ < MINB ? occ : MINB) / comm->n_local;
+    if (g_per > n_rows) g_per = n_rows;
+    if (g_per < 1) {
+        if (why) snprintf(why, why_len, "vp stream kernel: no resident CTA per local rank");
+        return cudaErrorInvalidConfiguration;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)(g_per * comm->n_local));
+    cfg.blockDim = dim3(NT + 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p, ns, pf);
+    if (e != cudaSuccess) return e;
+    if (plan) {
+        *plan = grpo_plan_t{};
+        plan->kernel = 8;
+        plan->ctas_per_sm = MINB;
+        plan->grid = (int32_t)(g_per * comm->n_local);
+        plan->vec_per_thread = NT;
+        plan->stages = ns;
+        plan->max_clusters = occ;
+        plan->smem_bytes = (int32_t)smem;
+        plan->lag = pf;
+    }
+    *launches += 1;
+    return cudaSuccess;
+}
+
 template <int NT, int U, int CPS>
 static cudaError_t launch_vp_plan(VpParams p, const grpo_vp_comm_t *comm, int lag, int64_t n_rows,
                                   cudaStream_t s, int *launches, grpo_plan_t *plan, char *why,
@@ -370,8 +653,17 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned lo
     p.term_ws = a.term_ws;
     p.logp_ws = a.logp_ws;
     p.flag_ws = a.flag_ws;
-    // the row-wise kernel's residency rule on the shard's row length (loss_aux.cu)
     const int n_vec = (comm->shard_cols + 7) / 8;
+    // long shards (>= 60000 columns), default schedule: the streamed ring kernel with the
+    // loss_fwd auto plan's geometry for that row length (api.cu).  On shorter shards the
+    // per-row wait for the peers' partials is a larger share of the row and the row-wise
+    // kernel is faster (R = 2 x 76032: 3.64 vs 4.0-4.2 ms; R = 4 x 38016: 2.28 vs 2.09-2.18,
+    // DESIGN.md section 9.1)
+    if (!lag && !comm->dynamic_rows && n_vec >= 11250)
+        return launch_vp_stream<512, 1, 2048>(p, comm, 6, 3, a.n_rows, s, launches, plan, why, why_len);
+    if (!lag && !comm->dynamic_rows && n_vec >= 7500)
+        return launch_vp_stream<256, 2, 1024>(p, comm, 6, 3, a.n_rows, s, launches, plan, why, why_len);
+    // the row-wise kernel's residency rule on the shard's row length (loss_aux.cu)
     if (n_vec >= 14000) return launch_vp_plan<512, 8, 2>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);
     if (n_vec >= 6000) return launch_vp_plan<256, 8, 4>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);
     return launch_vp_plan<256, 4, 8>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);

@@ -92,3 +92,44 @@ def test_vp_random_shapes(dev, seed):
                      calls=int(rng.integers(1, 3)))
     compare(gpu, ref, b, logits_pad=bits[:, b.V:])
     assert gpu["shard_pad_untouched"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_vp_stream_kernel(dev, world):
+    """Long shards (>= 60000 columns) with the default schedule run the streamed ring
+    kernel (plan kernel 8, loss_vp.cu vp_stream_kernel): several chunks and calls on the
+    same exchange buffers, forward-only, and against the row-wise VP kernel (lag 1)."""
+    import paper_2604_26256_b200 as Gp
+    rng = np.random.default_rng(70 + world)
+    V = {1: 80000, 2: 152064, 4: 262144}[world]
+    rows = [(rng.normal(size=V) * float(rng.uniform(0.5, 3)), int(rng.integers(0, V))) for _ in range(24)]
+    from tests.test_gpu_parity import _adversarial_batch
+    b, bits = _adversarial_batch(V, rows)
+    ref = run_oracle(b, bits)
+    gpu = run_gpu_vp(b, bits, dev, world, chunks=2, calls=2)
+    plan = Gp.grpo_async_last_plan()
+    assert plan["kernel"] == 8, plan
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+    assert gpu["shard_pad_untouched"]
+    old = run_gpu_vp(b, bits, dev, world, lag=1)
+    assert Gp.grpo_async_last_plan()["kernel"] == 7
+    compare(old, ref, b, logits_pad=bits[:, b.V:])
+    assert np.max(np.abs(old["logp"] - gpu["logp"])) < 1e-5
+    ref_f = run_oracle(b, bits, want_dlogits=False)
+    compare(run_gpu_vp(b, bits, dev, world, want_dlogits=False), ref_f, b, check_dlogits=False)
+
+
+def test_vp_stream_kernel_empty_shards(dev):
+    """shard_cols = 64000 over V = 80000 with world 4: ranks 2 and 3 hold no column (no
+    chunk to stream; their partial is (-inf, 0)) yet take part in the exchange."""
+    import paper_2604_26256_b200 as Gp
+    from tests.test_gpu_parity import _adversarial_batch
+    rng = np.random.default_rng(81)
+    V = 80000
+    rows = [(rng.normal(size=V) * 2.0, int(rng.integers(0, V))) for _ in range(12)]
+    b, bits = _adversarial_batch(V, rows)
+    ref = run_oracle(b, bits)
+    gpu = run_gpu_vp(b, bits, dev, 4, shard_cols=64000)
+    assert Gp.grpo_async_last_plan()["kernel"] == 8
+    compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+    assert gpu["shard_pad_untouched"]
