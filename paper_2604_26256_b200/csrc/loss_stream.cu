@@ -51,17 +51,23 @@ struct Geometry {
 };
 
 template <int CHUNK_VECS>
-__device__ __forceinline__ Geometry geometry(const Params &p, bool two_pass) {
+__device__ __forceinline__ Geometry geometry(const Params &p, int V, bool two_pass) {
     Geometry g;
-    g.n_vec = (p.V + 7) / 8;
+    g.n_vec = (V + 7) / 8;
     g.n = (g.n_vec + CHUNK_VECS - 1) / CHUNK_VECS;
     g.R = two_pass ? min(g.n, max(0, p.ns - p.pf)) : 0;
     g.loads = two_pass ? 2 * g.n - g.R : g.n;
-    g.tail_valid = p.V - (g.n_vec - 1) * 8;
+    g.tail_valid = V - (g.n_vec - 1) * 8;
     return g;
 }
 
-template <int NT, int MINB, int CHUNK_VECS>
+// SPLIT = 2: a cluster of two CTAs (two SMs) shares each row, CTA r streaming vectors
+// [r*h, ...) of it (h = ceil(ceil(V/8)/2)); after pass 1 the two (max, sum) partials cross
+// through distributed shared memory (st.async onto the partner's mbarrier, one buffer per
+// row parity) and both CTAs merge them in rank order, so they hold identical row scalars.
+// Halving the row halves the time between a chunk's pass-1 load and its pass-2 re-load, so
+// at V = 262144 (512 KB rows) the re-loads stay in L2.
+template <int NT, int MINB, int CHUNK_VECS, int SPLIT>
 __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
     constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr int U = CHUNK_VECS / NT;  // vectors per consumer thread per chunk
@@ -72,8 +78,14 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
     uint64_t *empty = full + p.ns;
     __shared__ float2 red[NW];
     __shared__ float row_scalars[4];
+    __shared__ float2 xbuf[2];
+    __shared__ __align__(8) uint64_t xbar[2];
     const bool two_pass = p.dlogits != nullptr;
-    const Geometry g = geometry<CHUNK_VECS>(p, two_pass);
+    const uint32_t crank = SPLIT == 2 ? cluster_ctarank() : 0u;
+    const int hv = ((p.V + 7) / 8 + 1) / 2;
+    const int col0 = SPLIT == 2 ? (int)crank * hv * 8 : 0;              // first column of the slice
+    const int Vloc = SPLIT == 2 ? (crank == 0 ? hv * 8 : p.V - hv * 8) : p.V;  // its width
+    const Geometry g = geometry<CHUNK_VECS>(p, Vloc, two_pass);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -81,11 +93,15 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, NW);
         }
+        mbar_init(xbar, 1);
+        mbar_init(xbar + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    if (SPLIT == 2) cluster_sync_all();  // the partner's barriers exist before any st.async
+    else __syncthreads();
 
-    const int64_t row0 = blockIdx.x, rstep = gridDim.x;
+    const int64_t row0 = SPLIT == 2 ? (int64_t)cluster_id_x() : (int64_t)blockIdx.x;
+    const int64_t rstep = SPLIT == 2 ? (int64_t)ncluster_x() : (int64_t)gridDim.x;
     if (warp == NW) {
         // ------------------------------------------------------------ producer
         if (lane == 0) {
@@ -94,7 +110,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
             int slot = 0;
             uint32_t par = 0;  // parity of the slot's current use
             for (int64_t row = row0; row < p.n_rows; row += rstep) {
-                const uint8_t *src = reinterpret_cast<const uint8_t *>(p.logits + row * p.ld);
+                const uint8_t *src = reinterpret_cast<const uint8_t *>(p.logits + row * p.ld + col0);
                 for (int i = 0; i < g.loads; ++i) {
                     const int c = i < g.n ? i : i - g.n;  // chunk (pass-1 load or re-load)
                     mbar_wait(empty + slot, par ^ 1u);
@@ -118,7 +134,8 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
     const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
     int slot = 0;      // slot of the next load this CTA consumes
     uint32_t par = 0;  // and the parity of that slot's use
-    for (int64_t row = row0; row < p.n_rows; row += rstep) {
+    uint32_t rowk = 0;  // rows this CTA has done (exchange buffer rowk & 1, parity rowk >> 1)
+    for (int64_t row = row0; row < p.n_rows; row += rstep, ++rowk) {
         const int base_slot = slot;  // slot of this row's pass-1 chunk 0
         // the epilogue's two dependent global reads (row info, then z_y), issued now so
         // that they complete under pass 1 instead of stalling the whole CTA at its end
@@ -167,6 +184,19 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
         if (warp == 0) {
             float cm = lane < NW ? red[lane].x : -INFINITY, cs = lane < NW ? red[lane].y : 0.0f;
             warp_lse2_combine(cm, cs);
+            if (SPLIT == 2 && lane == 0) {
+                const int b = rowk & 1;
+                mbar_arrive_expect_tx(xbar + b, 8);
+                st_async_v2(mapa_shared(smem_u32(xbuf + b), crank ^ 1u),
+                            mapa_shared(smem_u32(xbar + b), crank ^ 1u), cm, cs);
+                mbar_wait_cluster(xbar + b, (rowk >> 1) & 1u);
+                const float2 o = xbuf[b];
+                // rank order on both CTAs: bit-identical row scalars
+                float m0 = crank == 0 ? cm : o.x, s0 = crank == 0 ? cs : o.y;
+                lse2_merge(m0, s0, crank == 0 ? o.x : cm, crank == 0 ? o.y : cs);
+                cm = m0;
+                cs = s0;
+            }
             if (lane == 0) {
                 const bool y_valid = ri.target >= 0 && ri.target < p.V;
                 const float zy = y_valid ? __uint_as_float(((uint32_t)zy_bits) << 16) : __int_as_float(0x7FC00000);
@@ -175,12 +205,14 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
                 const double logp_d = row_logp(zy, cm, l2s);
                 const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                 const float logp = (float)logp_d;
-                if (p.logp_out) p.logp_out[row] = logp;
-                if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
-                if (p.scale_out) p.scale_out[row] = o.s;
-                p.term_ws[row] = o.term;
-                p.logp_ws[row] = logp;
-                p.flag_ws[row] = o.flags;
+                if (crank == 0) {
+                    if (p.logp_out) p.logp_out[row] = logp;
+                    if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
+                    if (p.scale_out) p.scale_out[row] = o.s;
+                    p.term_ws[row] = o.term;
+                    p.logp_ws[row] = logp;
+                    p.flag_ws[row] = o.flags;
+                }
                 row_scalars[0] = lse2;
                 row_scalars[1] = o.s;
                 row_scalars[2] = zy;
@@ -192,9 +224,10 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
         // ---- pass 2: resident chunks n-R..n-1 (loads base+n-R..), then the re-loads
         const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
             const auto gref = RowwiseBatch<NT, U>::grad_ref(sc, lse2);
-        const int32_t y = __float_as_int(row_scalars[3]);
+        const int32_t yfull = __float_as_int(row_scalars[3]);
+        const int32_t y = (yfull >= col0 && yfull < col0 + Vloc) ? yfull - col0 : -1;  // in this slice
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
-        uint16_t *drow = p.dlogits + row * p.ld;
+        uint16_t *drow = p.dlogits + row * p.ld + col0;
         uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
         for (int i = 0; i < g.n; ++i) {
             const bool resident = i < g.R;
@@ -275,6 +308,13 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
     const int cps = (tune && tune->row_cache == 2) ? 2 : 1;
     const int ckb = (tune && (tune->chunk_kb == 24 || tune->chunk_kb == 32 || tune->chunk_kb == 48 ||
                               tune->chunk_kb == 64)) ? tune->chunk_kb : 16;
+    // cluster_size 2: two SMs per row (SPLIT = 2; one 512-thread CTA per SM, 16 or 32 KB slots)
+    const int split = (tune && tune->cluster_size == 2) ? 2 : 1;
+    if (split == 2 && (cps != 1 || nt != 512 || (ckb != 16 && ckb != 32) || a.V < 16384)) {
+        if (why) snprintf(why, why_len, "stream kernel: cluster_size 2 needs 512 threads, 1 CTA per SM, "
+                          "16 or 32 KB slots and V >= 16384");
+        return cudaErrorInvalidValue;
+    }
     const int max_ns = (cps == 2 ? 96 : 208) / ckb;
     if (!(tune && tune->stages > 0)) p.ns = max_ns;
     if (p.ns < 2 || p.ns > max_ns || p.pf >= p.ns) {
@@ -286,14 +326,41 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)std::min<int64_t>(a.n_rows, (int64_t)n_sm * cps);
+    int grid = (int)std::min<int64_t>(a.n_rows, (int64_t)n_sm * cps);
     cudaError_t e;
+    if (split == 2) {
+        // one cluster per row in flight: as many clusters as can be co-resident (an SM pair
+        // must sit in one GPC, so this can be below n_sm / 2)
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.blockDim = dim3(512 + 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        auto kfn = ckb == 32 ? stream_kernel<512, 1, 2048, 2> : stream_kernel<512, 1, 1024, 2>;
+        e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int max_clusters = 0;
+        cfg.gridDim = dim3(n_sm);
+        e = cudaOccupancyMaxActiveClusters(&max_clusters, kfn, &cfg);
+        if (e != cudaSuccess) return e;
+        if (max_clusters < 1) max_clusters = 1;
+        grid = 2 * (int)std::min<int64_t>(a.n_rows, (int64_t)max_clusters);
+        cfg.gridDim = dim3(grid);
+        e = cudaLaunchKernelEx(&cfg, kfn, p);
+        if (e != cudaSuccess) return e;
+    } else {
 #define GRPO_K3C(NT_, MB_, CV_)                                                                         \
     do {                                                                                               \
-        e = cudaFuncSetAttribute(stream_kernel<NT_, MB_, CV_>,                                         \
+        e = cudaFuncSetAttribute(stream_kernel<NT_, MB_, CV_, 1>,                                         \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
         if (e != cudaSuccess) return e;                                                                \
-        stream_kernel<NT_, MB_, CV_><<<grid, NT_ + 32, smem, s>>>(p);                                  \
+        stream_kernel<NT_, MB_, CV_, 1><<<grid, NT_ + 32, smem, s>>>(p);                                  \
     } while (0)
     if (ckb == 64) {
         GRPO_K3C(512, 1, 4096);
@@ -313,6 +380,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
         else GRPO_K3C(256, 2, 1024);
     }
 #undef GRPO_K3C
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     *launches += 1;
@@ -320,6 +388,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
         *plan = grpo_plan_t{};
         plan->kernel = 3;
         plan->ctas_per_sm = cps;
+        plan->cluster_size = split;
         plan->stages = p.ns;
         plan->lag = p.pf;
         plan->vec_per_thread = nt;

@@ -318,10 +318,11 @@ def test_odd_vocabulary_sizes(dev, V):
 def test_auto_plan_choice(dev):
     """The auto plan (tune kernel 0): K3b below V = 34000, K3c with two 256-thread CTAs per
     SM and 16 KB slots up to V = 90000, K3c with one CTA per SM and 32 KB slots from there
-    on (DESIGN.md section 8 measurements); an explicitly tuned call is never redirected."""
+    on, each row split over a two-CTA cluster from V = 200000 (DESIGN.md section 8
+    measurements); an explicitly tuned call is never redirected."""
     import paper_2604_26256_b200 as Gp
     for V, kernel, cps in ((30000, 2, None), (34000, 3, 2), (76032, 3, 2), (89990, 3, 2),
-                           (90000, 3, 1), (152064, 3, 1)):
+                           (90000, 3, 1), (152064, 3, 1), (199999, 3, 1), (200000, 3, 1), (262144, 3, 1)):
         rows = [(np.random.default_rng(V).normal(size=V), 3) for _ in range(4)]
         b, bits = _adversarial_batch(V, rows)
         ref = run_oracle(b, bits)
@@ -332,6 +333,7 @@ def test_auto_plan_choice(dev):
             assert plan["stages"] == 6 and plan["ctas_per_sm"] == cps, (V, plan)
             assert plan["smem_bytes"] >= 6 * (32768 if cps == 1 else 16384)
             assert plan["vec_per_thread"] == (512 if cps == 1 else 256), (V, plan)
+            assert plan["cluster_size"] == (2 if V >= 200000 else 1), (V, plan)
         compare(gpu, ref, b, logits_pad=bits[:, b.V:])
     run_gpu(b, bits, dev, tune={"kernel": 2, "stages": 8})
     assert Gp.grpo_async_last_plan()["kernel"] == 2
@@ -423,4 +425,34 @@ def test_random_shapes_and_plans(dev, seed):
     for tune in plans:
         gpu = run_gpu(b, bits, dev, tune=tune, chunks=int(rng.integers(1, 4)),
                       inplace=bool(rng.integers(0, 2)))
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+
+
+SPLIT_PLANS = [{"kernel": 3, "cluster_size": 2, "chunk_kb": kb, "stages": ns, "lag": pf}
+               for kb, ns, pf in ((32, 6, 3), (32, 6, 1), (32, 2, 1), (16, 13, 3), (16, 3, 2))]
+
+
+@pytest.mark.parametrize("plan", SPLIT_PLANS,
+                         ids=lambda d: f"kb{d['chunk_kb']}ns{d['stages']}pf{d['lag']}")
+def test_stream_split_rows(dev, plan):
+    """K3c with each row shared by a cluster of two CTAs (cluster_size 2, the DSMEM exchange
+    of the two (max, sum) partials): configs with V = 152064 and 262144 in two chunks, forward
+    only, and odd vocabularies whose halves end in a ragged vector, against the oracle."""
+    for name in ("mid152k", "large_small"):
+        b, bits = _case(name, 9)
+        ref = run_oracle(b, bits)
+        gpu = run_gpu(b, bits, dev, tune=plan, chunks=2)
+        compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+    ref = run_oracle(b, bits, want_dlogits=False)
+    gpu = run_gpu(b, bits, dev, tune=plan, want_dlogits=False)
+    compare(gpu, ref, b, check_dlogits=False)
+    for V in (16384, 16391, 32777, 90007):
+        rng = np.random.default_rng(V)
+        # targets in the first half, the second half, at both ends and on the split column
+        h = (((V + 7) // 8 + 1) // 2) * 8
+        tg = [0, V - 1, h - 1, h, int(rng.integers(0, V)), int(rng.integers(0, V)), h + 1, 5]
+        rows = [(rng.normal(size=V) * 2, t) for t in tg]
+        b, bits = _adversarial_batch(V, rows)
+        ref = run_oracle(b, bits)
+        gpu = run_gpu(b, bits, dev, tune=plan)
         compare(gpu, ref, b, logits_pad=bits[:, b.V:])
