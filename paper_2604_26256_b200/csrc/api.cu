@@ -409,7 +409,7 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
         // free slots at the end of pass 1: 3, or 1 on very long rows (> 14 slots of
         // 32 KB) where the re-read part of every SM's row would crowd L2
         stream_tune.lag = (n_vec_row + 2047) / 2048 > 14 ? 1 : 3;
-        if (n_vec_row >= 25000) {
+        if (V >= 200000) {
             stream_tune.cluster_size = 2;
             stream_tune.lag = 3;
         }
