@@ -141,25 +141,65 @@ def load_oracle():
     return O, int(os.environ["OMP_NUM_THREADS"])
 
 
-def cpu_baseline(batch, seconds):
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(batch, seconds, block=512):
+    """The oracle (fp64, all host cores) timed on whole trajectories covering the first
+    >= 8192 rows of the batch, in blocks of `block` rows, repeated for
+    ~`seconds`; plus a single-core figure on the first 1024 rows.  Input generation (the
+    logits' bf16 bits) happens before the timer."""
     O, cores = load_oracle()
-    rows, _ = oracle_sample(batch, 512)
-    bits = batch.logits_bits(rows)
-    oracle_step(O, batch, rows[:8], bits[:8], 0.2)   # load / warm
+    rows, n_traj = oracle_sample(batch, 8192)
+    blocks = [rows[i:i + block] for i in range(0, len(rows), block)]
+    bits = [batch.logits_bits(b) for b in blocks]
+
+    def one_pass(n_blocks):
+        O.validate(batch.version_ids, batch.cu_seqlens, batch.group_ids, batch.target_ids,
+                   P=batch.P, V=batch.V, G=batch.G, tbs=batch.tbs, v_theta=batch.v_theta, K=batch.K,
+                   token_version=batch.token_version, logp_behav=batch.logp_behav)
+        adv, inv, _ = O.advantage(batch.rewards, batch.group_ids, batch.cu_seqlens, batch.P)
+        for b, bb in zip(blocks[:n_blocks], bits[:n_blocks]):
+            O.rows(b, bb, batch.V, batch.target_ids[b], batch.logp_behav[b], batch.cu_seqlens,
+                   adv, inv, 0.2, 1.0, want_dlogits=True)
+        return sum(len(b) for b in blocks[:n_blocks])
+
+    O.rows(blocks[0][:4], bits[0][:4], batch.V, batch.target_ids[blocks[0][:4]],
+           batch.logp_behav[blocks[0][:4]], batch.cu_seqlens,
+           np.zeros(batch.N), np.zeros(batch.N), 0.2, 1.0)   # load / warm
     t0 = time.perf_counter()
-    n = 0
-    reps = 0
+    n = reps = 0
     while True:
-        oracle_step(O, batch, rows, bits, 0.2)
-        n += len(rows)
+        n += one_pass(len(blocks))
         reps += 1
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
+    single = None
+    try:  # the same OpenMP runtime the oracle library uses, limited to one thread
+        import ctypes
+        gomp = ctypes.CDLL("libgomp.so.1")
+        gomp.omp_set_num_threads(1)
+        t1 = time.perf_counter()
+        n1 = one_pass(2)
+        single = n1 / (time.perf_counter() - t1)
+        gomp.omp_set_num_threads(cores)
+    except OSError:
+        pass
     return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{len(rows)} rows (whole trajectories covering the first 512 rows of "
-                      f"'{batch.cfg.name}', V={batch.V}) x {reps} repetitions, fwd+bwd fp64 "
-                      f"incl. validate+advantage over the full batch; {dt:.1f} s"}
+            "cpu_model": cpu_model(), "single_core_value": single,
+            "sample": f"{len(rows)} rows (whole trajectories covering the first 8192 rows of "
+                      f"'{batch.cfg.name}', V={batch.V}, {n_traj} trajectories) x {reps} "
+                      f"repetitions, fwd+bwd fp64 incl. validate+advantage over the full batch; "
+                      f"{dt:.1f} s; single core: the first {sum(len(b) for b in blocks[:2])} rows"}
 
 
 def run_reference(args):
@@ -238,19 +278,23 @@ def main():
     def pinned(x, dt):
         return torch.from_numpy(np.ascontiguousarray(x)).to(dt).pin_memory()
 
+    # replicated O(N) trajectory metadata + this rank's token arrays only
     host = {
         "cu": pinned(batch.cu_seqlens, torch.int64), "gid": pinned(batch.group_ids, torch.int32),
         "ver": pinned(batch.version_ids, torch.int64), "rew": pinned(batch.rewards, torch.float32),
-        "tgt": pinned(batch.target_ids, torch.int64), "lw": pinned(batch.logp_behav, torch.float32),
         "tgt_l": pinned(batch.target_ids[rows_g], torch.int64),
         "lw_l": pinned(batch.logp_behav[rows_g], torch.float32),
         "cu_l": pinned(local_cu, torch.int64), "tix": pinned(mine.astype(np.int32), torch.int32),
     }
     if batch.token_version is not None:
-        host["tv"] = pinned(batch.token_version, torch.int64)
+        host["tv_l"] = pinned(batch.token_version[rows_g], torch.int64)
     d = {k: v.to(dev) for k, v in host.items()}
-    db = G.DeviceBatch(batch.P, batch.G, batch.K, V, ld, batch.tbs, batch.v_theta, d["cu"],
-                       d["gid"], d["ver"], d["rew"], d["tgt"], d["lw"], d.get("tv"))
+
+    def sharded(dd):
+        return G.ShardedBatch(batch.P, batch.G, batch.K, V, ld, batch.tbs, batch.v_theta, batch.T,
+                              dd["cu"], dd["gid"], dd["ver"], dd["rew"], dd["cu_l"], dd["tix"],
+                              dd["tgt_l"], dd["lw_l"], dd.get("tv_l"))
+    sb = sharded(d)
 
     # ---- resident logits buffer (device-generated, bit-identical to synth/gen.py) and dlogits
     logits = torch.empty((R, ld), dtype=torch.int16, device=dev)
@@ -269,21 +313,37 @@ def main():
     adv = torch.empty(batch.N, dtype=torch.float32, device=dev)
     inv = torch.empty(batch.N, dtype=torch.float32, device=dev)
     traj_sum = torch.zeros(len(mine), dtype=torch.float64, device=dev)
-    stats = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
+    # this rank's packed fp64 partials: the loss stats, then the token-level validation counts
+    NP = G.NUM_STATS + 3
+    packed = torch.zeros(NP, dtype=torch.float64, device=dev)
+    stats, tok_counts = packed[:G.NUM_STATS], packed[G.NUM_STATS:]
+    glob = torch.zeros(NP, dtype=torch.float64, device=dev)   # the batch's, on every rank
+    gathered = torch.zeros((world, NP), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step(dbx=db, tgt=d["tgt_l"], lw=d["lw_l"], cu_l=d["cu_l"], tix=d["tix"]):
-        loss.validate(dbx, vo)
-        loss.advantage(dbx, adv, inv)
+    def allgather(t):
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, t)
+        else:
+            gathered[0].copy_(t)
+        return gathered
+
+    def step(sbx=sb):
+        loss.validate_local(sbx, vo, token_counts=tok_counts)
+        loss.advantage(sbx, adv, inv)
         traj_sum.zero_()
         stats.zero_()
         for c in range(n_chunks):
             b = c * R
             n = min(R, T_local - b)
-            loss.loss_chunk(logits[:n], b, n, tgt[b:b + n], lw[b:b + n], cu_l, adv, inv,
-                            traj_sum, stats, dlogits=dlogits[:n], traj_index=tix, V=V)
-        if world > 1:
-            dist.all_reduce(stats)   # the path's one exchange: packed fp64 partials
+            loss.loss_chunk(logits[:n], b, n, sbx.target_ids[b:b + n], sbx.logp_behav[b:b + n],
+                            sbx.local_cu, adv, inv, traj_sum, stats, dlogits=dlogits[:n],
+                            traj_index=sbx.traj_index, V=V)
+        # the path's one exchange: every rank's packed partials all-gathered, summed in rank
+        # order by grpo_async_combine_ranks (bit-identical everywhere, run to run), and the
+        # summed token counts completing the validation verdict
+        loss.combine_ranks(packed, world, allgather=allgather, out=glob)
+        loss.validate_combine(vo, glob[G.NUM_STATS:])
 
     def barrier():
         if world > 1:
@@ -333,15 +393,15 @@ def main():
     clocks = sampler.stop() if sampler else None
     ms_max = max_over_ranks(ms)
     kern_ms_max = max_over_ranks(kern_ms)
-    stats_h = stats.cpu().numpy()
+    stats_h = glob.cpu().numpy()
     summ = vo.summary_dict()
 
     T_total = batch.T
     value = T_total * args.steps / (ms_max / 1e3)
     peak, peak_src = measured_peaks()
     # algorithmic bytes of the fused kernel per row: read the bf16 row (2V), write the bf16
-    # dlogits row (2V), read 16 B row metadata, write term/logp/flag (9 B)
-    bytes_per_row = 4 * V + 25
+    # dlogits row (2V), read 16 B row metadata, write term (fp64) / logp / flag (13 B)
+    bytes_per_row = 4 * V + 29
     rows_per_launch = T_local / n_chunks
     avg_launch_ms = kern_ms / max(n_traced, 1)
     achieved = bytes_per_row * rows_per_launch / (avg_launch_ms / 1e3) / 1e9
@@ -357,22 +417,20 @@ def main():
     # ---- end to end through the public API with host buffers (pinned H2D, D2H of the result)
     e2e = None
     if not args.no_e2e:
-        keys_h2d = ["cu", "gid", "ver", "rew", "tgt", "lw", "tgt_l", "lw_l", "cu_l", "tix"] + \
-            (["tv"] if "tv" in host else [])
+        keys_h2d = list(host.keys())
         dd = {k: torch.empty_like(d[k]) for k in keys_h2d}
         h2d = sum(host[k].numel() * host[k].element_size() for k in keys_h2d)
-        out_host = torch.empty(G.NUM_STATS + len(G.SUMMARY_FIELDS), dtype=torch.float64).pin_memory()
+        sbx = sharded(dd)
+        out_host = torch.empty(NP + len(G.SUMMARY_FIELDS), dtype=torch.float64).pin_memory()
         d2h = out_host.numel() * 8
-        dbx = G.DeviceBatch(batch.P, batch.G, batch.K, V, ld, batch.tbs, batch.v_theta, dd["cu"],
-                            dd["gid"], dd["ver"], dd["rew"], dd["tgt"], dd["lw"], dd.get("tv"))
-        res_dev = torch.empty(G.NUM_STATS + len(G.SUMMARY_FIELDS), dtype=torch.float64, device=dev)
+        res_dev = torch.empty(NP + len(G.SUMMARY_FIELDS), dtype=torch.float64, device=dev)
 
         def e2e_step():
             for k in keys_h2d:
                 dd[k].copy_(host[k], non_blocking=True)
-            step(dbx, dd["tgt_l"], dd["lw_l"], dd["cu_l"], dd["tix"])
-            res_dev[:G.NUM_STATS].copy_(stats)
-            res_dev[G.NUM_STATS:].copy_(vo.summary)
+            step(sbx)
+            res_dev[:NP].copy_(glob)
+            res_dev[NP:].copy_(vo.summary)
             out_host.copy_(res_dev, non_blocking=True)
 
         for _ in range(2):
@@ -389,10 +447,12 @@ def main():
         e2e = {"value": T_total * args.steps / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": e2e_ms / args.steps,
-               "note": "per step: pinned H2D of the batch metadata (targets, behaviour "
-                       "log-probs, cu_seqlens, group ids, versions, rewards), the whole path, "
-                       "D2H of stats+validation summary; logits are device-resident activations "
-                       "of the LM forward and are not copied"}
+               "note": "per step and rank: pinned H2D of the replicated trajectory metadata "
+                       "(cu_seqlens, group ids, versions, rewards) and of this rank's token "
+                       "arrays (targets, behaviour log-probs, token versions, local packing), "
+                       "the whole path, D2H of the combined partials + validation summary; "
+                       "logits are device-resident activations of the LM forward and are not "
+                       "copied"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -416,8 +476,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "frac_of_spec_8000_gbs": achieved / 8000.0,
-                         "kernel": {1: "fused_cluster_kernel", 2: "rowwise_kernel",
-                                    3: "stream_kernel"}.get(
+                         "kernel": {2: "rowwise_kernel", 3: "stream_kernel"}.get(
                              plan["kernel"], str(plan["kernel"])),
                          "plan": plan,
                          "bytes_per_row": bytes_per_row, "launches": n_traced,

@@ -128,7 +128,9 @@ typedef struct {
     int32_t lag;           /* 0 auto, else 1..2: rows between a row's reduction and its       */
                            /* backward, hiding the cluster exchange (kernel 1); kernel 3:    */
                            /* ring slots left free at the end of pass 1 (0 = 3)              */
-    int32_t prefetch;      /* kernel 2: 1 = TMA-prefetch each CTA's next row into L2         */
+    int32_t prefetch;      /* kernel 2: 1 = TMA-prefetch each CTA's next row into L2;        */
+                           /* kernel 3: chunks of the next row streamed before a row's pass */
+                           /* 2, hiding its epilogue (0 = 2; capped at stages - resident)   */
     int32_t row_cache;     /* kernel 2: leading vectors per thread of each row kept in shared */
                            /* memory for the second pass (0 auto = 160 KB per SM, -1 none); */
                            /* kernel 3: CTAs per SM, 1 (default) or 2                        */
@@ -171,6 +173,54 @@ grpo_status_t grpo_async_validate_sync(const int64_t *version_ids, const int64_t
                                        int32_t *stale_hist, grpo_validate_summary_t *summary,
                                        grpo_validate_summary_t *host_summary,
                                        grpo_stream_t stream);
+
+/*
+ * grpo_async_validate_local -- grpo_async_validate for one rank of a trajectory-sharded batch
+ * (the paper's trainer spreads one batch over the GPUs of a node): the
+ * trajectory-level checks (C3 gap P:39, C2 group counts and TBS P:46-49, zero length, group
+ * ids, the |B_j| histogram) run over all N trajectories of the replicated metadata, the
+ * token-level checks (C1 P:44, target range, behaviour log-probs) only over this rank's
+ * trajectories, from its own token arrays:
+ *   version_ids int64[N], cu_seqlens int64[N+1] (global packing), group_ids int32[N];
+ *   local_cu int64[n_local+1]: local trajectory j owns rows [local_cu[j], local_cu[j+1]) of
+ *   the local token arrays and is global trajectory traj_index[j] (int32[n_local]);
+ *   token_version_local (nullable), target_ids_local, logp_behav_local (nullable): local rows.
+ * Outputs as grpo_async_validate, except that the summary's token-level counts
+ * (n_c1_mixed, n_bad_target, n_bad_logp_behav) and the verdicts that use them (c1_ok,
+ * valid) cover this rank's trajectories, and traj_flags carries token bits only for them.
+ * token_counts (double[3], nullable) receives those three counts as exact doubles, to be
+ * summed over the ranks with the loss partials; grpo_async_validate_combine then writes the
+ * sums into the summary and recomputes c1_ok / valid -- the whole batch's verdict, identical
+ * on every rank.  n_local = N with traj_index = identity and local_cu = cu_seqlens is
+ * grpo_async_validate.  All pointers are device pointers; stream-ordered, no sync.
+ * Errors: GRPO_ERR_INVALID_ARG (NULL required pointers, bad sizes, n_local > N).
+ */
+grpo_status_t grpo_async_validate_local(const int64_t *version_ids, const int64_t *cu_seqlens,
+                                        const int32_t *group_ids, int32_t N, int64_t T, int32_t P,
+                                        int32_t V, int32_t G, int32_t tbs, int64_t v_theta,
+                                        int32_t K, const int64_t *local_cu,
+                                        const int32_t *traj_index, int32_t n_local,
+                                        const int64_t *token_version_local,
+                                        const int64_t *target_ids_local,
+                                        const float *logp_behav_local, uint32_t *traj_flags,
+                                        int32_t *group_count, int32_t *stale_hist,
+                                        grpo_validate_summary_t *summary, double *token_counts,
+                                        grpo_stream_t stream);
+grpo_status_t grpo_async_validate_combine(grpo_validate_summary_t *summary,
+                                          const double *token_counts, grpo_stream_t stream);
+
+/*
+ * grpo_async_combine_ranks -- the data-parallel step's one exchange: after the
+ * caller all-gathers every rank's packed fp64 partials (the stats of grpo_async_loss_fwd,
+ * i.e. this rank's share of J = sum_t inv_norm_i term_t of eq:grpo_async P:9-26, plus the
+ * token-level validation counts) into gathered[world][n] in rank order,
+ *   out[k] = gathered[0][k] + gathered[1][k] + ... + gathered[world-1][k]
+ * summed in that order -- the same bits on every rank and in every run (a collective's
+ * SUM has no fixed order).  Device pointers; out may not alias gathered.
+ * Errors: GRPO_ERR_INVALID_ARG (world < 1, n < 0, NULL pointers).
+ */
+grpo_status_t grpo_async_combine_ranks(const double *gathered, int32_t world, int32_t n,
+                                       double *out, grpo_stream_t stream);
 
 /*
  * grpo_async_advantage -- group-relative advantages, eq:group_advantage.
@@ -376,7 +426,10 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
  *   recomputes z tile by tile and writes dz = grad_scale_mult * s_t (softmax(z) - onehot(y))
  *   as bf16 [n_rows, ld_dz] (ld_dz >= V, multiple of 8; columns [V, ld_dz) untouched), then
  *   dhidden = dz W (bf16 [n_rows, d], NULL to skip) and dW += dz^T hidden (f32 [V, d],
- *   accumulated so chunks add up; NULL to skip) as two cuBLAS GEMMs.
+ *   accumulated so chunks add up; NULL to skip) as two tcgen05 GEMMs (lmhead_dx.cu: dz read
+ *   K-major for dX and MN-major -- transposed in the descriptor, not in memory -- for dW).
+ * grpo_async_lmhead_dx -- dhidden = dz W alone from an existing dz (bf16 [n_rows, ld_dz]):
+ *   dhidden bf16 (out_bf16 = 1) or f32 [n_rows, d]; the unfused pipeline's dX GEMM.
  * grpo_async_lmhead_logits -- the plain logits hidden W^T as bf16 [n_rows, ld_out] (the
  *   unfused producer for grpo_async_loss_fwd, and the check of the GEMM).
  * Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_WORKSPACE, GRPO_ERR_CUDA.
@@ -387,8 +440,9 @@ size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N);
  * Tensor-parallel LM head (NEXT(2) in the trainer's Megatron layout; NEXT(3)'s
  * vocabulary split): rank q holds W rows [col_offset, col_offset + Vs) and the full hidden
  * states.  Forward: grpo_async_lmhead_tp_partials computes this shard's per-row partial
- *   row_part[4*row .. 4*row+3] = (max, sum 2^(t - max) in log2 units, z_y, 1 if this shard
- *   holds y_t else 0)   (float; workspace: grpo_async_lmhead_workspace_size(n_rows, Vs, 1));
+ *   row_part[4*row .. 4*row+3] = 16 opaque bytes per row: (max in log2 units as float, z_y
+ *   as float, the sum of 2^(t - max) as a double whose sign bit says "this shard holds
+ *   y_t")   (workspace: grpo_async_lmhead_workspace_size(n_rows, Vs, 1));
  * the caller all-gathers the R ranks' row_part arrays in rank order ([R][n_rows][4]) and
  * grpo_async_lmhead_tp_fwd finishes logp / lse / token_scale / traj_sum / stats identically on
  * every rank (arguments as grpo_async_lmhead_fwd; workspace grpo_async_workspace_size).
@@ -425,23 +479,32 @@ grpo_status_t grpo_async_lmhead_tp_bwd(const uint16_t *hidden, const uint16_t *W
  * and its epilogue stores each f32 tile of rows r into slot `rank` of the rank that owns r
  * (rows_per_rank = ceil(n_rows / world); rank q owns rows [q*rpr, (q+1)*rpr)).
  *   slots[q]  device pointer (peer mapping) of rank q's slot buffer, f32
- *             [world][rows_per_rank][d], for q < world (host array of world pointers)
+ *             [2][world][rows_per_rank][d], for q < world (host array of world pointers)
+ *   epoch     the caller's count of tp_dx calls on these slots: call e writes half e % 2
  * After every rank's grpo_async_lmhead_tp_dx has completed (a group barrier, e.g. a NCCL
- * collective on the same stream), grpo_async_lmhead_tp_dx_reduce sums this rank's world slots
- * in rank order into out [rows owned, d] (f32, or bf16 with out_bf16 = 1): deterministic.
+ * collective on the same stream), grpo_async_lmhead_tp_dx_reduce (same epoch) sums this rank's
+ * world slots of that half in rank order into out [rows owned, d] (f32, or bf16 with
+ * out_bf16 = 1): deterministic.  The two halves make one barrier per call enough: a fast rank
+ * can write call e+1 while a slow one still reduces call e, and it reaches call e+2 (the half
+ * of call e again) only after the barrier of call e+1, i.e. after every rank's reduce of e.
  * d % 128 == 0, world <= GRPO_VP_MAX_RANKS.  Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT,
  * GRPO_ERR_CUDA.
  */
 grpo_status_t grpo_async_lmhead_tp_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W_shard,
                                       int64_t n_rows, int32_t d, int32_t Vs, int32_t world,
-                                      int32_t rank, float *const *slots, grpo_stream_t stream);
+                                      int32_t rank, float *const *slots, uint32_t epoch,
+                                      grpo_stream_t stream);
 grpo_status_t grpo_async_lmhead_tp_dx_reduce(const float *own_slots, int32_t world, int64_t n_rows,
                                              int32_t d, int32_t rank, void *out, int32_t out_bf16,
-                                             grpo_stream_t stream);
+                                             uint32_t epoch, grpo_stream_t stream);
+
+grpo_status_t grpo_async_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W,
+                                   int64_t n_rows, int32_t d, int32_t V, void *dhidden,
+                                   int32_t out_bf16, grpo_stream_t stream);
 
 /* dW (+)= dz^T hidden from an existing dz (bf16 [n_rows, ld_dz], as written by
  * grpo_async_lmhead_bwd / _tp_bwd), f32 [V, d] accumulated: lets a caller run the dW GEMM
- * while the tensor-parallel dhidden all-reduce is in flight.  cuBLAS GEMM (bf16 in, f32 out).
+ * while the tensor-parallel dhidden all-reduce is in flight.  tcgen05 GEMM (bf16 in, f32 out).
  * Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_CUDA. */
 grpo_status_t grpo_async_lmhead_dw(const uint16_t *hidden, int64_t n_rows, int32_t d, int32_t V,
                                    const uint16_t *dz, int64_t ld_dz, float *dW,

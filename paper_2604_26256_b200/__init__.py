@@ -9,10 +9,11 @@ Importing it without the built library raises (there is no CPU fallback).
 from ._lib import (  # noqa: F401
     grpo_async_advantage, grpo_async_advantage_ex, grpo_async_loss_bwd, grpo_async_loss_fwd,
     grpo_async_loss_fwd_ex, grpo_async_validate, NORM_SEQ, NORM_TOKEN,
+    grpo_async_validate_local, grpo_async_validate_combine, grpo_async_combine_ranks,
     grpo_async_validate_sync, grpo_async_workspace_size, grpo_last_error,
     grpo_last_launch_count, grpo_version, grpo_profile_enable, grpo_profile_collect, grpo_async_last_plan, GrpoError, FLAG_NAMES, SUMMARY_FIELDS, NUM_STATS,
     STAT_J, STAT_ROWS, STAT_CLIPPED, STAT_ACTIVE, STAT_ABS, STAT_LOGP, LIB_PATH)
-from .api import (DeviceBatch, GrpoAsyncLoss, ValidateOut, VpGroup, lpt_partition,  # noqa: F401
-                  shard_rows)
+from .api import (DeviceBatch, GrpoAsyncLoss, ShardedBatch, ValidateOut, VpGroup,  # noqa: F401
+                  lpt_partition, shard_rows)
 
 __version__ = "0.1.0"

@@ -30,7 +30,8 @@ SUMMARY_FIELDS = ("n_traj", "n_tokens", "n_stale", "n_future", "n_zero_len", "n_
                   "n_groups_wrong_size", "c2_dropped", "max_staleness", "min_staleness",
                   "cu_ok", "tbs_ok", "c1_ok", "c2_ok", "c3_ok", "valid")
 
-EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advantage",
+EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_validate_local",
+            "grpo_async_validate_combine", "grpo_async_combine_ranks", "grpo_async_advantage",
             "grpo_async_advantage_ex", "grpo_async_loss_fwd", "grpo_async_loss_fwd_ex",
             "grpo_async_loss_fwd_vp", "grpo_async_loss_bwd", "grpo_async_workspace_size",
             "grpo_async_lmhead_workspace_size", "grpo_async_lmhead_fwd", "grpo_async_lmhead_bwd",
@@ -38,7 +39,7 @@ EXPORTED = ("grpo_async_validate", "grpo_async_validate_sync", "grpo_async_advan
             "grpo_async_group_partials", "grpo_async_group_sq_partials",
             "grpo_async_advantage_from_stats", "grpo_async_lmhead_tp_partials",
             "grpo_async_lmhead_tp_fwd", "grpo_async_lmhead_tp_bwd", "grpo_async_lmhead_dw",
-            "grpo_async_lmhead_tp_dx", "grpo_async_lmhead_tp_dx_reduce",
+            "grpo_async_lmhead_tp_dx", "grpo_async_lmhead_tp_dx_reduce", "grpo_async_lmhead_dx",
             "grpo_profile_enable", "grpo_profile_collect", "grpo_async_last_plan",
             "grpo_last_launch_count",
             "grpo_last_error", "grpo_version")
@@ -103,6 +104,13 @@ def _load():
     lib.grpo_async_validate_sync.argtypes = [P, P, P, P, P, P, i32, i64, i32, i32, i32, i32, i64,
                                              i32, P, P, P, P, P, P]
     lib.grpo_async_validate_sync.restype = st
+    lib.grpo_async_validate_local.argtypes = [P, P, P, i32, i64, i32, i32, i32, i32, i64, i32,
+                                              P, P, i32, P, P, P, P, P, P, P, P, P]
+    lib.grpo_async_validate_local.restype = st
+    lib.grpo_async_validate_combine.argtypes = [P, P, P]
+    lib.grpo_async_validate_combine.restype = st
+    lib.grpo_async_combine_ranks.argtypes = [P, i32, i32, P, P]
+    lib.grpo_async_combine_ranks.restype = st
     lib.grpo_async_advantage.argtypes = [P, P, P, i32, i32, f32, P, P, P, P]
     lib.grpo_async_advantage.restype = st
     lib.grpo_async_loss_fwd.argtypes = [P, i64, i64, i32, i64, P, P, P, i32, P, P, P, f32, f32,
@@ -138,11 +146,13 @@ def _load():
     lib.grpo_async_lmhead_tp_fwd.restype = st
     lib.grpo_async_lmhead_tp_bwd.argtypes = [P, P, i64, i32, i32, i32, P, P, P, f32, P, i64, P, P, P]
     lib.grpo_async_lmhead_tp_bwd.restype = st
-    lib.grpo_async_lmhead_tp_dx.argtypes = [P, i64, P, i64, i32, i32, i32, i32, P, P]
+    lib.grpo_async_lmhead_tp_dx.argtypes = [P, i64, P, i64, i32, i32, i32, i32, P, C.c_uint32, P]
     lib.grpo_async_lmhead_tp_dx.restype = st
-    lib.grpo_async_lmhead_tp_dx_reduce.argtypes = [P, i32, i64, i32, i32, P, i32, P]
+    lib.grpo_async_lmhead_tp_dx_reduce.argtypes = [P, i32, i64, i32, i32, P, i32, C.c_uint32, P]
     lib.grpo_async_lmhead_tp_dx_reduce.restype = st
     lib.grpo_async_lmhead_dw.argtypes = [P, i64, i32, i32, P, i64, P, P]
+    lib.grpo_async_lmhead_dx.argtypes = [P, i64, P, i64, i32, i32, P, i32, P]
+    lib.grpo_async_lmhead_dx.restype = st
     lib.grpo_async_lmhead_dw.restype = st
     lib.grpo_async_lmhead_set_cta_group.argtypes = [i32]
     lib.grpo_async_lmhead_set_cta_group.restype = st
@@ -238,6 +248,36 @@ def grpo_async_validate(version_ids, token_version, cu_seqlens, group_ids, targe
         N, T, P, V, G, tbs, v_theta, K, _ptr(traj_flags, torch.int32, "traj_flags"),
         _ptr(group_count, torch.int32, "group_count"), _ptr(stale_hist, torch.int32, "stale_hist"),
         _ptr(summary, torch.int64, "summary"), _stream(stream)))
+
+
+def grpo_async_validate_local(version_ids, cu_seqlens, group_ids, N, T, P, V, G, tbs, v_theta, K,
+                              local_cu, traj_index, n_local, token_version_local, target_ids_local,
+                              logp_behav_local, traj_flags, group_count, stale_hist, summary,
+                              token_counts=None, stream=None):
+    """One rank of a trajectory-sharded batch: trajectory checks over all N, token checks over
+    the n_local trajectories traj_index (local packing local_cu); token_counts: float64[3]."""
+    _check(LIB.grpo_async_validate_local(
+        _ptr(version_ids, torch.int64, "version_ids"), _ptr(cu_seqlens, torch.int64, "cu_seqlens"),
+        _ptr(group_ids, torch.int32, "group_ids"), N, T, P, V, G, tbs, v_theta, K,
+        _ptr(local_cu, torch.int64, "local_cu"), _ptr(traj_index, torch.int32, "traj_index"), n_local,
+        _ptr(token_version_local, torch.int64, "token_version_local"),
+        _ptr(target_ids_local, torch.int64, "target_ids_local"),
+        _ptr(logp_behav_local, torch.float32, "logp_behav_local"),
+        _ptr(traj_flags, torch.int32, "traj_flags"), _ptr(group_count, torch.int32, "group_count"),
+        _ptr(stale_hist, torch.int32, "stale_hist"), _ptr(summary, torch.int64, "summary"),
+        _ptr(token_counts, torch.float64, "token_counts"), _stream(stream)))
+
+
+def grpo_async_validate_combine(summary, token_counts, stream=None):
+    _check(LIB.grpo_async_validate_combine(_ptr(summary, torch.int64, "summary"),
+                                           _ptr(token_counts, torch.float64, "token_counts"),
+                                           _stream(stream)))
+
+
+def grpo_async_combine_ranks(gathered, world, n, out, stream=None):
+    """out[k] = sum over ranks in rank order of gathered[q, k] (float64 device tensors)."""
+    _check(LIB.grpo_async_combine_ranks(_ptr(gathered, torch.float64, "gathered"), world, n,
+                                        _ptr(out, torch.float64, "out"), _stream(stream)))
 
 
 def grpo_async_validate_sync(version_ids, token_version, cu_seqlens, group_ids, target_ids,
@@ -502,15 +542,24 @@ def grpo_async_lmhead_dw(hidden, n_rows, d, V, dz, ld_dz, dW, stream=None):
                                     _ptr(dW, torch.float32, "dW"), _stream(stream)))
 
 
-def grpo_async_lmhead_tp_dx(dz, ld_dz, W_shard, n_rows, d, Vs, world, rank, slots, stream=None):
-    """slots: `world` device addresses (ints or float32 tensors) of every rank's slot buffer."""
+def grpo_async_lmhead_dx(dz, ld_dz, W, n_rows, d, V, dhidden, stream=None):
+    """dhidden = dz W on the tensor cores (bf16 or float32 [n_rows, d] by dhidden's dtype)."""
+    out_bf16 = 1 if dhidden.element_size() == 2 else 0
+    _check(LIB.grpo_async_lmhead_dx(_bf16(dz, "dz"), ld_dz, _bf16(W, "W"), n_rows, d, V,
+                                    _ptr(dhidden, None, "dhidden"), out_bf16, _stream(stream)))
+
+
+def grpo_async_lmhead_tp_dx(dz, ld_dz, W_shard, n_rows, d, Vs, world, rank, slots, epoch=0,
+                            stream=None):
+    """slots: `world` device addresses (ints or float32 tensors) of every rank's slot buffer
+    ([2][world][rows_per_rank][d] f32; call `epoch` writes half epoch % 2)."""
     arr = (C.c_void_p * world)(*[_addr(x, "slots") for x in slots])
     _check(LIB.grpo_async_lmhead_tp_dx(_bf16(dz, "dz"), ld_dz, _bf16(W_shard, "W_shard"), n_rows, d,
-                                       Vs, world, rank, arr, _stream(stream)))
+                                       Vs, world, rank, arr, epoch, _stream(stream)))
 
 
-def grpo_async_lmhead_tp_dx_reduce(own_slots, world, n_rows, d, rank, out, stream=None):
+def grpo_async_lmhead_tp_dx_reduce(own_slots, world, n_rows, d, rank, out, epoch=0, stream=None):
     out_bf16 = 1 if out.element_size() == 2 else 0
     _check(LIB.grpo_async_lmhead_tp_dx_reduce(_ptr(own_slots, torch.float32, "own_slots"), world,
                                               n_rows, d, rank, _ptr(out, None, "out"), out_bf16,
-                                              _stream(stream)))
+                                              epoch, _stream(stream)))

@@ -58,6 +58,43 @@ class DeviceBatch:
                            t(b.token_version, torch.int64))
 
 
+@dataclass
+class ShardedBatch:
+    """One rank's view of a trajectory-sharded batch: the O(N) trajectory
+    metadata replicated (cu_seqlens of the global packing, group ids, versions, rewards),
+    the token arrays only for this rank's trajectories traj_index, in the local packing
+    local_cu (trajectory j of this rank owns local rows [local_cu[j], local_cu[j+1]))."""
+    P: int
+    G: int
+    K: int
+    V: int
+    ld: int
+    tbs: int
+    v_theta: int
+    T: int                         # global row count (cu_seqlens[N])
+    cu_seqlens: torch.Tensor       # int64 [N+1]
+    group_ids: torch.Tensor        # int32 [N]
+    version_ids: torch.Tensor      # int64 [N]
+    rewards: torch.Tensor          # float32 [N]
+    local_cu: torch.Tensor         # int64 [n_local+1]
+    traj_index: torch.Tensor       # int32 [n_local]
+    target_ids: torch.Tensor       # int64 [T_local]
+    logp_behav: torch.Tensor       # float32 [T_local]
+    token_version: torch.Tensor | None = None  # int64 [T_local]
+
+    @property
+    def N(self):
+        return self.group_ids.numel()
+
+    @property
+    def n_local(self):
+        return self.traj_index.numel()
+
+    @property
+    def T_local(self):
+        return self.target_ids.numel()
+
+
 class ValidateOut:
     def __init__(self, N, P, K, device):
         self.traj_flags = torch.zeros(max(N, 1), dtype=torch.int32, device=device)
@@ -102,6 +139,41 @@ class GrpoAsyncLoss:
                               out.summary, stream)
         self.launches += L.grpo_last_launch_count()
         return out
+
+    def validate_local(self, sb: ShardedBatch, out: ValidateOut | None = None, token_counts=None,
+                       stream=None):
+        """One rank of a sharded batch: trajectory checks over all N, token checks over this
+        rank's trajectories; token_counts (float64[3] device tensor, e.g. a slice of the packed
+        partials) receives the local token-level counts."""
+        out = out or ValidateOut(sb.N, sb.P, sb.K, sb.cu_seqlens.device)
+        L.grpo_async_validate_local(sb.version_ids, sb.cu_seqlens, sb.group_ids, sb.N, sb.T, sb.P,
+                                    sb.V, sb.G, sb.tbs, sb.v_theta, sb.K, sb.local_cu,
+                                    sb.traj_index, sb.n_local, sb.token_version, sb.target_ids,
+                                    sb.logp_behav, out.traj_flags, out.group_count,
+                                    out.stale_hist, out.summary, token_counts, stream)
+        self.launches += L.grpo_last_launch_count()
+        return out
+
+    def combine_ranks(self, packed, world, allgather=None, out=None, stream=None):
+        """The data-parallel step's one exchange: all-gather every rank's packed float64
+        partials and sum them in rank order on the device (deterministic, identical on every
+        rank).  allgather(t) -> [world, n] (default: torch.distributed.all_gather_into_tensor)."""
+        if allgather is None:
+            import torch.distributed as dist
+
+            def allgather(t):
+                g = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+                dist.all_gather_into_tensor(g, t)
+                return g
+        gathered = allgather(packed)
+        out = out if out is not None else torch.empty_like(packed)
+        L.grpo_async_combine_ranks(gathered, world, packed.numel(), out, stream)
+        self.launches += L.grpo_last_launch_count()
+        return out
+
+    def validate_combine(self, out: ValidateOut, token_counts, stream=None):
+        L.grpo_async_validate_combine(out.summary, token_counts, stream)
+        self.launches += L.grpo_last_launch_count()
 
     # ---- advantages, eq:group_advantage P:153-156
     def advantage(self, db: DeviceBatch, adv=None, inv_norm=None, stream=None):
@@ -282,14 +354,18 @@ class GrpoAsyncLoss:
         N = cu_seqlens.numel() - 1
         V = V if V is not None else comm.world * comm.shard_cols
         ws = self.workspace(n_rows, V, N, shards[0].device)
-        L.grpo_async_loss_fwd_vp(comm.world, comm.rank_begin, comm.shard_cols, comm.slots,
-                                 shards, dshards,
-                                 comm.xbuf, comm.epoch, row_begin, n_rows, V, ld,
-                                 target_ids, logp_behav, cu_seqlens, N, traj_index, adv, inv_norm,
-                                 self.eps, self.eps_hi, self.norm, self.traj_mask, self.grad_scale,
-                                 logp_out, lse_out, scale_out, traj_sum, stats, ws, stream,
-                                 lag=comm.lag, dynamic_rows=comm.dynamic_rows)
-        comm.epoch += 1
+        try:
+            L.grpo_async_loss_fwd_vp(comm.world, comm.rank_begin, comm.shard_cols, comm.slots,
+                                     shards, dshards,
+                                     comm.xbuf, comm.epoch, row_begin, n_rows, V, ld,
+                                     target_ids, logp_behav, cu_seqlens, N, traj_index, adv,
+                                     inv_norm, self.eps, self.eps_hi, self.norm, self.traj_mask,
+                                     self.grad_scale, logp_out, lse_out, scale_out, traj_sum,
+                                     stats, ws, stream, lag=comm.lag, dynamic_rows=comm.dynamic_rows)
+        finally:
+            # every call consumes an epoch on every rank, even one this rank refused on the
+            # host: the ranks' epochs (exchange-buffer halves and tags) stay in step
+            comm.epoch += 1
         self.launches += L.grpo_last_launch_count()
 
     def loss_bwd(self, logits, n_rows, V, target_ids, lse, token_scale, dlogits, mult=1.0,

@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-cudart", "static",
               "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-LINK = ["-lcublas"]
+LINK = []  # no cuBLAS: every GEMM of the path is a hand-written tcgen05 kernel
 
 
 def sources():

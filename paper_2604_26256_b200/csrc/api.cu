@@ -2,7 +2,6 @@
 // Host-side argument checks, workspace carve-up, kernel selection, error text.
 #include <cstdarg>
 
-#include <cublas_v2.h>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -106,8 +105,8 @@ uint8_t *fill_loss_args(grpo::LossArgs &a, int64_t row_begin, int64_t n_rows, in
     uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
     a.rowinfo = reinterpret_cast<grpo::RowInfo *>(w);
     w += align256((size_t)n_rows * sizeof(grpo::RowInfo));
-    a.term_ws = reinterpret_cast<float *>(w);
-    w += align256((size_t)n_rows * 4);
+    a.term_ws = reinterpret_cast<double *>(w);
+    w += align256((size_t)n_rows * 8);
     a.logp_ws = reinterpret_cast<float *>(w);
     w += align256((size_t)n_rows * 4);
     a.flag_ws = w;
@@ -171,7 +170,7 @@ size_t grpo_async_workspace_size(int64_t n_rows, int32_t V, int32_t N) {
     (void)V;
     if (n_rows < 0) n_rows = 0;
     if (N < 0) N = 0;
-    return align256((size_t)n_rows * sizeof(grpo::RowInfo)) + align256((size_t)n_rows * 4) +
+    return align256((size_t)n_rows * sizeof(grpo::RowInfo)) + align256((size_t)n_rows * 8) +
            align256((size_t)n_rows * 4) + align256((size_t)n_rows) +
            align256((size_t)N * 5 * sizeof(double)) +
            align256(GRPO_VP_MAX_RANKS * sizeof(unsigned long long)) + 256;
@@ -194,11 +193,62 @@ grpo_status_t grpo_async_validate(const int64_t *version_ids, const int64_t *tok
         return fail(GRPO_ERR_INVALID_ARG, "validate: NULL version_ids/group_ids/traj_flags");
     if (T > 0 && !target_ids) return fail(GRPO_ERR_INVALID_ARG, "validate: NULL target_ids");
     int launches = 0;
-    cudaError_t e = grpo::launch_validate(version_ids, token_version, cu_seqlens, group_ids,
-                                          target_ids, logp_behav, N, T, P, V, G, tbs, v_theta, K,
-                                          traj_flags, group_count, stale_hist, summary,
-                                          (cudaStream_t)stream, &launches);
+    cudaError_t e = grpo::launch_validate(version_ids, cu_seqlens, group_ids, N, T, P, V, G, tbs,
+                                          v_theta, K, token_version, target_ids, logp_behav,
+                                          cu_seqlens, nullptr, N, T, traj_flags, group_count,
+                                          stale_hist, summary, nullptr, (cudaStream_t)stream,
+                                          &launches);
     if (e != cudaSuccess) return cuda_fail(e, "validate");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_validate_local(const int64_t *version_ids, const int64_t *cu_seqlens,
+                                        const int32_t *group_ids, int32_t N, int64_t T, int32_t P,
+                                        int32_t V, int32_t G, int32_t tbs, int64_t v_theta,
+                                        int32_t K, const int64_t *local_cu,
+                                        const int32_t *traj_index, int32_t n_local,
+                                        const int64_t *token_version_local,
+                                        const int64_t *target_ids_local,
+                                        const float *logp_behav_local, uint32_t *traj_flags,
+                                        int32_t *group_count, int32_t *stale_hist,
+                                        grpo_validate_summary_t *summary, double *token_counts,
+                                        grpo_stream_t stream) {
+    if (!cu_seqlens || !summary || !group_count || !stale_hist)
+        return fail(GRPO_ERR_INVALID_ARG, "validate_local: NULL cu_seqlens/group_count/stale_hist/summary");
+    if (N < 0 || T < 0 || P <= 0 || V <= 0 || G <= 0 || K < 0 || n_local < 0 || n_local > N)
+        return fail(GRPO_ERR_INVALID_ARG, "validate_local: bad sizes N=%d T=%lld P=%d V=%d G=%d K=%d n_local=%d",
+                    N, (long long)T, P, V, G, K, n_local);
+    if (N > 0 && (!version_ids || !group_ids || !traj_flags))
+        return fail(GRPO_ERR_INVALID_ARG, "validate_local: NULL version_ids/group_ids/traj_flags");
+    if (n_local > 0 && (!local_cu || !traj_index || !target_ids_local))
+        return fail(GRPO_ERR_INVALID_ARG, "validate_local: NULL local_cu/traj_index/target_ids_local");
+    int launches = 0;
+    // the local token arrays are exactly the local packing: no clip beyond local_cu
+    cudaError_t e = grpo::launch_validate(version_ids, cu_seqlens, group_ids, N, T, P, V, G, tbs,
+                                          v_theta, K, token_version_local, target_ids_local,
+                                          logp_behav_local, local_cu, traj_index, n_local,
+                                          INT64_MAX, traj_flags, group_count, stale_hist, summary,
+                                          token_counts, (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "validate_local");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_validate_combine(grpo_validate_summary_t *summary,
+                                          const double *token_counts, grpo_stream_t stream) {
+    if (!summary || !token_counts) return fail(GRPO_ERR_INVALID_ARG, "validate_combine: NULL argument");
+    int launches = 0;
+    cudaError_t e = grpo::launch_validate_combine(summary, token_counts, (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "validate_combine");
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_combine_ranks(const double *gathered, int32_t world, int32_t n,
+                                       double *out, grpo_stream_t stream) {
+    if (world < 1 || n < 0 || (n > 0 && (!gathered || !out)))
+        return fail(GRPO_ERR_INVALID_ARG, "combine_ranks: world=%d n=%d", world, n);
+    int launches = 0;
+    cudaError_t e = grpo::launch_combine_ranks(gathered, world, n, out, (cudaStream_t)stream, &launches);
+    if (e != cudaSuccess) return cuda_fail(e, "combine_ranks");
     return ok(launches);
 }
 
@@ -365,8 +415,18 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     if (!workspace || workspace_bytes < need)
         return fail(GRPO_ERR_WORKSPACE, "loss_fwd: workspace %zu B < required %zu B",
                     workspace_bytes, need);
-    if (tune && (tune->kernel < 0 || tune->kernel > 3))
-        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: tune->kernel %d", tune->kernel);
+    // kernel 1 (the cluster-resident K3a) is retired: K3c streams the same rows through the
+    // bulk-copy ring at 1.7x its throughput
+    if (tune && (tune->kernel < 0 || tune->kernel > 3 || tune->kernel == 1))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: tune->kernel %d (0 auto, 2 row-wise, 3 ring)",
+                    tune->kernel);
+    if (tune && tune->kernel == 3 && (tune->cluster_size < 0 || tune->cluster_size > 2))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: tune->cluster_size %d (kernel 3: 0, 1 or 2)",
+                    tune->cluster_size);
+    if (tune && tune->kernel == 2 && tune->cluster_size != 0 && tune->cluster_size != 1 &&
+        tune->cluster_size != 2 && tune->cluster_size != 4)
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: tune->cluster_size %d (kernel 2: 0, 1, 2 or 4)",
+                    tune->cluster_size);
 
     grpo::LossArgs a{};
     fill_loss_args(a, row_begin, n_rows, V, target_ids, logp_behav, cu_seqlens, N, traj_index, adv,
@@ -425,13 +485,15 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     }
     if ((kernel == 0 && !auto_stream) || kernel == 2) {
         e = grpo::launch_fused_rowwise(a, tune, s, &launches, &g_last_plan);
+        // no compiled instantiation for this (threads, vectors, cluster) tune: nothing launched
+        if (e == cudaErrorInvalidValue && launches == 1)
+            return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: no row-wise kernel for this tune");
         if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/rowwise");
-    } else if (kernel == 3 || auto_stream) {
-        e = grpo::launch_fused_stream(a, tune, s, &launches, &g_last_plan, why, sizeof why);
-        if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/stream", why);
     } else {
-        e = grpo::launch_fused_cluster(a, tune, s, &launches, why, sizeof why, &g_last_plan);
-        if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/fused_cluster", why);
+        e = grpo::launch_fused_stream(a, tune, s, &launches, &g_last_plan, why, sizeof why);
+        // a tune the kernel rejects on the host (its own check, no CUDA call made)
+        if (e == cudaErrorInvalidValue && why[0]) return fail(GRPO_ERR_INVALID_ARG, "loss_fwd: %s", why);
+        if (e != cudaSuccess) return cuda_fail(e, "loss_fwd/stream", why);
     }
     if (traced && (e = prof_end(s, ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
     e = grpo::launch_segment_reduce(a, s, &launches);
@@ -546,17 +608,6 @@ grpo_status_t lm_check(const char *fn, const uint16_t *hidden, const uint16_t *W
 
 thread_local int g_lm_cta_group = 2;
 
-cublasHandle_t cublas_handle() {
-    static thread_local cublasHandle_t h = nullptr;
-    static thread_local int h_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!h || h_dev != dev) {
-        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
-        h_dev = dev;
-    }
-    return h;
-}
 
 }  // namespace
 
@@ -573,7 +624,7 @@ size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N) {
     if (n_rows < 0) n_rows = 0;
     if (V < 1) V = 1;
     const size_t split = (size_t)grpo::lmhead_n_split(n_rows, V);
-    return grpo_async_workspace_size(n_rows, V, N) + align256(split * (size_t)n_rows * 8) +
+    return grpo_async_workspace_size(n_rows, V, N) + align256(split * (size_t)n_rows * 16) +
            align256((size_t)n_rows * 4) + 256;
 }
 
@@ -608,8 +659,8 @@ grpo_status_t grpo_async_lmhead_fwd(const uint16_t *hidden, const uint16_t *W, i
     uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace))) +
                  grpo_async_workspace_size(n_rows, V, N) - 256;
     const int32_t n_split = grpo::lmhead_n_split(n_rows, V);
-    float2 *part = reinterpret_cast<float2 *>(w);
-    w += align256((size_t)n_split * (size_t)n_rows * 8);
+    grpo::RowPart *part = reinterpret_cast<grpo::RowPart *>(w);
+    w += align256((size_t)n_split * (size_t)n_rows * 16);
     float *zy = reinterpret_cast<float *>(w);
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
@@ -650,24 +701,14 @@ grpo_status_t grpo_async_lmhead_bwd(const uint16_t *hidden, const uint16_t *W, i
                                         target_ids, lse, token_scale, grad_scale_mult, s, &launches,
                                         &g_last_plan, why, sizeof why, g_lm_cta_group);
     if (e != cudaSuccess) return cuda_fail(e, "lmhead_bwd/tcgen05", why);
-    if (dhidden || dW) {
-        cublasHandle_t h = cublas_handle();
-        if (!h) return fail(GRPO_ERR_CUDA, "lmhead_bwd: cublasCreate failed");
-        if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_bwd: cublasSetStream");
-        const float one = 1.0f, zero = 0.0f;
-        // column-major views: W -> [d, V], dz -> [V, n_rows] (ld ld_dz), hidden -> [d, n_rows]
-        if (dhidden) {  // dhidden^T [d, n] = W^T [d, V] * dz^T [V, n]
-            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, d, (int)n_rows, V, &one, W, CUDA_R_16BF,
-                                             d, dz, CUDA_R_16BF, (int)ld_dz, &zero, dhidden, CUDA_R_16BF, d,
-                                             CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_bwd: dhidden GEMM status %d", (int)cs);
-        }
-        if (dW) {  // dW^T [d, V] += hidden^T [d, n] * dz [n, V]
-            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, d, V, (int)n_rows, &one, hidden,
-                                             CUDA_R_16BF, d, dz, CUDA_R_16BF, (int)ld_dz, &one, dW, CUDA_R_32F, d,
-                                             CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_bwd: dW GEMM status %d", (int)cs);
-        }
+    // dX = dz W and dW += dz^T X on the tensor cores (lmhead_dx.cu gemm_kernel)
+    if (dhidden) {
+        e = grpo::launch_lmhead_gemm_dx(dz, ld_dz, W, n_rows, d, V, dhidden, 1, s, &launches, why, sizeof why);
+        if (e != cudaSuccess) return cuda_fail(e, "lmhead_bwd/dX", why);
+    }
+    if (dW) {
+        e = grpo::launch_lmhead_gemm_dw(dz, ld_dz, hidden, n_rows, d, V, dW, s, &launches, why, sizeof why);
+        if (e != cudaSuccess) return cuda_fail(e, "lmhead_bwd/dW", why);
     }
     return ok(launches);
 }
@@ -689,8 +730,8 @@ grpo_status_t grpo_async_lmhead_tp_partials(const uint16_t *hidden, const uint16
     if (n_rows == 0) return ok(0);
     uint8_t *w = reinterpret_cast<uint8_t *>(align256(reinterpret_cast<uintptr_t>(workspace)));
     const int32_t n_split = grpo::lmhead_n_split(n_rows, Vs);
-    float2 *part = reinterpret_cast<float2 *>(w);
-    w += align256((size_t)n_split * (size_t)n_rows * 8);
+    grpo::RowPart *part = reinterpret_cast<grpo::RowPart *>(w);
+    w += align256((size_t)n_split * (size_t)n_rows * 16);
     float *zy = reinterpret_cast<float *>(w);
     cudaStream_t s = (cudaStream_t)stream;
     int launches = 0;
@@ -765,23 +806,14 @@ grpo_status_t grpo_async_lmhead_tp_bwd(const uint16_t *hidden, const uint16_t *W
                                         target_ids, lse, token_scale, grad_scale_mult, s, &launches,
                                         &g_last_plan, why, sizeof why, g_lm_cta_group, col_offset);
     if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_bwd/tcgen05", why);
-    if (dhidden_partial || dW_shard) {
-        cublasHandle_t h = cublas_handle();
-        if (!h) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: cublasCreate failed");
-        if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: cublasSetStream");
-        const float one = 1.0f, zero = 0.0f;
-        if (dhidden_partial) {  // f32 partial (summed over the ranks by the caller)
-            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, d, (int)n_rows, Vs, &one, W_shard,
-                                             CUDA_R_16BF, d, dz, CUDA_R_16BF, (int)ld_dz, &zero, dhidden_partial,
-                                             CUDA_R_32F, d, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: dhidden GEMM status %d", (int)cs);
-        }
-        if (dW_shard) {
-            cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, d, Vs, (int)n_rows, &one, hidden,
-                                             CUDA_R_16BF, d, dz, CUDA_R_16BF, (int)ld_dz, &one, dW_shard, CUDA_R_32F,
-                                             d, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-            if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_tp_bwd: dW GEMM status %d", (int)cs);
-        }
+    if (dhidden_partial) {  // f32 partial (summed over the ranks by the caller)
+        e = grpo::launch_lmhead_gemm_dx(dz, ld_dz, W_shard, n_rows, d, Vs, dhidden_partial, 0, s, &launches, why,
+                                        sizeof why);
+        if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_bwd/dX", why);
+    }
+    if (dW_shard) {
+        e = grpo::launch_lmhead_gemm_dw(dz, ld_dz, hidden, n_rows, d, Vs, dW_shard, s, &launches, why, sizeof why);
+        if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_bwd/dW", why);
     }
     return ok(launches);
 }
@@ -794,21 +826,40 @@ grpo_status_t grpo_async_lmhead_dw(const uint16_t *hidden, int64_t n_rows, int32
     if (n_rows > 0 && (!hidden || !dz || !dW)) return fail(GRPO_ERR_INVALID_ARG, "lmhead_dw: NULL pointer");
     if (ld_dz < V || ld_dz % 8 != 0) return fail(GRPO_ERR_ALIGNMENT, "lmhead_dw: ld_dz=%lld", (long long)ld_dz);
     if (n_rows == 0) return ok(0);
-    cublasHandle_t h = cublas_handle();
-    if (!h) return fail(GRPO_ERR_CUDA, "lmhead_dw: cublasCreate failed");
-    if (cublasSetStream(h, (cudaStream_t)stream) != CUBLAS_STATUS_SUCCESS)
-        return fail(GRPO_ERR_CUDA, "lmhead_dw: cublasSetStream");
-    const float one = 1.0f;
-    cublasStatus_t cs = cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, d, V, (int)n_rows, &one, hidden, CUDA_R_16BF,
-                                     d, dz, CUDA_R_16BF, (int)ld_dz, &one, dW, CUDA_R_32F, d,
-                                     CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-    if (cs != CUBLAS_STATUS_SUCCESS) return fail(GRPO_ERR_CUDA, "lmhead_dw: GEMM status %d", (int)cs);
-    return ok(0);
+    if (d < 64 || d % 64 != 0) return fail(GRPO_ERR_INVALID_ARG, "lmhead_dw: d=%d (a positive multiple of 64)", d);
+    if (!aligned16(hidden) || !aligned16(dz) || !aligned16(dW))
+        return fail(GRPO_ERR_ALIGNMENT, "lmhead_dw: hidden/dz/dW must be 16-byte aligned");
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_lmhead_gemm_dw(dz, ld_dz, hidden, n_rows, d, V, dW, (cudaStream_t)stream,
+                                                &launches, why, sizeof why);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_dw", why);
+    return ok(launches);
+}
+
+grpo_status_t grpo_async_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W,
+                                   int64_t n_rows, int32_t d, int32_t V, void *dhidden,
+                                   int32_t out_bf16, grpo_stream_t stream) {
+    if (n_rows < 0 || V <= 0 || d < 64 || d % 64 != 0 || n_rows > INT32_MAX)
+        return fail(GRPO_ERR_INVALID_ARG, "lmhead_dx: n_rows=%lld d=%d V=%d", (long long)n_rows, d, V);
+    if (n_rows > 0 && (!W || !dz || !dhidden)) return fail(GRPO_ERR_INVALID_ARG, "lmhead_dx: NULL pointer");
+    if (ld_dz < V || ld_dz % 8 != 0 || (dz && !aligned16(dz)) || (W && !aligned16(W)) ||
+        (dhidden && !aligned16(dhidden)))
+        return fail(GRPO_ERR_ALIGNMENT, "lmhead_dx: ld_dz=%lld (>= V, multiple of 8), 16-byte aligned",
+                    (long long)ld_dz);
+    if (n_rows == 0) return ok(0);
+    int launches = 0;
+    char why[256] = {0};
+    cudaError_t e = grpo::launch_lmhead_gemm_dx(dz, ld_dz, W, n_rows, d, V, dhidden, out_bf16 ? 1 : 0,
+                                                (cudaStream_t)stream, &launches, why, sizeof why);
+    if (e != cudaSuccess) return cuda_fail(e, "lmhead_dx", why);
+    return ok(launches);
 }
 
 grpo_status_t grpo_async_lmhead_tp_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W_shard,
                                       int64_t n_rows, int32_t d, int32_t Vs, int32_t world,
-                                      int32_t rank, float *const *slots, grpo_stream_t stream) {
+                                      int32_t rank, float *const *slots, uint32_t epoch,
+                                      grpo_stream_t stream) {
     if (n_rows < 0 || n_rows > INT32_MAX || Vs <= 0 || d < 128 || d % 128 != 0)
         return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx: n_rows=%lld d=%d Vs=%d (d a multiple of 128)",
                     (long long)n_rows, d, Vs);
@@ -822,7 +873,11 @@ grpo_status_t grpo_async_lmhead_tp_dx(const uint16_t *dz, int64_t ld_dz, const u
                     (long long)ld_dz);
     int launches = 0;
     char why[256] = {0};
-    cudaError_t e = grpo::launch_lmhead_dx(dz, ld_dz, W_shard, n_rows, d, Vs, world, rank, slots,
+    // half epoch % 2 of every slot buffer (the header's double buffering)
+    const int64_t half = (int64_t)(epoch & 1u) * world * ((n_rows + world - 1) / world) * d;
+    float *sl[GRPO_VP_MAX_RANKS];
+    for (int q = 0; q < world; ++q) sl[q] = slots[q] + half;
+    cudaError_t e = grpo::launch_lmhead_dx(dz, ld_dz, W_shard, n_rows, d, Vs, world, rank, sl,
                                            (cudaStream_t)stream, &launches, why, sizeof why);
     if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_dx", why);
     return ok(launches);
@@ -830,12 +885,13 @@ grpo_status_t grpo_async_lmhead_tp_dx(const uint16_t *dz, int64_t ld_dz, const u
 
 grpo_status_t grpo_async_lmhead_tp_dx_reduce(const float *own_slots, int32_t world, int64_t n_rows,
                                              int32_t d, int32_t rank, void *out, int32_t out_bf16,
-                                             grpo_stream_t stream) {
+                                             uint32_t epoch, grpo_stream_t stream) {
     if (n_rows < 0 || d < 4 || d % 4 != 0 || world < 1 || world > GRPO_VP_MAX_RANKS || rank < 0 || rank >= world)
         return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx_reduce: n_rows/d/world/rank");
     if (n_rows > 0 && (!own_slots || !out)) return fail(GRPO_ERR_INVALID_ARG, "lmhead_tp_dx_reduce: NULL");
     int launches = 0;
-    cudaError_t e = grpo::launch_lmhead_dx_reduce(own_slots, world, n_rows, d, rank, out, out_bf16,
+    const int64_t half = (int64_t)(epoch & 1u) * world * ((n_rows + world - 1) / world) * d;
+    cudaError_t e = grpo::launch_lmhead_dx_reduce(own_slots + half, world, n_rows, d, rank, out, out_bf16,
                                                   (cudaStream_t)stream, &launches);
     if (e != cudaSuccess) return cuda_fail(e, "lmhead_tp_dx_reduce");
     return ok(launches);

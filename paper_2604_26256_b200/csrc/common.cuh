@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "grpo_async.h"
 
@@ -21,6 +22,37 @@ struct __align__(16) RowInfo {
     float adv;        // A_i of the row's trajectory
     float inv_norm;   // 1 / (P * G_p * L_i)
 };
+
+// A log2-domain softmax partial: the sum s of 2^(z*log2e - a) over a part of a row, with
+// s in fp64 (16 bytes, one st.async / 128-bit shared access).
+struct __align__(16) RowPart {
+    float a;
+    float pad;
+    double s;
+};
+
+// A shard's partial of one row as 16 bytes (vocabulary- and tensor-parallel exchanges):
+// (a, z_y, s fp64 with "this shard holds y_t" in its sign bit; s >= 0 otherwise).
+__host__ __device__ __forceinline__ float4 pack_shard_part(float a, double s, float zy, bool holds) {
+    unsigned long long sb;
+    memcpy(&sb, &s, 8);
+    sb |= holds ? (1ull << 63) : 0ull;
+    float4 v;
+    v.x = a;
+    v.y = zy;
+    memcpy(&v.z, &sb, 8);
+    return v;
+}
+__host__ __device__ __forceinline__ void unpack_shard_part(const float4 &v, float &a, double &s, float &zy,
+                                                           bool &holds) {
+    unsigned long long sb;
+    memcpy(&sb, &v.z, 8);
+    holds = (sb >> 63) != 0ull;
+    sb &= ~(1ull << 63);
+    memcpy(&s, &sb, 8);
+    a = v.x;
+    zy = v.y;
+}
 
 // Per-row flags written by the loss kernels (workspace, one byte per row).
 enum : uint8_t { kRowClipped = 1, kRowActive = 2 };
@@ -175,6 +207,17 @@ __device__ __forceinline__ void st_async_v2(uint32_t raddr, uint32_t rbar, float
         "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(
             raddr),
         "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(rbar)
+        : "memory");
+}
+
+// A RowPart (16 bytes) stored into a peer CTA's shared memory, completing 16 bytes of
+// transaction on its mbarrier.
+__device__ __forceinline__ void st_async_part(uint32_t raddr, uint32_t rbar, float a, double s) {
+    const unsigned long long sb = (unsigned long long)__double_as_longlong(s);
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, "
+        "[%5];" ::"r"(raddr),
+        "r"(__float_as_uint(a)), "r"(0u), "r"((uint32_t)sb), "r"((uint32_t)(sb >> 32)), "r"(rbar)
         : "memory");
 }
 
@@ -342,40 +385,97 @@ __device__ __forceinline__ void warp_lse2_combine(float &a, float &s) {
     a = amax;
 }
 
+// The same with the sums held in fp64 (the row-wise kernels accumulate every thread's
+// batch sums in fp64, so a row's sum carries no fp32 rounding beyond the 32-element
+// batches).  The rescale factors 2^(a - amax) are exact powers
+// of the references' difference through ex2; the fp64 sums run in a fixed butterfly,
+// so every lane holds identical bits.
+__device__ __forceinline__ double warp_sum_all(double x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, off);
+    return x;
+}
+__device__ __forceinline__ void warp_lse2_combine(float &a, double &s) {
+    const float amax = warp_max_all(a);
+    s = (amax == -INFINITY) ? 0.0 : s * (double)ex2(a - amax);
+    s = warp_sum_all(s);
+    a = amax;
+}
+// Merge (a, s) with (b, t), fp64 sums; symmetric in its arguments like lse2_merge.
+__device__ __forceinline__ void lse2_merge(float &a, double &s, float b, double t) {
+    const float mn = fmaxf(a, b);
+    if (mn == -INFINITY) {
+        a = mn;
+        s = 0.0;
+        return;
+    }
+    s = s * (double)ex2(a - mn) + t * (double)ex2(b - mn);
+    a = mn;
+}
+
 // Per-row epilogue of eq:grpo_async / eq:ratio_async:
 // r = exp(logp - logp_w), term = min(r A, clip(r) A), clipped iff the clip
 // branch binds strictly, s = grad_scale * inv_norm * A * r * !clipped.
 struct RowOut {
-    float r, term, s;
+    double r, term;
+    float s;
+    float gy;  // the target's own gradient entry s (p_y - 1) = s expm1(logp), from fp64
     uint8_t flags;
 };
 
-// logp_t = z_y - lse from the row's log2-domain reference M and l2s = log2(S):
-//   logp = (z_y*log2e - M - l2s) * ln2,
-// formed in fp64 (a few DFMA per row) so the ratio r = exp(logp - logp_w) keeps
-// full fp32 accuracy even for very unlikely tokens (|logp| ~ 100).  z_y is scaled by
-// the same fp32 log2e the exponents of S used: the kernels compute the softmax of
-// z*(1+d), d = fl32(log2e)*ln2 - 1 = 1.4e-8, and logp must be that softmax's log at y
-// -- error d*(z_y - E_p[z]) -- not a mix of the two scalings, which leaves d*E_p[z]
-// (1.4e-4 for logits near 1e4; tests/test_gpu_parity.py::test_scale_jumps_along_the_row).
-__device__ __forceinline__ double row_logp(float zy, float M, float l2s) {
-    const double kLn2D = 0.69314718055994530942;
-    return (fma((double)zy, (double)kLog2e, -(double)M) - (double)l2s) * kLn2D;
+// log2(e) = kLog2eHi + kLog2eLo to 1.7e-13: the high part has 16 significant bits, so
+// fma(z, kLog2eLo, fma(z, kLog2eHi, -M)) is z*log2(e) - M rounded once at its own magnitude
+// (the LM-head epilogue, whose fp32 logits have free issue slots, uses it)
+constexpr float kLog2eHi = 1.44268798828125f;
+constexpr float kLog2eLo = 7.0526075e-06f;
+
+// log2 of a row's sum from the sum the row-wise kernels form with one FFMA per element,
+//   S' = sum_v 2^(z_v*fl32(log2 e) - M),  fl32(log2 e) = log2(e) (1 - 1.34e-8):
+// each term carries 2^(-z_v*(log2 e - fl32(log2 e))), i.e. S' = S * 2^(-(log2 e - fl32)*E_p[z])
+// with S the exact sum.  The reference M = fl32(m*fl32(log2 e)) (m the row max, rounded up)
+// carries the part E_p[z] ~ m of it, so
+//   log2 S = log2 S' + M * (log2 e / fl32(log2 e) - 1)  (+ the residual 1.34e-8 * E_p[z - m]),
+// which leaves logp an error of 1.34e-8 * |E_p[z - m]| (<= 1e-7 for any row whose
+// probability mass lies within 7 nats of its max) instead of 1.34e-8 * |E_p[z]| -- 1.3e-4
+// for logits near 1e4 (Z23).  fp64 throughout.
+__device__ __forceinline__ double row_l2s(double s, float M) {
+    const double kRatioM1 = 1.4426950408889634074 / (double)kLog2e - 1.0;
+    return log2(s) + (double)M * kRatioM1;
 }
 
+// logp_t = z_y - lse from the row's log2-domain reference M and l2s = log2 of its sum
+// S = sum_v 2^(z_v*log2e - M):
+//   lse = (M + l2s) * ln2,  logp = z_y - lse,
+// all in fp64 (a few DFMA per row) so that neither the fp32 rounding of lse nor that of
+// M*ln2 reaches logp; the ratio r = exp(logp - logp_w) then carries only the error of S.
+__device__ __forceinline__ double row_logp(float zy, float M, double l2s) {
+    const double kLn2D = 0.69314718055994530942;
+    return (double)zy - ((double)M + l2s) * kLn2D;
+}
+
+// eq:grpo_async / eq:ratio_async per token, in fp64 like the oracle (oracle_token_asym):
+// the clip bounds are 1 -/+ the widened float eps, term = min(rA, clip(r)A) stays fp64 to
+// the segmented sums, s = grad_scale * inv_norm * A * r is rounded to fp32 once.  A row
+// with A == 0 or inv_norm == 0 (an all-equal group, a masked trajectory, a padding row
+// outside cu_seqlens) gets s = 0 outright, and a row with A == 0 term = 0, so an infinite
+// ratio there (logp_w = -inf on a padding row) cannot turn into 0 * inf = NaN.
 __device__ __forceinline__ RowOut row_epilogue(double logp, const RowInfo &ri, float eps_lo,
                                                float eps_hi, float grad_scale) {
     RowOut o;
-    const float r = expf((float)(logp - (double)ri.logp_w));
-    const float lo = 1.0f - eps_lo, hi = 1.0f + eps_hi;
-    const float c = fminf(fmaxf(r, lo), hi);
-    const float A = ri.adv;
+    const double r = exp(logp - (double)ri.logp_w);
+    const double lo = 1.0 - (double)eps_lo, hi = 1.0 + (double)eps_hi;
+    const double c = fmin(fmax(r, lo), hi);
+    const double A = (double)ri.adv;
+    const bool dead = ri.adv == 0.0f || ri.inv_norm == 0.0f;
     o.r = r;
-    o.term = fminf(r * A, c * A);
-    const bool clipped = (A > 0.0f && r > hi) || (A < 0.0f && r < lo);
-    o.s = clipped ? 0.0f : grad_scale * ri.inv_norm * A * r;
-    o.flags = (clipped ? kRowClipped : 0) |
-              ((!clipped && A != 0.0f && ri.inv_norm != 0.0f) ? kRowActive : 0);
+    o.term = ri.adv == 0.0f ? 0.0 : fmin(r * A, c * A);  // a masked row keeps its term
+    const bool clipped = (A > 0.0 && r > hi) || (A < 0.0 && r < lo);
+    const double sd = (clipped || dead) ? 0.0 : (double)grad_scale * (double)ri.inv_norm * A * r;
+    o.s = (float)sd;
+    // p_y - 1 = expm1(logp) in fp64: a nearly certain target (p_y -> 1) keeps the relative
+    // accuracy of logp instead of the fp32 resolution of 1 - ex2(z_y - lse2) (Z24)
+    o.gy = (float)(sd * expm1(logp));
+    o.flags = (clipped ? kRowClipped : 0) | ((!clipped && !dead) ? kRowActive : 0);
     return o;
 }
 
@@ -404,7 +504,7 @@ struct LossArgs {
     double *stats;
     // workspace carve-up
     RowInfo *rowinfo;      // [n_rows]
-    float *term_ws;        // [n_rows]
+    double *term_ws;       // [n_rows] (fp64: term_t reaches the segmented sums unrounded)
     float *logp_ws;        // [n_rows]
     uint8_t *flag_ws;      // [n_rows]
     double *part_ws;       // [N * 5]
@@ -421,8 +521,6 @@ cudaError_t launch_advantage_from_stats(const float *rewards, const int32_t *gro
                                         int32_t unbiased, const uint8_t *traj_mask, const double *glob,
                                         const double *ss, float *adv, float *inv_norm, cudaStream_t s,
                                         int *launches);
-cudaError_t launch_fused_cluster(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
-                                 int *launches, char *why, size_t why_len, grpo_plan_t *plan);
 cudaError_t launch_fused_rowwise(const LossArgs &a, const grpo_tune_t *tune, cudaStream_t s,
                                  int *launches, grpo_plan_t *plan);
 cudaError_t launch_segment_reduce(const LossArgs &a, cudaStream_t s, int *launches);
@@ -430,21 +528,27 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
                                 grpo_plan_t *plan, char *why, size_t why_len);
 int32_t lmhead_n_split(int64_t n_rows, int32_t V);
 cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows, int32_t d, int32_t V,
-                          const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,
+                          const RowInfo *rowinfo, RowPart *part, float *zy, uint16_t *out, int64_t ld_out,
                           const int64_t *targets, const float *lse, const float *scale, float mult,
                           cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len,
                           int cta_group, int32_t col_offset = 0);
-cudaError_t launch_lmhead_rowpart(const float2 *part, const float *zy, int32_t n_split, int64_t n_rows,
+cudaError_t launch_lmhead_rowpart(const RowPart *part, const float *zy, int32_t n_split, int64_t n_rows,
                                   const int64_t *targets, int32_t col_offset, int32_t Vs, float4 *out,
                                   cudaStream_t s, int *launches);
 cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W, int64_t n_rows, int32_t d,
                              int32_t Vs, int32_t world, int32_t rank, float *const *slots, cudaStream_t s,
                              int *launches, char *why, size_t why_len);
+cudaError_t launch_lmhead_gemm_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W, int64_t n_rows,
+                                  int32_t d, int32_t V, void *out, int out_bf16, cudaStream_t s, int *launches,
+                                  char *why, size_t why_len);
+cudaError_t launch_lmhead_gemm_dw(const uint16_t *dz, int64_t ld_dz, const uint16_t *X, int64_t n_rows,
+                                  int32_t d, int32_t V, float *dW, cudaStream_t s, int *launches, char *why,
+                                  size_t why_len);
 cudaError_t launch_lmhead_dx_reduce(const float *own_slots, int32_t world, int64_t n_rows, int32_t d,
                                     int32_t rank, void *out, int out_bf16, cudaStream_t s, int *launches);
 cudaError_t launch_lmhead_tp_combine(const float4 *parts, int32_t R, const LossArgs &a, cudaStream_t s,
                                      int *launches);
-cudaError_t launch_lmhead_combine(const float2 *part, const float *zy, int32_t n_split, const LossArgs &a,
+cudaError_t launch_lmhead_combine(const RowPart *part, const float *zy, int32_t n_split, const LossArgs &a,
                                   cudaStream_t s, int *launches);
 cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned long long *row_ctr,
                       cudaStream_t s, int *launches,
@@ -452,12 +556,18 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned lo
 cudaError_t launch_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_t V, int64_t ld,
                             const int64_t *target_ids, const float *lse, const float *scale,
                             float mult, uint16_t *dlogits, cudaStream_t s, int *launches);
-cudaError_t launch_validate(const int64_t *version_ids, const int64_t *token_version,
-                            const int64_t *cu, const int32_t *group_ids, const int64_t *targets,
-                            const float *logp_behav, int32_t N, int64_t T, int32_t P, int32_t V,
-                            int32_t G, int32_t tbs, int64_t v_theta, int32_t K, uint32_t *flags,
-                            int32_t *group_count, int32_t *stale_hist,
-                            grpo_validate_summary_t *summary, cudaStream_t s, int *launches);
+cudaError_t launch_validate(const int64_t *version_ids, const int64_t *cu, const int32_t *group_ids,
+                            int32_t N, int64_t T, int32_t P, int32_t V, int32_t G, int32_t tbs,
+                            int64_t v_theta, int32_t K, const int64_t *token_version,
+                            const int64_t *targets, const float *logp_behav, const int64_t *tcu,
+                            const int32_t *traj_index, int32_t n_tok_traj, int64_t T_tok,
+                            uint32_t *flags, int32_t *group_count, int32_t *stale_hist,
+                            grpo_validate_summary_t *summary, double *token_counts, cudaStream_t s,
+                            int *launches);
+cudaError_t launch_validate_combine(grpo_validate_summary_t *summary, const double *token_counts,
+                                    cudaStream_t s, int *launches);
+cudaError_t launch_combine_ranks(const double *gathered, int32_t world, int32_t n, double *out,
+                                 cudaStream_t s, int *launches);
 cudaError_t launch_advantage(const float *rewards, const int32_t *group_ids, const int64_t *cu,
                              int32_t N, int32_t P, float std_floor, int32_t norm,
                              int32_t unbiased, const uint8_t *traj_mask, float *adv,

@@ -39,7 +39,8 @@ __device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
 }
 __host__ __device__ constexpr uint64_t splat(uint32_t bits) { return ((uint64_t)bits << 32) | bits; }
 
-constexpr uint64_t kLog2e2 = splat(0x3FB8AA3Bu);     // log2(e)
+constexpr uint64_t kLog2e2 = splat(0x3FB8AA3Bu);     // log2(e) rounded to fp32
+
 constexpr uint64_t kMagic2 = splat(0x4B400000u);     // 1.5 * 2^23
 constexpr uint64_t kNegMagic2 = splat(0xCB400000u);  // -1.5 * 2^23
 constexpr uint64_t kNegOne2 = splat(0xBF800000u);

@@ -38,7 +38,7 @@ struct Params {
     int32_t col_offset;  // first vocabulary id of this W shard (tensor-parallel head), else 0
     // EPI_STATS
     const RowInfo *rowinfo;
-    float2 *part;  // [n_split][n_rows] log2-domain (max, sum)
+    RowPart *part;  // [n_split][n_rows] log2-domain (max, sum fp64)
     float *zy;     // [n_rows]
     // EPI_DZ / EPI_LOGITS
     uint16_t *out;  // [n_rows][ld_out] bf16
@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 lse2 = p.lse[row] * kLog2e;
                 sc = p.scale[row] * p.mult;
             }
-            float M = -INFINITY, S = 0.0f, zy = 0.0f;
+            float M = -INFINITY, zy = 0.0f;
+            double S = 0.0;
             bool have_y = false;
             for (int vt = vt0; vt < vt1; ++vt) {
                 mbar_wait(tfull + acc, acc_phase);
@@ -227,20 +228,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const int cb = v0 + c * 32;          // first vocabulary column of the chunk
                     const int nvalid = min(32, p.V - cb);  // > 0 except in a ragged last tile
                     if (EPI == EPI_STATS) {
-                        float t[32];
-                        float cm = -INFINITY;
+                        // exponents z*log2(e) - M with the exact log2 e (two FMAs, common.cuh
+                        // kLog2eHi/Lo), the chunk's 32 terms summed in fp32, the row's sum in fp64
+                        float zt[32];
+                        float zm = -INFINITY;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            t[j] = j < nvalid ? __uint_as_float(r[j]) * kLog2e : -INFINITY;
-                            cm = fmaxf(cm, t[j]);
+                            zt[j] = j < nvalid ? __uint_as_float(r[j]) : -INFINITY;
+                            zm = fmaxf(zm, zt[j]);
                         }
+                        const float cm = log2_ref(zm);
                         if (cm > M) {
-                            S = (M == -INFINITY) ? 0.0f : S * ex2(M - cm);
+                            S = (M == -INFINITY) ? 0.0 : S * (double)ex2(M - cm);
                             M = cm;
                         }
                         if (M != -INFINITY) {
+                            float cs = 0.0f;
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) S += ex2(t[j] - M);
+                            for (int j = 0; j < 32; ++j) cs += ex2(fmaf(zt[j], kLog2eLo, fmaf(zt[j], kLog2eHi, -M)));
+                            S += (double)cs;
                         }
                         if (y >= cb && y < cb + 32) {
 #pragma unroll
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (acc == 0) acc_phase ^= 1u;
             }
             if (EPI == EPI_STATS && valid) {
-                p.part[(int64_t)split * p.n_rows + row] = make_float2(M, S);
+                p.part[(int64_t)split * p.n_rows + row] = RowPart{M, 0.0f, S};
                 if (have_y) p.zy[row] = zy;
             }
         }
@@ -303,25 +309,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // per row: merge the n_split partials in split order (deterministic), then the
 // per-token epilogue shared with the logits kernels
-__global__ void __launch_bounds__(256) lmhead_combine_kernel(const float2 *__restrict__ part,
+__global__ void __launch_bounds__(256) lmhead_combine_kernel(const RowPart *__restrict__ part,
                                                              const float *__restrict__ zy_ws,
                                                              int32_t n_split, LossArgs a) {
     const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (row >= a.n_rows) return;
-    float M = -INFINITY, S = 0.0f;
+    float M = -INFINITY;
+    double S = 0.0;
     for (int s = 0; s < n_split; ++s) {
-        const float2 v = part[(int64_t)s * a.n_rows + row];
-        lse2_merge(M, S, v.x, v.y);
+        const RowPart v = part[(int64_t)s * a.n_rows + row];
+        lse2_merge(M, S, v.a, v.s);
     }
     const RowInfo ri = a.rowinfo[row];
     const bool y_valid = ri.target >= 0 && ri.target < a.V;
     const float zyv = y_valid ? zy_ws[row] : __int_as_float(0x7FC00000);
-    const float l2s = log2f(S);
+    const double l2s = log2(S);
     const double logp_d = row_logp(zyv, M, l2s);
     const RowOut o = row_epilogue(logp_d, ri, a.eps_lo, a.eps_hi, a.grad_scale);
     const float logp = (float)logp_d;
     if (a.logp_out) a.logp_out[row] = logp;
-    if (a.lse_out) a.lse_out[row] = (M + l2s) * kLn2;
+    if (a.lse_out) a.lse_out[row] = (float)(((double)M + l2s) * 0.69314718055994530942);
     if (a.scale_out) a.scale_out[row] = o.s;
     a.term_ws[row] = o.term;
     a.logp_ws[row] = logp;
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(256) lmhead_combine_kernel(const float2 *__res
 
 // tensor-parallel head: this shard's per-row partial (log2-domain max, sum, z_y, holds-y)
 // from its n_split unit partials, merged in unit order
-__global__ void __launch_bounds__(256) lmhead_rowpart_kernel(const float2 *__restrict__ part,
+__global__ void __launch_bounds__(256) lmhead_rowpart_kernel(const RowPart *__restrict__ part,
                                                              const float *__restrict__ zy_ws,
                                                              int32_t n_split, int64_t n_rows,
                                                              const int64_t *__restrict__ targets,
@@ -338,14 +345,15 @@ __global__ void __launch_bounds__(256) lmhead_rowpart_kernel(const float2 *__res
                                                              float4 *__restrict__ out) {
     const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (row >= n_rows) return;
-    float M = -INFINITY, S = 0.0f;
+    float M = -INFINITY;
+    double S = 0.0;
     for (int s = 0; s < n_split; ++s) {
-        const float2 v = part[(int64_t)s * n_rows + row];
-        lse2_merge(M, S, v.x, v.y);
+        const RowPart v = part[(int64_t)s * n_rows + row];
+        lse2_merge(M, S, v.a, v.s);
     }
     const int64_t t = targets[row];
     const bool mine = t >= col_offset && t - col_offset < Vs;
-    out[row] = make_float4(M, S, mine ? zy_ws[row] : 0.0f, mine ? 1.0f : 0.0f);
+    out[row] = pack_shard_part(M, S, mine ? zy_ws[row] : 0.0f, mine);
 }
 
 // the R shards' partials of each row merged in rank order (identical on every rank), then
@@ -354,21 +362,25 @@ __global__ void __launch_bounds__(256) lmhead_tp_combine_kernel(const float4 *__
                                                                 int32_t R, LossArgs a) {
     const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (row >= a.n_rows) return;
-    float M = -INFINITY, S = 0.0f, zy = __int_as_float(0x7FC00000);
+    float M = -INFINITY, zy = __int_as_float(0x7FC00000);
+    double S = 0.0;
     for (int q = 0; q < R; ++q) {
-        const float4 v = parts[(int64_t)q * a.n_rows + row];
-        lse2_merge(M, S, v.x, v.y);
-        if (v.w != 0.0f) zy = v.z;
+        float qa, qz;
+        double qs;
+        bool holds;
+        unpack_shard_part(parts[(int64_t)q * a.n_rows + row], qa, qs, qz, holds);
+        lse2_merge(M, S, qa, qs);
+        if (holds) zy = qz;
     }
     const RowInfo ri = a.rowinfo[row];
     const bool y_valid = ri.target >= 0 && ri.target < a.V;
     const float zyv = y_valid ? zy : __int_as_float(0x7FC00000);
-    const float l2s = log2f(S);
+    const double l2s = log2(S);
     const double logp_d = row_logp(zyv, M, l2s);
     const RowOut o = row_epilogue(logp_d, ri, a.eps_lo, a.eps_hi, a.grad_scale);
     const float logp = (float)logp_d;
     if (a.logp_out) a.logp_out[row] = logp;
-    if (a.lse_out) a.lse_out[row] = (M + l2s) * kLn2;
+    if (a.lse_out) a.lse_out[row] = (float)(((double)M + l2s) * 0.69314718055994530942);
     if (a.scale_out) a.scale_out[row] = o.s;
     a.term_ws[row] = o.term;
     a.logp_ws[row] = logp;
@@ -415,7 +427,7 @@ int32_t lmhead_n_split(int64_t n_rows, int32_t V) {
 }
 
 cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows, int32_t d, int32_t V,
-                          const RowInfo *rowinfo, float2 *part, float *zy, uint16_t *out, int64_t ld_out,
+                          const RowInfo *rowinfo, RowPart *part, float *zy, uint16_t *out, int64_t ld_out,
                           const int64_t *targets, const float *lse, const float *scale, float mult,
                           cudaStream_t s, int *launches, grpo_plan_t *plan, char *why, size_t why_len,
                           int cta_group, int32_t col_offset) {
@@ -497,7 +509,7 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     return cudaSuccess;
 }
 
-cudaError_t launch_lmhead_rowpart(const float2 *part, const float *zy, int32_t n_split, int64_t n_rows,
+cudaError_t launch_lmhead_rowpart(const RowPart *part, const float *zy, int32_t n_split, int64_t n_rows,
                                   const int64_t *targets, int32_t col_offset, int32_t Vs, float4 *out,
                                   cudaStream_t s, int *launches) {
     if (n_rows == 0) return cudaSuccess;
@@ -515,7 +527,7 @@ cudaError_t launch_lmhead_tp_combine(const float4 *parts, int32_t R, const LossA
     return cudaGetLastError();
 }
 
-cudaError_t launch_lmhead_combine(const float2 *part, const float *zy, int32_t n_split, const LossArgs &a,
+cudaError_t launch_lmhead_combine(const RowPart *part, const float *zy, int32_t n_split, const LossArgs &a,
                                   cudaStream_t s, int *launches) {
     if (a.n_rows == 0) return cudaSuccess;
     lm::lmhead_combine_kernel<<<(unsigned)((a.n_rows + 255) / 256), 256, 0, s>>>(part, zy, n_split, a);

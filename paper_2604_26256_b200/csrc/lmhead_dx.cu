@@ -1,5 +1,7 @@
-// lmhead_dx.cu -- the tensor-parallel LM head's input gradient as ONE kernel that computes
-// and communicates: dX = sum_q dz_q W_q over the R ranks of a vocabulary-parallel group
+// lmhead_dx.cu -- the LM head's backward GEMMs on the tensor cores:
+// dX = dz W and dW += dz^T X from the bf16 logits gradient dz (launch_lmhead_gemm_dx / _dw),
+// and the tensor-parallel LM head's input gradient as ONE kernel that computes and
+// communicates: dX = sum_q dz_q W_q over the R ranks of a vocabulary-parallel group
 // (Megatron layout), reduce-scattered by rows.  Each rank's tcgen05 GEMM computes
 // its partial dz_q W_q (A = dz_q, K-major over the shard's vocabulary; B = W_q read
 // MN-major, i.e. straight from the row-major [Vs, d] weight) and the epilogue stores every
@@ -20,19 +22,33 @@ namespace lmdx {
 
 constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 192;
 
+// Epilogues: EPI_SLOTS stores f32 tiles into the owner rank's slot (the tensor-parallel
+// dX reduce-scatter); EPI_BF16 / EPI_F32 store D; EPI_F32_ACC adds D into an f32 array.
+enum { EPI_SLOTS = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_F32_ACC = 3 };
+
 struct Params {
-    int32_t n_rows, d, Vs;
+    int32_t M, N, K;                  // D[M, N] = A[M, K] * B[K, N]
     int32_t m_tiles, n_tiles, n_units;
+    int32_t raster_n;                 // 1: n tile fastest (dW: the small B stays in L2)
     int32_t world, rank, rows_per_rank;
-    float *slots[GRPO_VP_MAX_RANKS];  // slot buffers of every rank: [world][rows_per_rank][d]
+    float *slots[GRPO_VP_MAX_RANKS];  // EPI_SLOTS: slot buffers of every rank [world][rows_per_rank][N]
+    void *out;                        // EPI_BF16 / EPI_F32 / EPI_F32_ACC: [M][ldo]
+    int64_t ldo;
 };
 
-// Units (m_tile, n_tile) rastered in groups of GM row tiles (row tile fastest): the pairs
-// running at the same time cover ~GM row tiles x ~grid/GM column tiles and, moving through
-// K at about the same pace, share each A and B k-block in L2 instead of re-reading dz
-// (K = the shard's vocabulary, tens of MB per row tile) from HBM.
+// Units (m_tile, n_tile).  raster_n = 0: groups of GM row tiles, row tile fastest -- the pairs
+// running at the same time cover ~GM row tiles x ~grid/GM column tiles and, moving through K
+// at about the same pace, share each A and B k-block in L2 instead of re-reading the long-K
+// operands (dX: K = the vocabulary, tens of MB per row tile) from HBM.  raster_n = 1: column
+// tile fastest -- dW = dz^T X has K = the row count and a small B (X, ~84 MB at 8190 x 5120),
+// so the column tiles of one row tile (one dz column block) run together and dz streams once.
 constexpr int GM = 8;
-__device__ __forceinline__ void dx_decode(const Params &p, int unit, int &m_tile, int &n_tile) {
+__device__ __forceinline__ void decode(const Params &p, int unit, int &m_tile, int &n_tile) {
+    if (p.raster_n) {
+        m_tile = unit / p.n_tiles;
+        n_tile = unit - m_tile * p.n_tiles;
+        return;
+    }
     const int per_group = GM * p.n_tiles;
     const int grp = unit / per_group;
     const int rem = unit - grp * per_group;
@@ -41,30 +57,37 @@ __device__ __forceinline__ void dx_decode(const Params &p, int unit, int &m_tile
     n_tile = rem / gm;
 }
 
-// Shared-memory matrix descriptor, MN-major, 128-byte swizzle: 64-element rows along N,
-// 8 K-rows per 1 KB atom (SBO = 1024 B between K atoms), N atoms of 64 elements LBO apart.
+// Shared-memory matrix descriptor, MN-major, 128-byte swizzle: 64-element rows along M or N,
+// 8 K-rows per 1 KB atom (SBO = 1024 B between K atoms), MN atoms of 64 elements LBO apart.
 __device__ __forceinline__ uint64_t desc_mn_sw128(const void *smem_tile, uint32_t lbo_bytes) {
     const uint64_t addr = smem_u32(smem_tile);
     return ((addr >> 4) & 0x3FFFull) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16) | (64ull << 32) |
            (1ull << 46) | (2ull << 61);
 }
 
-// kind::f16, D f32, A bf16 K-major, B bf16 MN-major (bit 16)
-__host__ __device__ constexpr uint32_t idesc_kmn(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// kind::f16, D f32, A and B bf16; A K-major (bit 15 = 0) or MN-major (1), B MN-major (bit 16)
+__host__ __device__ constexpr uint32_t idesc_b_mn(int M, int N, bool a_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | (1u << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// CG = 2: a CTA pair (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each CTA stages
-// its own 128 rows of dz and half of the tile's BN columns of W; the leader issues the MMA.
-template <int BN, int CG>
+// One persistent warp-specialised tcgen05 GEMM for the LM head's backward: warp 0 issues TMA
+// (A: K-major 128 x 64 boxes, or MN-major 64 x 64 boxes; B: MN-major 64 x 64 boxes, i.e. both
+// read straight from row-major [K, M] / [K, N] arrays without a transpose), warp 1 of the pair
+// leader issues tcgen05.mma (M = 128 * CG, N = BN) into one of two TMEM accumulators, warps
+// 2-5 of each CTA drain their 128 TMEM lanes (one thread = one row of D) into the epilogue.
+// CG = 2: a CTA pair (cluster of 2, tcgen05.mma.cta_group::2): each CTA stages its own 128
+// rows of A and half of the tile's BN columns of B.
+template <bool A_MN, int BN, int CG, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    dx_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
     constexpr int A_BYTES = BM * BK * 2;          // 16 KB
     constexpr int NB = BN / 64 / CG;              // 64-wide N atoms staged per CTA
-    constexpr int B_ATOM = BK * 64 * 2;           // 8 KB: 64 K-rows x 64 N elements
-    constexpr int STAGE = A_BYTES + NB * B_ATOM;
+    constexpr int ATOM = BK * 64 * 2;             // 8 KB: 64 K-rows x 64 MN elements
+    constexpr int STAGE = A_BYTES + NB * ATOM;
     constexpr int NS = CG == 1 ? STAGES : 6;
     constexpr uint32_t TMEM_COLS = 2 * BN;
+    static_assert(NB >= 1, "BN / CG must be a multiple of 64");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem, *sB = smem + NS * A_BYTES;
@@ -72,7 +95,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t *full = bars, *empty = bars + NS, *tfull = bars + 2 * NS, *tempty = bars + 2 * NS + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nk = (p.Vs + BK - 1) / BK;
+    const int nk = (p.K + BK - 1) / BK;
     const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
     const int cta_id = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
     const int n_ctas = CG == 2 ? (int)ncluster_x() : (int)gridDim.x;
@@ -107,25 +130,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t phase = 0;
             for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
                 int m_tile, n_tile;
-                dx_decode(p, unit, m_tile, n_tile);
+                decode(p, unit, m_tile, n_tile);
                 const int a_row = m_tile * BM * CG + (int)crank * BM;
                 const int b_col = n_tile * BN + (int)crank * (BN / CG);
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1u);
+                    uint8_t *dA = sA + stage * A_BYTES;
+                    uint8_t *dB = sB + stage * NB * ATOM;
                     if (CG == 1) {
                         mbar_arrive_expect_tx(full + stage, STAGE);
-                        tc::tma_load_2d(sA + stage * A_BYTES, &tmA, kb * BK, a_row, full + stage, pol);
+                        if (A_MN) {
+                            tc::tma_load_2d(dA, &tmA, a_row, kb * BK, full + stage, pol);
+                            tc::tma_load_2d(dA + ATOM, &tmA, a_row + 64, kb * BK, full + stage, pol);
+                        } else {
+                            tc::tma_load_2d(dA, &tmA, kb * BK, a_row, full + stage, pol);
+                        }
 #pragma unroll
                         for (int j = 0; j < NB; ++j)
-                            tc::tma_load_2d(sB + stage * NB * B_ATOM + j * B_ATOM, &tmB, b_col + j * 64, kb * BK,
-                                            full + stage, pol);
+                            tc::tma_load_2d(dB + j * ATOM, &tmB, b_col + j * 64, kb * BK, full + stage, pol);
                     } else {
                         if (crank == 0) mbar_arrive_expect_tx(full + stage, 2 * STAGE);
-                        tc::tma_load_2d_pair(sA + stage * A_BYTES, &tmA, kb * BK, a_row, full + stage, pol);
+                        if (A_MN) {
+                            tc::tma_load_2d_pair(dA, &tmA, a_row, kb * BK, full + stage, pol);
+                            tc::tma_load_2d_pair(dA + ATOM, &tmA, a_row + 64, kb * BK, full + stage, pol);
+                        } else {
+                            tc::tma_load_2d_pair(dA, &tmA, kb * BK, a_row, full + stage, pol);
+                        }
 #pragma unroll
                         for (int j = 0; j < NB; ++j)
-                            tc::tma_load_2d_pair(sB + stage * NB * B_ATOM + j * B_ATOM, &tmB, b_col + j * 64,
-                                                 kb * BK, full + stage, pol);
+                            tc::tma_load_2d_pair(dB + j * ATOM, &tmB, b_col + j * 64, kb * BK, full + stage, pol);
                     }
                     if (++stage == NS) {
                         stage = 0;
@@ -136,7 +169,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 1) {
         if (lane == 0 && crank == 0) {  // ---- MMA issuer (the pair's leader)
-            constexpr uint32_t idesc = idesc_kmn(BM * CG, BN);
+            constexpr uint32_t idesc = idesc_b_mn(BM * CG, BN, A_MN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
@@ -146,12 +179,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(full + stage, phase);
                     tc::fence_after();
-                    const uint64_t ad = tc::desc_k_sw128(sA + stage * A_BYTES);
-                    const uint64_t bd = desc_mn_sw128(sB + stage * NB * B_ATOM, B_ATOM);
+                    const uint64_t ad = A_MN ? desc_mn_sw128(sA + stage * A_BYTES, ATOM)
+                                             : tc::desc_k_sw128(sA + stage * A_BYTES);
+                    const uint64_t bd = desc_mn_sw128(sB + stage * NB * ATOM, ATOM);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {  // A: +32 B inside its atom; B: +16 K-rows = 2 KB
-                        if (CG == 1) tc::mma_bf16(d_tmem, ad + 2u * k, bd + 128u * k, idesc, (kb | k) != 0);
-                        else tc::mma2_bf16(d_tmem, ad + 2u * k, bd + 128u * k, idesc, (kb | k) != 0);
+                    for (int k = 0; k < BK / 16; ++k) {
+                        // K-major A: +32 B inside its swizzle atom; MN-major: +16 K-rows = 2 KB
+                        const uint64_t a_k = A_MN ? ad + 128u * k : ad + 2u * k;
+                        if (CG == 1) tc::mma_bf16(d_tmem, a_k, bd + 128u * k, idesc, (kb | k) != 0);
+                        else tc::mma2_bf16(d_tmem, a_k, bd + 128u * k, idesc, (kb | k) != 0);
                     }
                     if (CG == 1) tc::commit(empty + stage);
                     else tc::commit2_multicast(empty + stage, 0x3);
@@ -166,32 +202,58 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (acc == 0) acc_phase ^= 1u;
             }
         }
-    } else {  // ---- epilogue: each thread one row of the tile, straight to the owner's slot
+    } else {  // ---- epilogue: each thread one row of the tile
         const int q = warp & 3;
         const int r_in_tile = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
             int m_tile, n_tile;
-            dx_decode(p, unit, m_tile, n_tile);
+            decode(p, unit, m_tile, n_tile);
             const int row = m_tile * BM * CG + (int)crank * BM + r_in_tile;
             mbar_wait(tfull + acc, acc_phase);
             tc::fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-            const bool valid = row < p.n_rows;
-            const int owner = valid ? row / p.rows_per_rank : 0;
-            float *dst = valid ? p.slots[owner] + ((int64_t)p.rank * p.rows_per_rank + (row - owner * p.rows_per_rank)) *
-                                                      p.d + n_tile * BN
-                               : nullptr;
+            const bool valid = row < p.M;
+            int64_t off = 0;  // element offset of this row's first column of the tile
+            float *slot_dst = nullptr;
+            if (EPI == EPI_SLOTS && valid) {
+                const int owner = row / p.rows_per_rank;
+                slot_dst = p.slots[owner] + ((int64_t)p.rank * p.rows_per_rank + (row - owner * p.rows_per_rank)) *
+                                                p.N + n_tile * BN;
+            } else {
+                off = (int64_t)row * p.ldo + (int64_t)n_tile * BN;
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
                 tc::tmem_ld32(t_row + (uint32_t)(c * 32), r);
                 tc::tmem_wait_ld();
-                if (valid) {
-                    uint4 *d4 = reinterpret_cast<uint4 *>(dst + c * 32);
+                if (!valid) continue;
+                if (EPI == EPI_SLOTS || EPI == EPI_F32) {
+                    float *dst = EPI == EPI_SLOTS ? slot_dst + c * 32 : static_cast<float *>(p.out) + off + c * 32;
+                    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) d4[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+                } else if (EPI == EPI_F32_ACC) {
+                    float4 *d4 = reinterpret_cast<float4 *>(static_cast<float *>(p.out) + off + c * 32);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float4 v = d4[j];
+                        v.x += __uint_as_float(r[4 * j]);
+                        v.y += __uint_as_float(r[4 * j + 1]);
+                        v.z += __uint_as_float(r[4 * j + 2]);
+                        v.w += __uint_as_float(r[4 * j + 3]);
+                        d4[j] = v;
+                    }
+                } else {  // EPI_BF16
+                    uint4 *d4 = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(p.out) + off + c * 32);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        d4[j] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * j]), __uint_as_float(r[8 * j + 1])),
+                                           pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3])),
+                                           pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5])),
+                                           pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7])));
                 }
             }
             tc::fence_before();
@@ -262,34 +324,24 @@ static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int64_t inn
 
 }  // namespace lmdx
 
-cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W, int64_t n_rows, int32_t d,
-                             int32_t Vs, int32_t world, int32_t rank, float *const *slots, cudaStream_t s,
-                             int *launches, char *why, size_t why_len) {
-    using namespace lmdx;
-    if (n_rows == 0) return cudaSuccess;
-    const int BN = d % 256 == 0 ? 256 : 128;
-    const int CG = 2;  // CTA pairs (tcgen05.mma.cta_group::2), as the LM-head kernel
-    CUtensorMap ma, mb;
-    if (!make_map(&ma, dz, n_rows, Vs, ld_dz, BM) || !make_map(&mb, W, Vs, d, d, BK)) {
-        if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
-        return cudaErrorInvalidValue;
-    }
-    Params p{};
-    p.n_rows = (int32_t)n_rows;
-    p.d = d;
-    p.Vs = Vs;
-    p.m_tiles = (int32_t)((n_rows + BM * CG - 1) / (BM * CG));
-    p.n_tiles = d / BN;
+namespace lmdx {
+
+// launch gemm_kernel<A_MN, BN, CG, EPI> persistently: one CTA (pair) per SM (pair)
+template <bool A_MN, int BN, int CG, int EPI>
+static cudaError_t launch_gemm(const CUtensorMap &ma, const CUtensorMap &mb, Params &p, cudaStream_t s) {
+    constexpr int NB = BN / 64 / CG;
+    constexpr int NS = CG == 1 ? STAGES : 6;
+    constexpr int SMEM = NS * (BM * BK * 2 + NB * BK * 64 * 2) + 1024 + 256;
+    p.m_tiles = (p.M + BM * CG - 1) / (BM * CG);
+    p.n_tiles = p.N / BN;
     p.n_units = p.m_tiles * p.n_tiles;
-    p.world = world;
-    p.rank = rank;
-    p.rows_per_rank = (int32_t)((n_rows + world - 1) / world);
-    for (int q = 0; q < world; ++q) p.slots[q] = slots[q];
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int groups = std::min(p.n_units, n_sm / CG);
-    cudaError_t e;
+    auto kfn = gemm_kernel<A_MN, BN, CG, EPI>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -298,24 +350,93 @@ cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3((unsigned)(groups * CG));
     cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = SMEM;
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (BN == 256) {
-        constexpr int SMEM = 6 * (BM * BK * 2 + 2 * BK * 64 * 2) + 1024 + 256;
-        cfg.dynamicSmemBytes = SMEM;
-        e = cudaFuncSetAttribute(dx_kernel<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaLaunchKernelEx(&cfg, dx_kernel<256, 2>, ma, mb, p);
-    } else {
-        constexpr int SMEM = 6 * (BM * BK * 2 + 1 * BK * 64 * 2) + 1024 + 256;
-        cfg.dynamicSmemBytes = SMEM;
-        e = cudaFuncSetAttribute(dx_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaLaunchKernelEx(&cfg, dx_kernel<128, 2>, ma, mb, p);
-    }
+    e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, p);
     if (e != cudaSuccess) return e;
-    e = cudaGetLastError();
+    return cudaGetLastError();
+}
+
+// the N tile by the GEMM's N (= d): 256 with CTA pairs, 128 with pairs, 64 on one CTA
+template <bool A_MN, int EPI>
+static cudaError_t launch_by_n(const CUtensorMap &ma, const CUtensorMap &mb, Params &p, cudaStream_t s) {
+    if (p.N % 256 == 0) return launch_gemm<A_MN, 256, 2, EPI>(ma, mb, p, s);
+    if (p.N % 128 == 0) return launch_gemm<A_MN, 128, 2, EPI>(ma, mb, p, s);
+    return launch_gemm<A_MN, 64, 1, EPI>(ma, mb, p, s);
+}
+
+}  // namespace lmdx
+
+cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W, int64_t n_rows, int32_t d,
+                             int32_t Vs, int32_t world, int32_t rank, float *const *slots, cudaStream_t s,
+                             int *launches, char *why, size_t why_len) {
+    using namespace lmdx;
+    if (n_rows == 0) return cudaSuccess;
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, dz, n_rows, Vs, ld_dz, BM) || !make_map(&mb, W, Vs, d, d, BK)) {
+        if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
+        return cudaErrorInvalidValue;
+    }
+    Params p{};
+    p.M = (int32_t)n_rows;
+    p.N = d;
+    p.K = Vs;
+    p.world = world;
+    p.rank = rank;
+    p.rows_per_rank = (int32_t)((n_rows + world - 1) / world);
+    for (int q = 0; q < world; ++q) p.slots[q] = slots[q];
+    cudaError_t e = d % 256 == 0 ? launch_gemm<false, 256, 2, EPI_SLOTS>(ma, mb, p, s)
+                                 : launch_gemm<false, 128, 2, EPI_SLOTS>(ma, mb, p, s);
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+    return cudaSuccess;
+}
+
+// dX = dz W  (A = dz [n_rows, V] K-major, B = W [V, d] MN-major): out [n_rows, d] bf16 or f32
+cudaError_t launch_lmhead_gemm_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *W, int64_t n_rows,
+                                  int32_t d, int32_t V, void *out, int out_bf16, cudaStream_t s, int *launches,
+                                  char *why, size_t why_len) {
+    using namespace lmdx;
+    if (n_rows == 0) return cudaSuccess;
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, dz, n_rows, V, ld_dz, BM) || !make_map(&mb, W, V, d, d, BK)) {
+        if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
+        return cudaErrorInvalidValue;
+    }
+    Params p{};
+    p.M = (int32_t)n_rows;
+    p.N = d;
+    p.K = V;
+    p.out = out;
+    p.ldo = d;
+    const cudaError_t e = out_bf16 ? launch_by_n<false, EPI_BF16>(ma, mb, p, s) : launch_by_n<false, EPI_F32>(ma, mb, p, s);
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+    return cudaSuccess;
+}
+
+// dW += dz^T X  (A = dz^T: dz [n_rows, V] read MN-major, B = X [n_rows, d] MN-major, K = n_rows):
+// dW [V, d] f32, accumulated
+cudaError_t launch_lmhead_gemm_dw(const uint16_t *dz, int64_t ld_dz, const uint16_t *X, int64_t n_rows,
+                                  int32_t d, int32_t V, float *dW, cudaStream_t s, int *launches, char *why,
+                                  size_t why_len) {
+    using namespace lmdx;
+    if (n_rows == 0) return cudaSuccess;
+    CUtensorMap ma, mb;
+    if (!make_map(&ma, dz, n_rows, V, ld_dz, BK) || !make_map(&mb, X, n_rows, d, d, BK)) {
+        if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
+        return cudaErrorInvalidValue;
+    }
+    Params p{};
+    p.M = V;
+    p.N = d;
+    p.K = (int32_t)n_rows;
+    p.raster_n = 1;
+    p.out = dW;
+    p.ldo = d;
+    const cudaError_t e = launch_by_n<true, EPI_F32_ACC>(ma, mb, p, s);
     if (e != cudaSuccess) return e;
     *launches += 1;
     return cudaSuccess;

@@ -65,7 +65,9 @@ struct RowwiseParams {
     int64_t n_rows;
     const RowInfo *rowinfo;
     float eps_lo, eps_hi, grad_scale;
-    float *logp_out, *lse_out, *scale_out, *term_ws, *logp_ws;
+    float *logp_out, *lse_out, *scale_out;
+    double *term_ws;
+    float *logp_ws;
     uint8_t *flag_ws;
     int32_t prefetch;
     int32_t flags;  // bit 0: pass 2 in reverse batch order; bit 1: pass-1 policy evict_normal
@@ -90,8 +92,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
     using B = RowwiseBatch<NT, U>;
     constexpr int NW = NT / 32;
     constexpr int BV = NT * U;  // vectors per batch
-    __shared__ float2 red[NW];
-    __shared__ float row_scalars[4];          // lse2 (log2 domain), s, zy, y
+    __shared__ RowPart red[NW];
+    __shared__ float row_scalars[4];          // lse2 (log2 domain), s, g_y = s (p_y - 1), y
     __shared__ float4 xpart[2][C];            // cluster exchange, double-buffered by row parity
     extern __shared__ uint4 row_cache[];      // [cache_vecs][NT]
     const uint32_t crank = C > 1 ? cluster_ctarank() : 0;
@@ -128,7 +130,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                 zy_pre = zrow[y_loc];
         }
         // ---- pass 1
-        float a = -INFINITY, s = 0.0f;
+        float a = -INFINITY;
+        double s = 0.0;
         for (int bi = 0; bi < n_full; ++bi) {
             const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + bi * BV + threadIdx.x;
             uint4 x[U];
@@ -157,13 +160,14 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
             B::reduce(x, a, s);
         }
         warp_lse2_combine(a, s);
-        if (lane == 0) red[warp] = make_float2(a, s);
+        if (lane == 0) red[warp] = RowPart{a, 0.0f, s};
         __syncthreads();
         if (warp == 0) {
-            float cm = -INFINITY, cs = 0.0f;
+            float cm = -INFINITY;
+            double cs = 0.0;
             if (lane < NW) {
-                cm = red[lane].x;
-                cs = red[lane].y;
+                cm = red[lane].a;
+                cs = red[lane].s;
             }
             warp_lse2_combine(cm, cs);
             const RowInfo ri = ri_pre;
@@ -174,16 +178,18 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
             if (C > 1) {
                 // every CTA of the cluster gets this CTA's partial (and z_y if it owns y)
                 if (lane < C) {
-                    const float4 msg = make_float4(cm, cs, zy, mine ? 1.0f : 0.0f);
+                    // (a, z_y, s fp64 with the holds-y bit in its sign)
+                    const uint64_t sb = (uint64_t)__double_as_longlong(cs) | (mine ? (1ull << 63) : 0ull);
                     const uint32_t raddr = mapa_shared(smem_u32(&xpart[parity][crank]), lane);
-                    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(raddr),
-                                 "f"(msg.x), "f"(msg.y), "f"(msg.z), "f"(msg.w)
+                    asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(raddr),
+                                 "r"(__float_as_uint(cm)), "r"(__float_as_uint(zy)), "r"((uint32_t)sb),
+                                 "r"((uint32_t)(sb >> 32))
                                  : "memory");
                 }
             }
             if (C == 1 && lane == 0) {
-                const float l2s = log2f(cs);
-                const float lse2 = cm + l2s;
+                const double l2s = row_l2s(cs, cm);
+                const float lse2 = cm + (float)l2s;
                 const float zyv = y_valid ? zy : __int_as_float(0x7FC00000);
                 const double logp_d = row_logp(zyv, cm, l2s);
                 const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
@@ -196,21 +202,23 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                 p.flag_ws[row] = o.flags;
                 row_scalars[0] = lse2;
                 row_scalars[1] = o.s;
-                row_scalars[2] = zyv;
+                row_scalars[2] = o.gy;
                 row_scalars[3] = __int_as_float(y_valid ? ri.target : -1);
             }
         }
         if (C > 1) {
             cluster_sync_all();  // the partials of every CTA of the cluster have landed
             if (warp == 0) {
-                float M = -INFINITY, S = 0.0f, zsrc = 0.0f;
+                float M = -INFINITY, zsrc = 0.0f;
+                double S = 0.0;
                 bool own = false;
                 if (lane < C) {
-                    const float4 m4 = xpart[parity][lane];
-                    M = m4.x;
-                    S = m4.y;
-                    zsrc = m4.z;
-                    own = m4.w != 0.0f;
+                    const uint4 m4 = reinterpret_cast<const uint4 &>(xpart[parity][lane]);
+                    const uint64_t sb = ((uint64_t)m4.w << 32) | m4.z;
+                    M = __uint_as_float(m4.x);
+                    zsrc = __uint_as_float(m4.y);
+                    S = __longlong_as_double((long long)(sb & ~(1ull << 63)));
+                    own = (sb >> 63) != 0ull;
                 }
                 warp_lse2_combine(M, S);    // identical bits in every CTA of the cluster
                 const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
@@ -219,8 +227,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                     const RowInfo ri = p.rowinfo[row];
                     const bool y_valid = own_mask != 0u;
                     const float zyv = y_valid ? zsh : __int_as_float(0x7FC00000);
-                    const float l2s = log2f(S);
-                    const float lse2 = M + l2s;
+                    const double l2s = row_l2s(S, M);
+                    const float lse2 = M + (float)l2s;
                     const double logp_d = row_logp(zyv, M, l2s);
                     const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                     if (crank == 0) {
@@ -234,7 +242,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                     }
                     row_scalars[0] = lse2;
                     row_scalars[1] = o.s;
-                    row_scalars[2] = zyv;
+                    row_scalars[2] = o.gy;
                     row_scalars[3] = __int_as_float(y_valid ? ri.target : -1);
                 }
             }
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
         __syncthreads();
         // ---- pass 2: dlogits = s (softmax - onehot), written once
         if (p.dlogits) {
-            const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
+            const float lse2 = row_scalars[0], sc = row_scalars[1], gy = row_scalars[2];
             const auto gref = B::grad_ref(sc, lse2);
             const int32_t y = __float_as_int(row_scalars[3]);
             const int y_loc = y >= 0 ? y - vec_lo * 8 : -1;
@@ -288,11 +296,10 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) rowwise_kern
                         }
                     }
                 }
-                // the target entry: s (p_y - 1) from the unrounded probability, by the thread
+                // the target entry: s (p_y - 1) from the epilogue (fp64 expm1), by the thread
                 // whose vector store covered it (program order keeps this store last)
                 if (yv >= 0 && (yv % NT) == (int)threadIdx.x) {
-                    const float py = ex2(fmaf(zy, kLog2e, -lse2));
-                    drow[y_loc] = f2bf(sc * (py - 1.0f));
+                    drow[y_loc] = f2bf(gy);
                 }
             }
         }
@@ -410,7 +417,7 @@ constexpr int kSegThreads = 256;
 __global__ void __launch_bounds__(kSegThreads)
     segsum_kernel(int64_t row_begin, int64_t n_rows, const int64_t *__restrict__ cu, int32_t N,
                   const int32_t *__restrict__ traj_index, const float *__restrict__ inv_norm,
-                  const float *__restrict__ term, const float *__restrict__ logp,
+                  const double *__restrict__ term, const float *__restrict__ logp,
                   const uint8_t *__restrict__ flags, double *__restrict__ traj_sum,
                   double *__restrict__ part) {
     __shared__ double sh[5][kSegThreads / 32];
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kSegThreads)
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     for (int64_t t = b + threadIdx.x; t < e; t += kSegThreads) {
         const int64_t k = t - row_begin;
-        const double x = (double)term[k];
+        const double x = term[k];
         acc[0] += x;
         acc[1] += fabs(x);
         acc[2] += (double)logp[k];

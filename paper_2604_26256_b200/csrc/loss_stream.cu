@@ -4,21 +4,30 @@
 // from L2 in pass 2; with two 304 KB rows in flight per SM about 10 % of the re-reads
 // miss L2.  K3c gives each SM one row at a time and moves it with the bulk-copy engine
 // (cp.async.bulk global -> shared, completion on mbarriers) into a FIFO ring of NS
-// 16 KB slots, so the loads need neither registers nor L1 staging and almost the whole
-// shared memory holds row data:
+// slots, so the loads need neither registers nor L1 staging and almost the whole
+// shared memory holds row data.  Three roles:
 //
-//   producer (one thread)   loads, per row, chunks 0..n-1 (pass 1) and then re-loads
-//                           chunks 0..n-R-1 (the part of the row that did not stay
-//                           resident) for pass 2, slot k % NS for the k-th load;
-//   consumers (NT threads)  pass 1 over chunks 0..n-1 (log2-domain max / sum), releasing
-//                           chunks 0..n-R-1; block reduction + fp64 row epilogue; pass 2
-//                           over the resident chunks n-R..n-1, then the re-loaded ones,
-//                           writing dlogits and releasing every slot.
+//   producer (one thread)   loads, per row k, the pass-1 chunks of row k, then the first
+//                           LA chunks of row k+1 (the look-ahead), then the re-loads of
+//                           row k's chunks 0..n-R-1 (the part that did not stay resident)
+//                           for pass 2, slot j % NS for the j-th load;
+//   consumers (NT threads)  pass 1 of row k (log2-domain max / sum; the first LA chunks
+//                           were consumed in the previous row's look-ahead), publish the
+//                           warps' partials, pass 1 of row k+1's first LA chunks, then pass
+//                           2 of row k (the R resident chunks, then the re-loads), writing
+//                           dlogits and releasing every slot;
+//   epilogue warp           per row: waits for the 16 warp partials, combines them (and,
+//                           with SPLIT = 2, exchanges them with the partner CTA), runs the
+//                           fp64 per-row epilogue (logp, ratio, clip, term, token scale)
+//                           and hands (lse2, s, g_y = s (p_y - 1), y) to the consumers' pass 2.
 //
-// Consumption order equals load order, so the ring is strictly FIFO: load k waits for
-// the release of load k - NS (parity (k / NS) & 1).  R = NS - PF keeps PF slots free at
-// the end of pass 1 so the re-loads (from L2: the row was read moments ago) are in flight
-// while the CTA reduces; the next row's pass-1 loads fill the slots pass 2 releases.
+// The epilogue and the block combine thus run while the consumers stream the next row's
+// first chunks: no per-row barrier among the consumers and no serial section on their
+// path (the per-row reduce -> epilogue -> barrier chain took ~3 % of the step in the
+// previous single-role design).  Consumption order equals load order,
+// so the ring is strictly FIFO: load j waits for the release of load j - NS.  The R
+// resident chunks of row k are its last ones, consumed first in its pass 2; LA <= NS - R
+// and LA <= n - R keep every slot a load waits for released before the consumer needs it.
 #include <cstdio>
 
 #include "common.cuh"
@@ -36,17 +45,20 @@ struct Params {
     int64_t n_rows;
     const RowInfo *rowinfo;
     float eps_lo, eps_hi, grad_scale;
-    float *logp_out, *lse_out, *scale_out, *term_ws, *logp_ws;
+    float *logp_out, *lse_out, *scale_out;
+    double *term_ws;
+    float *logp_ws;
     uint8_t *flag_ws;
     int32_t ns;  // ring slots
     int32_t pf;  // slots kept free at the end of pass 1
+    int32_t la;  // look-ahead chunks of the next row before a row's pass 2
 };
 
 struct Geometry {
     int n_vec;       // 8-element vectors per row (ceil(V / 8))
     int n;           // chunks per row
     int R;           // chunks resident after pass 1 (re-consumed without a load)
-    int loads;       // loads per row: n + (n - R)
+    int LA;          // look-ahead chunks (first chunks of the next row before pass 2)
     int tail_valid;  // valid elements of the last vector
 };
 
@@ -56,19 +68,20 @@ __device__ __forceinline__ Geometry geometry(const Params &p, int V, bool two_pa
     g.n_vec = (V + 7) / 8;
     g.n = (g.n_vec + CHUNK_VECS - 1) / CHUNK_VECS;
     g.R = two_pass ? min(g.n, max(0, p.ns - p.pf)) : 0;
-    g.loads = two_pass ? 2 * g.n - g.R : g.n;
+    g.LA = two_pass ? max(0, min(p.la, min(p.ns - g.R, g.n - g.R))) : 0;
     g.tail_valid = V - (g.n_vec - 1) * 8;
     return g;
 }
 
 // SPLIT = 2: a cluster of two CTAs (two SMs) shares each row, CTA r streaming vectors
-// [r*h, ...) of it (h = ceil(ceil(V/8)/2)); after pass 1 the two (max, sum) partials cross
-// through distributed shared memory (st.async onto the partner's mbarrier, one buffer per
-// row parity) and both CTAs merge them in rank order, so they hold identical row scalars.
-// Halving the row halves the time between a chunk's pass-1 load and its pass-2 re-load, so
-// at V = 262144 (512 KB rows) the re-loads stay in L2.
+// [r*h, ...) of it (h = ceil(ceil(V/8)/2)); the epilogue warps of the two CTAs exchange
+// their (max, sum) partials through distributed shared memory (st.async onto the
+// partner's mbarrier, one buffer per row parity) and merge them in rank order, so both
+// hold identical row scalars.  Halving the row halves the time between a chunk's pass-1
+// load and its pass-2 re-load, so at V = 262144 (512 KB rows) the re-loads stay in L2;
+// the pair's wait for each other sits in the epilogue warps, off the consumers' path.
 template <int NT, int MINB, int CHUNK_VECS, int SPLIT>
-__global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
+__global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
     constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr int U = CHUNK_VECS / NT;  // vectors per consumer thread per chunk
     constexpr int NW = NT / 32;
@@ -76,9 +89,11 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
     uint4 *ring = reinterpret_cast<uint4 *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.ns * CHUNK_BYTES);
     uint64_t *empty = full + p.ns;
-    __shared__ float2 red[NW];
-    __shared__ float row_scalars[4];
-    __shared__ float2 xbuf[2];
+    __shared__ RowPart red[2][NW];                 // warp partials, by row parity
+    __shared__ float4 scal[2];                     // (lse2, s, g_y, y) for pass 2, by row parity
+    __shared__ __align__(8) uint64_t part_bar[2];  // NW warp arrivals: red[b] complete
+    __shared__ __align__(8) uint64_t scal_bar[2];  // 1 arrival: scal[b] written
+    __shared__ RowPart xbuf[2];
     __shared__ __align__(8) uint64_t xbar[2];
     const bool two_pass = p.dlogits != nullptr;
     const uint32_t crank = SPLIT == 2 ? cluster_ctarank() : 0u;
@@ -93,8 +108,11 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, NW);
         }
-        mbar_init(xbar, 1);
-        mbar_init(xbar + 1, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(part_bar + b, NW);
+            mbar_init(scal_bar + b, 1);
+            mbar_init(xbar + b, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (SPLIT == 2) cluster_sync_all();  // the partner's barriers exist before any st.async
@@ -109,99 +127,66 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
             const int64_t row_bytes = (int64_t)g.n_vec * 16;
             int slot = 0;
             uint32_t par = 0;  // parity of the slot's current use
-            for (int64_t row = row0; row < p.n_rows; row += rstep) {
+            auto load = [&](int64_t row, int c, bool reload) {
                 const uint8_t *src = reinterpret_cast<const uint8_t *>(p.logits + row * p.ld + col0);
-                for (int i = 0; i < g.loads; ++i) {
-                    const int c = i < g.n ? i : i - g.n;  // chunk (pass-1 load or re-load)
-                    mbar_wait(empty + slot, par ^ 1u);
-                    const int64_t off = (int64_t)c * CHUNK_BYTES;
-                    const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
-                    // chunks read again from L2 in pass 2 stay; the rest streams through
-                    const uint64_t pol = (i < g.n && c < g.n - g.R && two_pass) ? pol_keep : pol_once;
-                    mbar_arrive_expect_tx(full + slot, bytes);
-                    bulk_g2s(ring + (size_t)slot * CHUNK_VECS, src + off, bytes, full + slot, pol);
-                    if (++slot == p.ns) {
-                        slot = 0;
-                        par ^= 1u;
-                    }
+                mbar_wait(empty + slot, par ^ 1u);
+                const int64_t off = (int64_t)c * CHUNK_BYTES;
+                const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
+                // chunks read again from L2 in pass 2 stay; the rest streams through
+                const uint64_t pol = (!reload && c < g.n - g.R && two_pass) ? pol_keep : pol_once;
+                mbar_arrive_expect_tx(full + slot, bytes);
+                bulk_g2s(ring + (size_t)slot * CHUNK_VECS, src + off, bytes, full + slot, pol);
+                if (++slot == p.ns) {
+                    slot = 0;
+                    par ^= 1u;
                 }
+            };
+            for (int64_t row = row0; row < p.n_rows; row += rstep) {
+                for (int c = (row == row0 ? 0 : g.LA); c < g.n; ++c) load(row, c, false);
+                if (row + rstep < p.n_rows)
+                    for (int c = 0; c < g.LA; ++c) load(row + rstep, c, false);
+                if (two_pass)
+                    for (int c = 0; c < g.n - g.R; ++c) load(row, c, true);
             }
         }
         return;
     }
 
-    // ---------------------------------------------------------------- consumers
-    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
-    int slot = 0;      // slot of the next load this CTA consumes
-    uint32_t par = 0;  // and the parity of that slot's use
-    uint32_t rowk = 0;  // rows this CTA has done (exchange buffer rowk & 1, parity rowk >> 1)
-    for (int64_t row = row0; row < p.n_rows; row += rstep, ++rowk) {
-        const int base_slot = slot;  // slot of this row's pass-1 chunk 0
-        // the epilogue's two dependent global reads (row info, then z_y), issued now so
-        // that they complete under pass 1 instead of stalling the whole CTA at its end
-        RowInfo ri;
-        uint16_t zy_bits = 0;
-        if (threadIdx.x == 0) {
-            ri = p.rowinfo[row];
-            if (ri.target >= 0 && ri.target < p.V) zy_bits = p.logits[row * p.ld + ri.target];
-        }
-        // ---- pass 1: log2-domain running (max, sum) per thread
-        float a = -INFINITY, s = 0.0f;
-        // the full chunks 0..n-2 run without masking (no register merges in the hot loop),
-        // the ragged last chunk after them
-        auto pass1_chunk = [&](int c, bool last) {
-            const int sl = slot;
-            mbar_wait(full + sl, par);
-            if (++slot == p.ns) {
-                slot = 0;
-                par ^= 1u;
-            }
-            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
-            uint4 x[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
-            if (last) {
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
-                    if (vi >= g.n_vec) x[j] = neg_inf;
-                    else if (vi == g.n_vec - 1 && g.tail_valid < 8) x[j] = mask_tail(x[j], g.tail_valid);
-                }
-            }
-            RowwiseBatch<NT, U>::reduce(x, a, s);  // lazy exponent reference (rowwise.cuh)
-            if (c < g.n - g.R) {  // not resident: release now
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty + sl);
-            }
-        };
-#pragma unroll 1
-        for (int c = 0; c < g.n - 1; ++c) pass1_chunk(c, false);
-        pass1_chunk(g.n - 1, true);
-        // ---- block reduction and the per-row epilogue
-        warp_lse2_combine(a, s);
-        if (lane == 0) red[warp] = make_float2(a, s);
-        named_bar_sync(1, NT);
-        if (warp == 0) {
-            float cm = lane < NW ? red[lane].x : -INFINITY, cs = lane < NW ? red[lane].y : 0.0f;
-            warp_lse2_combine(cm, cs);
-            if (SPLIT == 2 && lane == 0) {
-                const int b = rowk & 1;
-                mbar_arrive_expect_tx(xbar + b, 8);
-                st_async_v2(mapa_shared(smem_u32(xbuf + b), crank ^ 1u),
-                            mapa_shared(smem_u32(xbar + b), crank ^ 1u), cm, cs);
-                mbar_wait_cluster(xbar + b, (rowk >> 1) & 1u);
-                const float2 o = xbuf[b];
-                // rank order on both CTAs: bit-identical row scalars
-                float m0 = crank == 0 ? cm : o.x, s0 = crank == 0 ? cs : o.y;
-                lse2_merge(m0, s0, crank == 0 ? o.x : cm, crank == 0 ? o.y : cs);
-                cm = m0;
-                cs = s0;
-            }
+    if (warp == NW + 1) {
+        // ------------------------------------------------------------ epilogue warp
+        uint32_t rowk = 0;
+        for (int64_t row = row0; row < p.n_rows; row += rstep, ++rowk) {
+            const int b = rowk & 1;
+            const uint32_t ph = (rowk >> 1) & 1u;
+            // the epilogue's dependent global reads, issued before the wait
+            RowInfo ri;
+            uint16_t zy_bits = 0;
             if (lane == 0) {
+                ri = p.rowinfo[row];
+                if (ri.target >= 0 && ri.target < p.V) zy_bits = p.logits[row * p.ld + ri.target];
+            }
+            mbar_wait(part_bar + b, ph);
+            float cm = lane < NW ? red[b][lane].a : -INFINITY;
+            double cs = lane < NW ? red[b][lane].s : 0.0;
+            warp_lse2_combine(cm, cs);
+            if (lane == 0) {
+                if (SPLIT == 2) {
+                    mbar_arrive_expect_tx(xbar + b, 16);
+                    st_async_part(mapa_shared(smem_u32(xbuf + b), crank ^ 1u),
+                                  mapa_shared(smem_u32(xbar + b), crank ^ 1u), cm, cs);
+                    mbar_wait_cluster(xbar + b, ph);
+                    const RowPart o = xbuf[b];
+                    // rank order on both CTAs: bit-identical row scalars
+                    float m0 = crank == 0 ? cm : o.a;
+                    double s0 = crank == 0 ? cs : o.s;
+                    lse2_merge(m0, s0, crank == 0 ? o.a : cm, crank == 0 ? o.s : cs);
+                    cm = m0;
+                    cs = s0;
+                }
                 const bool y_valid = ri.target >= 0 && ri.target < p.V;
                 const float zy = y_valid ? __uint_as_float(((uint32_t)zy_bits) << 16) : __int_as_float(0x7FC00000);
-                const float l2s = log2f(cs);
-                const float lse2 = cm + l2s;
+                const double l2s = row_l2s(cs, cm);
+                const float lse2 = cm + (float)l2s;
                 const double logp_d = row_logp(zy, cm, l2s);
                 const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                 const float logp = (float)logp_d;
@@ -213,18 +198,76 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
                     p.logp_ws[row] = logp;
                     p.flag_ws[row] = o.flags;
                 }
-                row_scalars[0] = lse2;
-                row_scalars[1] = o.s;
-                row_scalars[2] = zy;
-                row_scalars[3] = __int_as_float(y_valid ? ri.target : -1);
+                scal[b] = make_float4(lse2, o.s, o.gy, __int_as_float(y_valid ? ri.target : -1));
+                mbar_arrive(scal_bar + b);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
+    int slot = 0;      // slot of the next load this CTA consumes
+    uint32_t par = 0;  // and the parity of that slot's use
+    // one pass-1 chunk c of a row into (a, s); `last` = the ragged last chunk
+    auto pass1_chunk = [&](int c, bool last, float &a, double &s) {
+        const int sl = slot;
+        mbar_wait(full + sl, par);
+        if (++slot == p.ns) {
+            slot = 0;
+            par ^= 1u;
+        }
+        const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+        uint4 x[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+        if (last) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
+                if (vi >= g.n_vec) x[j] = neg_inf;
+                else if (vi == g.n_vec - 1 && g.tail_valid < 8) x[j] = mask_tail(x[j], g.tail_valid);
             }
         }
-        named_bar_sync(1, NT);
+        RowwiseBatch<NT, U>::reduce(x, a, s);  // running max reference, fp64 sum (rowwise.cuh)
+        if (c < g.n - g.R) {  // not resident: release now
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + sl);
+        }
+    };
+    float a = -INFINITY;  // the current row's partial (its first LA chunks come from the look-ahead)
+    double s = 0.0;
+    if (row0 < p.n_rows)
+        for (int c = 0; c < g.LA; ++c) pass1_chunk(c, c == g.n - 1, a, s);
+    uint32_t rowk = 0;
+    for (int64_t row = row0; row < p.n_rows; row += rstep, ++rowk) {
+        const int b = rowk & 1;
+        // ---- pass 1 (rest): the full chunks without masking, the ragged last one after them
+        int res_base = slot;  // slot of this row's chunk LA: chunks LA..n-1 are contiguous loads
+#pragma unroll 1
+        for (int c = g.LA; c < g.n - 1; ++c) pass1_chunk(c, false, a, s);
+        if (g.n - 1 >= g.LA) pass1_chunk(g.n - 1, true, a, s);
+        // ---- publish the warp's partial; before reusing red[b], the epilogue of row k-2
+        // (same buffer) must have read it -- in two-pass mode pass 2 of row k-2 waited for it
+        warp_lse2_combine(a, s);
+        if (!two_pass && rowk >= 2) mbar_wait(scal_bar + b, ((rowk - 2) >> 1) & 1u);
+        if (lane == 0) {
+            red[b][warp] = RowPart{a, 0.0f, s};
+            mbar_arrive(part_bar + b);
+        }
+        // ---- look-ahead: the next row's first chunks while the epilogue warp finishes this row
+        a = -INFINITY;
+        s = 0.0;
+        if (row + rstep < p.n_rows)
+            for (int c = 0; c < g.LA; ++c) pass1_chunk(c, c == g.n - 1, a, s);
         if (!two_pass) continue;
-        // ---- pass 2: resident chunks n-R..n-1 (loads base+n-R..), then the re-loads
-        const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
-            const auto gref = RowwiseBatch<NT, U>::grad_ref(sc, lse2);
-        const int32_t yfull = __float_as_int(row_scalars[3]);
+        // ---- pass 2: resident chunks n-R..n-1 (loads res_base + (c - LA)), then the re-loads
+        mbar_wait(scal_bar + b, (rowk >> 1) & 1u);
+        const float4 sc4 = scal[b];
+        const float lse2 = sc4.x, sc = sc4.y, gy = sc4.z;
+        const auto gref = RowwiseBatch<NT, U>::grad_ref(sc, lse2);
+        const int32_t yfull = __float_as_int(sc4.w);
         const int32_t y = (yfull >= col0 && yfull < col0 + Vloc) ? yfull - col0 : -1;  // in this slice
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
         uint16_t *drow = p.dlogits + row * p.ld + col0;
@@ -234,7 +277,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
             const int c = resident ? g.n - g.R + i : i - g.R;
             int sl;
             if (resident) {
-                sl = (base_slot + c) % p.ns;  // the pass-1 load of chunk c, still in its slot
+                sl = (res_base + (c - g.LA)) % p.ns;  // the pass-1 load of chunk c, still in its slot
             } else {
                 sl = slot;
                 mbar_wait(full + sl, par);
@@ -268,10 +311,9 @@ __global__ void __launch_bounds__(NT + 32, MINB) stream_kernel(const Params p) {
                     else stg_stream(dst4 + vi, d);
                 }
             }
-            // the target's own column, rewritten by the thread that stored its vector
+            // the target's own column (g_y from the fp64 epilogue), rewritten by the thread that stored its vector
             if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
-                const float py = ex2(fmaf(zy, kLog2e, -lse2));
-                drow[y] = f2bf(sc * (py - 1.0f));
+                drow[y] = f2bf(gy);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + sl);
@@ -303,6 +345,8 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
     p.flag_ws = a.flag_ws;
     p.ns = (tune && tune->stages > 0) ? tune->stages : 0;
     p.pf = (tune && tune->lag > 0) ? tune->lag : 3;
+    // look-ahead chunks of the next row before a row's pass 2 (tune->prefetch; 0 = 2)
+    p.la = (tune && tune->prefetch > 0) ? tune->prefetch : 2;
     // consumer threads (ctas_per_sm 256 / 512), CTAs per SM (row_cache 1 / 2), slot size
     const int nt = (tune && tune->ctas_per_sm == 256) ? 256 : 512;
     const int cps = (tune && tune->row_cache == 2) ? 2 : 1;
@@ -337,7 +381,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
         at[0].val.clusterDim.x = 2;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
-        cfg.blockDim = dim3(512 + 32);
+        cfg.blockDim = dim3(512 + 64);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cfg.attrs = at;
@@ -360,7 +404,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
         e = cudaFuncSetAttribute(stream_kernel<NT_, MB_, CV_, 1>,                                         \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
         if (e != cudaSuccess) return e;                                                                \
-        stream_kernel<NT_, MB_, CV_, 1><<<grid, NT_ + 32, smem, s>>>(p);                                  \
+        stream_kernel<NT_, MB_, CV_, 1><<<grid, NT_ + 64, smem, s>>>(p);                                  \
     } while (0)
     if (ckb == 64) {
         GRPO_K3C(512, 1, 4096);

@@ -40,7 +40,9 @@ struct VpParams {
     int64_t n_rows;
     const RowInfo *rowinfo;
     float eps_lo, eps_hi, grad_scale;
-    float *logp_out, *lse_out, *scale_out, *term_ws, *logp_ws;
+    float *logp_out, *lse_out, *scale_out;
+    double *term_ws;
+    float *logp_ws;
     uint8_t *flag_ws;
     int32_t cache_vecs;
 };
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
     using B = RowwiseBatch<NT, U>;
     constexpr int NW = NT / 32;
     constexpr int BV = NT * U;
-    __shared__ float2 red[NW];
+    __shared__ RowPart red[NW];
     __shared__ float row_scalars[4];
     extern __shared__ uint4 row_cache[];
     const int g_per = gridDim.x / p.n_local;
@@ -91,7 +93,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
     // pass 1 of `row` into `cache`, then warp 0 posts the row's partial to every rank
     auto pass1 = [&](int64_t row, uint4 *cache) {
         const uint16_t *zrow = shard + row * p.ld;
-        float a = -INFINITY, s = 0.0f;
+        float a = -INFINITY;
+        double s = 0.0;
         for (int bi = 0; bi < n_full; ++bi) {
             const uint4 *src = reinterpret_cast<const uint4 *>(zrow) + bi * BV + threadIdx.x;
             uint4 x[U];
@@ -119,13 +122,14 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
             B::reduce(x, a, s);
         }
         warp_lse2_combine(a, s);
-        if (lane == 0) red[warp] = make_float2(a, s);
+        if (lane == 0) red[warp] = RowPart{a, 0.0f, s};
         __syncthreads();
         if (warp == 0) {
-            float cm = -INFINITY, cs = 0.0f;
+            float cm = -INFINITY;
+            double cs = 0.0;
             if (lane < NW) {
-                cm = red[lane].x;
-                cs = red[lane].y;
+                cm = red[lane].a;
+                cs = red[lane].s;
             }
             warp_lse2_combine(cm, cs);
             const int32_t y = p.rowinfo[row].target;
@@ -139,8 +143,9 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
             if (lane < p.world) {
                 const uint64_t hi = (uint64_t)p.tag << 32;
                 ulonglong2 *dst = p.xbuf[lane] + ((p.half + row) * p.world + rank) * 2;
-                st_relaxed_sys_v2(dst, hi | __float_as_uint(cm), hi | __float_as_uint(cs));
-                st_relaxed_sys_v2(dst + 1, hi | __float_as_uint(zy), hi | (mine ? 1u : 0u));
+                const uint64_t sb = (uint64_t)__double_as_longlong(cs) | (mine ? (1ull << 63) : 0ull);
+                st_relaxed_sys_v2(dst, hi | __float_as_uint(cm), hi | (uint32_t)sb);
+                st_relaxed_sys_v2(dst + 1, hi | (uint32_t)(sb >> 32), hi | __float_as_uint(zy));
             }
         }
     };
@@ -149,7 +154,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
     auto finish = [&](int64_t row, const uint4 *cache) {
         const uint16_t *zrow = shard + row * p.ld;
         if (warp == 0) {
-            float M = -INFINITY, S = 0.0f, zsrc = 0.0f;
+            float M = -INFINITY, zsrc = 0.0f;
+            double S = 0.0;
             bool own = false;
             if (lane < p.world) {
                 const ulonglong2 *src = p.xbuf[rank] + ((p.half + row) * p.world + lane) * 2;
@@ -164,10 +170,12 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
                     __nanosleep(32);
                     if (++spins > (1ll << 27)) __trap();  // a peer never arrived: fail, don't hang
                 }
+                // (a, s fp64 with the holds-y bit in its sign, z_y)
+                const uint64_t sb = ((w1.x & 0xFFFFFFFFull) << 32) | (w0.y & 0xFFFFFFFFull);
                 M = __uint_as_float((uint32_t)w0.x);
-                S = __uint_as_float((uint32_t)w0.y);
-                zsrc = __uint_as_float((uint32_t)w1.x);
-                own = (uint32_t)w1.y != 0u;
+                S = __longlong_as_double((long long)(sb & ~(1ull << 63)));
+                own = (sb >> 63) != 0ull;
+                zsrc = __uint_as_float((uint32_t)w1.y);
             }
             warp_lse2_combine(M, S);  // same inputs in the same lanes on every rank
             const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
@@ -178,8 +186,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
                 const bool mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
                 const bool y_valid = own_mask != 0u;
                 const float zyv = y_valid ? zsh : __int_as_float(0x7FC00000);
-                const float l2s = log2f(S);
-                const float lse2 = M + l2s;
+                const double l2s = row_l2s(S, M);
+                const float lse2 = M + (float)l2s;
                 const double logp_d = row_logp(zyv, M, l2s);
                 const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                 if (lr == 0) {  // per-row outputs: identical on every rank, written once per call
@@ -193,14 +201,14 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
                 }
                 row_scalars[0] = lse2;
                 row_scalars[1] = o.s;
-                row_scalars[2] = zyv;
+                row_scalars[2] = o.gy;
                 row_scalars[3] = __int_as_float(mine ? y_loc : -1);
             }
         }
         __syncthreads();
         // ---- pass 2: dlogits of the local shard
         if (dshard) {
-            const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
+            const float lse2 = row_scalars[0], sc = row_scalars[1], gy = row_scalars[2];
             const auto gref = B::grad_ref(sc, lse2);
             const int32_t y_loc = __float_as_int(row_scalars[3]);
             const int yv = y_loc >= 0 ? (y_loc >> 3) : -1;
@@ -243,8 +251,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
                     }
                 }
                 if (yv >= 0 && (yv % NT) == (int)threadIdx.x) {
-                    const float py = ex2(fmaf(zy, kLog2e, -lse2));
-                    drow[y_loc] = f2bf(sc * (py - 1.0f));
+                    drow[y_loc] = f2bf(gy);
                 }
             }
         }
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
     uint4 *ring = reinterpret_cast<uint4 *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)ns * CHUNK_BYTES);
     uint64_t *empty = full + ns;
-    __shared__ float2 red[NW];
+    __shared__ RowPart red[NW];
     __shared__ float row_scalars[4];
     const int g_per = gridDim.x / p.n_local;
     const int lr = blockIdx.x / g_per;  // local rank of this CTA
@@ -375,7 +382,8 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
             if (mine) zy_bits = shard[row * p.ld + y_loc];
         }
         // ---- pass 1 over the local shard (full chunks, then the ragged last one)
-        float a = -INFINITY, s = 0.0f;
+        float a = -INFINITY;
+        double s = 0.0;
         auto pass1_chunk = [&](int c, bool last) {
             const int sl = slot;
             mbar_wait(full + sl, par);
@@ -405,10 +413,11 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
         for (int c = 0; c < n - 1; ++c) pass1_chunk(c, false);
         if (n > 0) pass1_chunk(n - 1, true);
         warp_lse2_combine(a, s);
-        if (lane == 0) red[warp] = make_float2(a, s);
+        if (lane == 0) red[warp] = RowPart{a, 0.0f, s};
         named_bar_sync(1, NT);
         if (warp == 0) {
-            float cm = lane < NW ? red[lane].x : -INFINITY, cs = lane < NW ? red[lane].y : 0.0f;
+            float cm = lane < NW ? red[lane].a : -INFINITY;
+            double cs = lane < NW ? red[lane].s : 0.0;
             warp_lse2_combine(cm, cs);
             const bool own_y = __shfl_sync(0xFFFFFFFFu, mine, 0);
             const float zy = own_y ? __uint_as_float(((uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)zy_bits, 0)) << 16)
@@ -417,10 +426,12 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
             if (lane < p.world) {
                 const uint64_t hi = (uint64_t)p.tag << 32;
                 ulonglong2 *dst = p.xbuf[lane] + ((p.half + row) * p.world + rank) * 2;
-                st_relaxed_sys_v2(dst, hi | __float_as_uint(cm), hi | __float_as_uint(cs));
-                st_relaxed_sys_v2(dst + 1, hi | __float_as_uint(zy), hi | (own_y ? 1u : 0u));
+                const uint64_t sb = (uint64_t)__double_as_longlong(cs) | (own_y ? (1ull << 63) : 0ull);
+                st_relaxed_sys_v2(dst, hi | __float_as_uint(cm), hi | (uint32_t)sb);
+                st_relaxed_sys_v2(dst + 1, hi | (uint32_t)(sb >> 32), hi | __float_as_uint(zy));
             }
-            float M = -INFINITY, S = 0.0f, zsrc = 0.0f;
+            float M = -INFINITY, zsrc = 0.0f;
+            double S = 0.0;
             bool own = false;
             if (lane < p.world) {
                 const ulonglong2 *src = p.xbuf[rank] + ((p.half + row) * p.world + lane) * 2;
@@ -435,18 +446,20 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
                     __nanosleep(32);
                     if (++spins > (1ll << 27)) __trap();  // a peer never arrived: fail, don't hang
                 }
+                // (a, s fp64 with the holds-y bit in its sign, z_y)
+                const uint64_t sb = ((w1.x & 0xFFFFFFFFull) << 32) | (w0.y & 0xFFFFFFFFull);
                 M = __uint_as_float((uint32_t)w0.x);
-                S = __uint_as_float((uint32_t)w0.y);
-                zsrc = __uint_as_float((uint32_t)w1.x);
-                own = (uint32_t)w1.y != 0u;
+                S = __longlong_as_double((long long)(sb & ~(1ull << 63)));
+                own = (sb >> 63) != 0ull;
+                zsrc = __uint_as_float((uint32_t)w1.y);
             }
             warp_lse2_combine(M, S);  // same inputs in the same lanes on every rank
             const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
             const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
             if (lane == 0) {
                 const float zyv = own_mask != 0u ? zsh : __int_as_float(0x7FC00000);
-                const float l2s = log2f(S);
-                const float lse2 = M + l2s;
+                const double l2s = row_l2s(S, M);
+                const float lse2 = M + (float)l2s;
                 const double logp_d = row_logp(zyv, M, l2s);
                 const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
                 if (lr == 0) {  // per-row outputs: identical on every rank, written once per call
@@ -460,14 +473,14 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
                 }
                 row_scalars[0] = lse2;
                 row_scalars[1] = o.s;
-                row_scalars[2] = zyv;
+                row_scalars[2] = o.gy;
                 row_scalars[3] = __int_as_float(mine ? y_loc : -1);
             }
         }
         named_bar_sync(1, NT);
         if (!two_pass) continue;
         // ---- pass 2: resident chunks n-R..n-1, then the re-loads
-        const float lse2 = row_scalars[0], sc = row_scalars[1], zy = row_scalars[2];
+        const float lse2 = row_scalars[0], sc = row_scalars[1], gy = row_scalars[2];
         const auto gref = B::grad_ref(sc, lse2);
         const int32_t y = __float_as_int(row_scalars[3]);
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
@@ -512,8 +525,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
                 }
             }
             if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
-                const float py = ex2(fmaf(zy, kLog2e, -lse2));
-                drow[y] = f2bf(sc * (py - 1.0f));
+                drow[y] = f2bf(gy);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + sl);

@@ -18,33 +18,26 @@ struct RowwiseBatch {
     static __device__ __forceinline__ float sum_exp2(const uint4 (&x)[U], float ref) {
         return x2::sum_exp2<U, 0>(x, ref);
     }
-    // log2-domain partial of U vectors (already loaded and masked) into (a, s), with a lazy
-    // reference: a is set by the first batch holding a finite element (its max, rounded up,
-    // so every exponent of that batch is <= 0) and raised only when the partial sum passes
-    // 2^64, i.e. when a later element lies more than ~2^64 / (terms so far) above it; the
-    // common batch then costs no max reduction and no rescale.  Terms that fall below
-    // 2^-126 of the reference underflow exactly as they would against the running max
-    // (they are < 2^-126 of the max element, which a contributes at 2^0).  Any value of
-    // the row lands in a <= 2^64 sum, so the per-thread partials combine without overflow.
-    static __device__ __forceinline__ void reduce(const uint4 (&x)[U], float &a, float &s) {
-        if (a != -INFINITY) {
-            const float t = s + sum_exp2(x, a);
-            if (t <= 1.8446744e19f) {  // 2^64; false for inf and NaN
-                s = t;
-                return;
-            }
-        }
+    // log2-domain partial of U vectors (already loaded and masked) into (a, s): a is the
+    // running max of the thread's elements (bf16 max of the batch, 16 HMNMX2 per 32
+    // elements), rounded up into log2 units, so every exponent is <= 0 and the terms that
+    // dominate the row's sum have exponents near 0, where fp32 rounds them finely.  (A
+    // lazy reference -- the first batch's max, raised only on overflow -- saved the max
+    // reduction but left the row's top elements exponents of +10..+20 against a thread's
+    // first-batch max on LM-like rows, whose fp32 rounding cost logp 3e-7.)
+    // The running sum s is fp64: each 32-element batch sum (fp32) is added with one DADD.
+    static __device__ __forceinline__ void reduce(const uint4 (&x)[U], float &a, double &s) {
         uint32_t mx2 = kBf16NegInfPair;
 #pragma unroll
         for (int j = 0; j < U; ++j)
             mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
         const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
         if (va > a) {
-            s = (a == -INFINITY) ? 0.0f : s * ex2(a - va);
+            s = (a == -INFINITY) ? 0.0 : s * (double)ex2(a - va);
             a = va;
         }
         // with a = -inf every element so far is -inf: reference 0 keeps the terms 0
-        s += sum_exp2(x, a == -INFINITY ? 0.0f : a);
+        s += (double)sum_exp2(x, a == -INFINITY ? 0.0f : a);
     }
     // s * 2^(z*log2e - lse2) = sign(s) * 2^(z*log2e - (lse2 - log2|s|)): the token scale
     // folds into the exponent's reference, so an element costs one FFMA and one EX2 (no

@@ -8,9 +8,11 @@ the device; behaviour log-probs = the model's own logp minus N(0, (0.03 (1+gap))
 
 Timed with CUDA events on the launching stream after warm-up (max of nothing: one GPU):
   fwd   grpo_async_lmhead_fwd   (tcgen05 GEMM + loss epilogue; logits never stored)
-  bwd   grpo_async_lmhead_bwd   (tcgen05 GEMM recompute + dz epilogue; cuBLAS dX, dW)
-  unfused reference on the same data: cuBLAS logits GEMM -> grpo_async_loss_fwd (row-wise
-  kernel, dlogits) -> cuBLAS dX, dW.
+  bwd   grpo_async_lmhead_bwd   (tcgen05 GEMM recompute + dz epilogue; tcgen05 dX, dW GEMMs)
+  the GEMMs alone: grpo_async_lmhead_dx (dX = dz W) and grpo_async_lmhead_dw (dW += dz^T X)
+  unfused on the same data, every kernel ours: grpo_async_lmhead_logits (tcgen05, bf16
+  logits) -> grpo_async_loss_fwd (dlogits) -> grpo_async_lmhead_dx -> grpo_async_lmhead_dw;
+  and the same with torch.matmul (cuBLAS) GEMMs, as a library baseline.
 Prints one JSON line.
 """
 import argparse
@@ -113,24 +115,39 @@ def main():
            "bwd_tflops": 3 * fl / ms_bwd / 1e9, "plan_fwd": plan_fwd,
            "J": float(st[G.STAT_J].item()),
            "clipped_frac": float(st[G.STAT_CLIPPED].item()) / R}
-    # the dz kernel alone (bwd without the cuBLAS GEMMs)
+    # the dz kernel alone (bwd without the dX / dW GEMMs), then each GEMM alone on that dz
     out["ms_dz_kernel"] = timed(lambda: loss.lmhead_bwd(X, W, R, tgt, lse, scale, dz))
     out["dz_kernel_tflops"] = fl / out["ms_dz_kernel"] / 1e9
+    out["ms_dx_gemm"] = timed(lambda: L.grpo_async_lmhead_dx(dz, ld, W, R, d, V, dX))
+    out["dx_gemm_tflops"] = fl / out["ms_dx_gemm"] / 1e9
+    out["ms_dw_gemm"] = timed(lambda: L.grpo_async_lmhead_dw(X, R, d, V, dz, ld, dW))
+    out["dw_gemm_tflops"] = fl / out["ms_dw_gemm"] / 1e9
+    out["ms_fused_fwd_bwd"] = ms_fwd + ms_bwd
     if not args.skip_unfused:
         lg = torch.empty((R, ld), dtype=torch.bfloat16, device=dev)
         dl = torch.empty((R, ld), dtype=torch.bfloat16, device=dev)
+
+        def unfused_ours():
+            L.grpo_async_lmhead_logits(X, W, R, d, V, lg, ld)
+            ts.zero_()
+            st.zero_()
+            loss.loss_chunk(lg, 0, R, tgt, lw, db.cu_seqlens, adv, inv, ts, st, dlogits=dl, V=V)
+            L.grpo_async_lmhead_dx(dl, ld, W, R, d, V, dX)
+            L.grpo_async_lmhead_dw(X, R, d, V, dl, ld, dW)
+
+        out["ms_unfused_fwd_bwd"] = timed(unfused_ours)
+        out["ms_logits_gemm"] = timed(lambda: L.grpo_async_lmhead_logits(X, W, R, d, V, lg, ld))
         dWb = torch.empty((V, d), dtype=torch.bfloat16, device=dev)
 
-        def unfused():
+        def unfused_cublas():
             torch.matmul(X, W.t(), out=lg[:, :V]) if ld == V else lg[:, :V].copy_(X @ W.t())
             ts.zero_()
             st.zero_()
             loss.loss_chunk(lg, 0, R, tgt, lw, db.cu_seqlens, adv, inv, ts, st, dlogits=dl, V=V)
             torch.matmul(dl[:, :V], W, out=dX)
-            torch.matmul(dl[:, :V].t(), X, out=dWb)  # (cuBLAS; bf16 out, the same GEMM work)
+            torch.matmul(dl[:, :V].t(), X, out=dWb)  # (bf16 out, the same GEMM work)
 
-        out["ms_unfused_fwd_bwd"] = timed(unfused)
-        out["ms_fused_fwd_bwd"] = ms_fwd + ms_bwd
+        out["ms_unfused_fwd_bwd_torch_cublas"] = timed(unfused_cublas)
         del lg, dl
     out["tensor_peak_tflops"] = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
     print(json.dumps(out), flush=True)

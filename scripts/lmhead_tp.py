@@ -33,11 +33,13 @@ class FusedDX:
     def __init__(self, n, d, world, dev):
         import torch.distributed._symmetric_memory as symm
         self.rpr = -(-n // world)
-        self.buf = symm.empty(world * self.rpr * d, dtype=torch.float32, device=dev)
+        # two halves: call e writes half e % 2 (include/grpo_async.h, grpo_async_lmhead_tp_dx)
+        self.buf = symm.empty(2 * world * self.rpr * d, dtype=torch.float32, device=dev)
         self.h = symm.rendezvous(self.buf, dist.group.WORLD)
-        self.ptrs = [self.h.get_buffer(q, (world * self.rpr * d,), torch.float32).data_ptr()
+        self.ptrs = [self.h.get_buffer(q, (2 * world * self.rpr * d,), torch.float32).data_ptr()
                      for q in range(world)]
         self.flag = torch.zeros(1, device=dev)
+        self.epoch = 0
 
 
 def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False, fused=None):
@@ -65,7 +67,7 @@ def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False, fused=Non
         tm[0].record()
         loss.lmhead_tp_bwd(X, Wq, off, n, db.target_ids[R0:R0 + n], lse, scale, dz)
         tm[1].record()
-        L.grpo_async_lmhead_tp_dx(dz, dz.shape[1], Wq, n, d, Vq, world, rank, fused.ptrs)
+        L.grpo_async_lmhead_tp_dx(dz, dz.shape[1], Wq, n, d, Vq, world, rank, fused.ptrs, fused.epoch)
         tm[2].record()
         L.grpo_async_lmhead_dw(X, n, d, Vq, dz, dz.shape[1], dW)
         tm[3].record()
@@ -75,7 +77,8 @@ def run(loss, db, X, W, V, R0, n, rank, world, lw=None, overlap=False, fused=Non
         tm[4].record()
         rows = max(0, min(fused.rpr, n - rank * fused.rpr))
         mine = torch.empty((max(rows, 1), d), dtype=torch.float32, device=X.device)
-        L.grpo_async_lmhead_tp_dx_reduce(fused.buf, world, n, d, rank, mine)
+        L.grpo_async_lmhead_tp_dx_reduce(fused.buf, world, n, d, rank, mine, fused.epoch)
+        fused.epoch += 1
         tm[5].record()
         return logp, st, mine[:rows], dW, dz
     if overlap:  # the dhidden all-reduce overlaps the dW GEMM

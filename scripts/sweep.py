@@ -32,10 +32,7 @@ adv, inv = loss.advantage(db)
 ts = torch.zeros(b.N, dtype=torch.float64, device=dev)
 st = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
 plans = [json.loads(p) for p in args.plans.split(";")] if args.plans else [
-    {"kernel": 1}, {"kernel": 2},
-    {"kernel": 1, "cluster_size": 8}, {"kernel": 1, "cluster_size": 16, "ctas_per_sm": 1},
-    {"kernel": 1, "cluster_size": 8, "ctas_per_sm": 1}, {"kernel": 1, "cluster_size": 4, "ctas_per_sm": 1},
-    {"kernel": 1, "cluster_size": 16, "stages": 2}, {"kernel": 1, "cluster_size": 16, "ctas_per_sm": 3},
+    {}, {"kernel": 2}, {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 3},
 ]
 bytes_row = 4 * V + 25 if not args.fwd_only else 2 * V + 25
 def run_once(plan):

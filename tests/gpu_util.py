@@ -11,10 +11,9 @@ import paper_2604_26256_b200 as G
 from synth.gen import bf16_bits_to_f32
 
 EPS32 = float(np.float32(0.2))
-# DESIGN.md Z17: the relative loss criterion is taken against max(|J|, Z17_GUARD * S_abs).  The
-# fp32 per-token path carries |d logp| ~ 1e-6 (7e-7 observed at worst on the fuzz), i.e.
-# |dJ| <~ 1e-6 * S_abs whatever the cancellation in J; 1e-5 of 0.1 * S_abs is that floor.
-Z17_GUARD = 0.1
+# DESIGN.md Z17: the relative loss criterion is taken against
+# max(|J|, Z17_GUARD * S_abs), S_abs = sum_t inv_norm_i |term_t| the L1 mass of J's summands
+Z17_GUARD = 1e-2
 
 
 def to_dev_bits(bits: np.ndarray, device) -> torch.Tensor:
@@ -86,7 +85,7 @@ def near_boundary(r, eps=EPS32, tol=1e-5, eps_hi=None):
 
 
 def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5, dl_rel=1e-2,
-            logits_pad=None, eps_hi=None):
+            logits_pad=None, eps_hi=None, extra_J_tol=0.0):
     """Assert the north_star criteria; returns a dict of measured errors."""
     rr = ref["rows"]
     errs = {}
@@ -111,7 +110,11 @@ def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5,
     errs["J_ref"], errs["J_gpu"] = J_ref, J_gpu
     errs["J_rel_guarded"] = abs(J_gpu - J_ref) / max(abs(J_ref), Z17_GUARD * S_abs, 1e-300)
     errs["J_rel_raw"] = abs(J_gpu - J_ref) / max(abs(J_ref), 1e-300)
-    assert errs["J_rel_guarded"] <= loss_rtol, errs
+    if extra_J_tol:  # the LM head's logits error (Z25), propagated into J
+        errs["J_extra_tol"] = extra_J_tol
+        assert abs(J_gpu - J_ref) <= loss_rtol * max(abs(J_ref), Z17_GUARD * S_abs) + extra_J_tol, errs
+    else:
+        assert errs["J_rel_guarded"] <= loss_rtol, errs
     assert abs(gpu["stats"][G.STAT_ABS] - S_abs) <= 1e-5 * S_abs + 1e-300
     # per-trajectory sums of terms (fp64 reductions of fp32 terms)
     ts_scale = np.maximum(np.abs(ref["traj_sum"]), 1e-3 * batch.lengths)
@@ -140,6 +143,18 @@ def compare(gpu, ref, batch, check_dlogits=True, logp_atol=2e-3, loss_rtol=1e-5,
         assert (errs["dlogits_rel_l2"] <= dl_rel) if den > 0 else num == 0.0, errs
         zero_rows = (rr.s == 0.0) & ~nb
         assert np.all(got[zero_rows] == 0.0), "rows with s = 0 must be exactly zero"
+        # and row by row: every row with s != 0 within the same 1e-2 relative L2, so that a
+        # single wrong row cannot hide in the batch norm.  A row whose target is nearly certain
+        # (p_y -> 1) has an exact gradient s (p - onehot) of norm ~ |s| (1 - p_y), far below
+        # what p_y - 1 resolves in fp32 (|s| 2^-24 per entry); such rows are measured against
+        # the floor 2^-16 |s| (the per-row dlogits criterion).
+        live = (rr.s != 0.0) & ~nb
+        if live.any():
+            rn = np.linalg.norm(got[live] - ref_dl[live], axis=1)
+            rd = np.linalg.norm(ref_dl[live], axis=1)
+            row_rel = rn / np.maximum(rd, 2.0 ** -16 * np.abs(rr.s[live]))
+            errs["dlogits_row_rel_l2_max"] = float(np.max(row_rel))
+            assert np.all(row_rel <= dl_rel), (int(np.argmax(row_rel)), errs["dlogits_row_rel_l2_max"])
         # padding columns [V, ld) are never written
         raw = gpu["dlogits_raw"]
         if raw.shape[1] > batch.V:
@@ -208,6 +223,25 @@ def run_gpu_vp(batch, logits_bits, device, world, chunks=1, grad_scale=1.0, eps=
         out["dlogits"] = bf16_bits_to_f32(raw[:, :V]).astype(np.float64)
         out["shard_pad_untouched"] = bool(np.all(cat[:, V:] == 0x7FC3))
     return out
+
+
+def lmhead_accum_J_bound(batch, X_bits, W_bits, ref):
+    """DESIGN.md Z25: on the LM-head path the logits z = X W^T are fp32 tensor-core sums, one
+    accumulator rounding per tcgen05.mma K-step of 16 products, each within 1 ulp
+    (<= 2^-23 |acc|) -- so |dz_tv| <= ceil(d/16) 2^-23 sum_k |x_tk| |w_vk|, |d logp_t| <=
+    2 max_v |dz_tv|, and J (eq:grpo_async) moves by at most sum over unclipped tokens of
+    inv_norm |A| r |d logp_t|.  A bound from the inputs alone (no GPU value enters it)."""
+    X = np.abs(bf16_bits_to_f32(X_bits).astype(np.float64))
+    W = np.abs(bf16_bits_to_f32(W_bits).astype(np.float64))
+    d = X.shape[1]
+    zabs = np.zeros(X.shape[0])
+    for v0 in range(0, W.shape[0], 16384):
+        zabs = np.maximum(zabs, (X @ W[v0:v0 + 16384].T).max(axis=1))
+    B = 2.0 * -(-d // 16) * 2.0 ** -23 * zabs
+    rr = ref["rows"]
+    tok = np.repeat(np.arange(batch.N), batch.lengths)
+    live = ~rr.clipped
+    return float(np.sum((ref["inv_norm"][tok] * np.abs(ref["adv"][tok]) * rr.r * B)[live]))
 
 
 def lmhead_batch(name, seed, d, sigma=0.05):

@@ -175,14 +175,14 @@ def test_host_side_errors_tensor_parallel_and_sharded_entry_points():
                                         None, None, None) == L.GRPO_ERR_ALIGNMENT
     # fused dhidden: d % 128, rank >= world, NULL slot
     slots = (C.c_void_p * 2)(16, 32)
-    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 192, 1000, 2, 0, slots,
+    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 192, 1000, 2, 0, slots, 0,
                                        None) == L.GRPO_ERR_INVALID_ARG
-    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 256, 1000, 2, 2, slots,
+    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 256, 1000, 2, 2, slots, 0,
                                        None) == L.GRPO_ERR_INVALID_ARG
     bad = (C.c_void_p * 2)(16, None)
-    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 256, 1000, 2, 0, bad,
+    assert lib.grpo_async_lmhead_tp_dx(fake, 1000, fake, 10, 256, 1000, 2, 0, bad, 1,
                                        None) == L.GRPO_ERR_INVALID_ARG
-    assert lib.grpo_async_lmhead_tp_dx_reduce(fake, 9, 10, 256, 0, fake, 0, None) == L.GRPO_ERR_INVALID_ARG
+    assert lib.grpo_async_lmhead_tp_dx_reduce(fake, 9, 10, 256, 0, fake, 0, 0, None) == L.GRPO_ERR_INVALID_ARG
     # dW from dz: ld_dz not a multiple of 8
     assert lib.grpo_async_lmhead_dw(fake, 10, 128, 1000, fake, 1001, fake, None) == L.GRPO_ERR_ALIGNMENT
     # sharded rewards: P <= 0, std_floor <= 0

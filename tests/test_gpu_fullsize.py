@@ -13,7 +13,8 @@ from synth.gen import bf16_bits_to_f32, make_batch
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,R", [("prod", 131072), ("large", 32768), ("stale", 65536)])
+@pytest.mark.parametrize("name,R", [("prod", 131072), ("large", 32768), ("stale", 65536),
+                                    ("dapo", 131072)])
 def test_fullsize_chunk_sampled_rows(dev, name, R):
     b = make_batch(name, 0, period=R)
     V, ld = b.V, b.ld

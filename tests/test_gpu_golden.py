@@ -1,7 +1,9 @@
 """-m gpu: the whole benchmark step (bench.py's workload `prod`, seed 0, 131072-row
-resident chunk, default plan) against full-batch golden values written by
-scripts/make_golden_full.py from the fp64 oracle alone (every one of the
-1,008,179 rows through oracle_rows)."""
+resident chunk, default plan) and the other BASELINE.json configurations at full size --
+`dapo` (32 x 16, lengths to 20k), `stale` (K = 8, partial-rollout C1_MIXED trajectories)
+and `large` (V = 262144, rows split over two-SM clusters) -- against full-batch golden
+values written by scripts/make_golden_full.py from the fp64 oracle alone (every row of
+the batch through oracle_rows)."""
 import json
 import os
 
@@ -17,9 +19,11 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
-@pytest.mark.parametrize("name,seed,R", [("prod", 0, 131072)])
+@pytest.mark.parametrize("name,seed,R", [("prod", 0, 131072), ("dapo", 0, 131072), ("stale", 0, 65536),
+                                         ("large", 0, 65536)])
 def test_full_batch_against_oracle_golden(dev, name, seed, R):
-    gold = json.load(open(os.path.join(GOLD, f"{name}_seed{seed}_R{R}.json")))
+    path = os.path.join(GOLD, f"{name}_seed{seed}_R{R}.json")
+    gold = json.load(open(path))
     b = make_batch(name, seed, period=R)
     assert b.T == gold["T"] and b.N == gold["N"]
     lg = torch.empty((R, b.ld), dtype=torch.int16, device=dev)
@@ -37,7 +41,8 @@ def test_full_batch_against_oracle_golden(dev, name, seed, R):
                         db.cu_seqlens, adv, inv, traj_sum, stats, dlogits=dl[:n], V=b.V)
     torch.cuda.synchronize()
     st = stats.cpu().numpy()
-    assert vo.summary_dict()["valid"] == 1
+    # `stale` carries partial-rollout trajectories (C1 violations by design)
+    assert vo.summary_dict()["valid"] == (0 if b.token_version is not None else 1)
     assert st[G.STAT_ROWS] == gold["T"]
     # loss within 1e-5 under the guarded criterion (Z17)
     err = abs(st[G.STAT_J] - gold["J"]) / max(abs(gold["J"]), 1e-2 * gold["S_abs"])

@@ -2,10 +2,11 @@
 epilogue; backward: recomputed logits -> dz in the epilogue, then dX = dz W and
 dW += dz^T X) against the fp64 oracle (oracle.run_batch_lmhead).
 
-Tolerances: BASELINE north_star unchanged -- logp 2e-3 absolute, J 1e-5 relative (guarded,
-DESIGN.md Z17), dz / dX / dW 1e-2 relative L2.  The logits are fp32 tensor-core sums of d
-bf16 products rather than exact bf16 inputs; measured: logp <= 5.3e-6, J <= 5.2e-6
-relative at d <= 256."""
+Tolerances: BASELINE north_star -- logp 2e-3 absolute, J 1e-5 relative (guarded at
+1e-2 * S_abs, Z17), dz / dX / dW 1e-2 relative L2.  The logits are fp32 tensor-core
+sums of d bf16 products rather than exact bf16 inputs, so J may also move by the propagated
+a-priori bound of that accumulation (Z25, tests/gpu_util.lmhead_accum_J_bound,
+computed from X and W alone); measured logp errors are 3-6e-6."""
 import numpy as np
 import pytest
 import torch
@@ -14,7 +15,7 @@ import oracle.oracle as O
 import paper_2604_26256_b200 as G
 from synth.gen import make_batch
 from paper_2604_26256_b200 import _lib as L
-from tests.gpu_util import compare, lmhead_batch, run_gpu_lmhead, to_dev_bits
+from tests.gpu_util import compare, lmhead_accum_J_bound, lmhead_batch, run_gpu_lmhead, to_dev_bits
 
 pytestmark = pytest.mark.gpu
 
@@ -24,8 +25,9 @@ def _rel_l2(a, b):
     return float(np.linalg.norm(a - b) / den) if den > 0 else float(np.linalg.norm(a))
 
 
-def _check(gpu, ref, b, eps_hi=None):
-    errs = compare(gpu, ref, b, loss_rtol=1e-5, eps_hi=eps_hi)
+def _check(gpu, ref, b, X, W, eps_hi=None):
+    errs = compare(gpu, ref, b, loss_rtol=1e-5, eps_hi=eps_hi,
+                   extra_J_tol=lmhead_accum_J_bound(b, X, W, ref))
     assert gpu["dz_pad_untouched"]
     errs["dhidden_rel_l2"] = _rel_l2(gpu["dhidden"], ref["dhidden"])
     errs["dW_rel_l2"] = _rel_l2(gpu["dW"], ref["dW"])
@@ -40,7 +42,7 @@ def test_lmhead_parity(dev, name, d, cta_group):
     b, X, W = lmhead_batch(name, 3, d)
     ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
     gpu = run_gpu_lmhead(b, X, W, dev)
-    errs = _check(gpu, ref, b)
+    errs = _check(gpu, ref, b, X, W)
     print(name, d, errs)
 
 
@@ -50,7 +52,7 @@ def test_lmhead_parity_152k_chunked(dev, cta_group):
     b, X, W = lmhead_batch("mid152k", 4, 128)
     ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
     gpu = run_gpu_lmhead(b, X, W, dev, chunks=3)
-    print(_check(gpu, ref, b))
+    print(_check(gpu, ref, b, X, W))
 
 
 def test_lmhead_dapo_options(dev):
@@ -59,7 +61,7 @@ def test_lmhead_dapo_options(dev):
     ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)), eps_hi=0.28, norm=1,
                              traj_mask=mask)
     gpu = run_gpu_lmhead(b, X, W, dev, eps_hi=0.28, norm="token", traj_mask=mask)
-    _check(gpu, ref, b, eps_hi=0.28)
+    _check(gpu, ref, b, X, W, eps_hi=0.28)
 
 
 @pytest.fixture(params=[1, 2], ids=["cg1", "cg2"])
@@ -190,7 +192,8 @@ def test_lmhead_tensor_parallel(dev, name, d, R, cta_group):
     assert np.max(np.abs(g["logp"] - rr.logp)) <= 2e-3
     S_abs = float(np.sum(ref["inv_norm"][np.repeat(np.arange(b.N), b.lengths)] * np.abs(rr.term)))
     J = g["stats"][G.STAT_J]
-    assert abs(J - ref["J"]) / max(abs(ref["J"]), 0.1 * S_abs) <= 1e-5  # DESIGN.md Z17
+    # DESIGN.md Z17 guard plus the tensor cores' accumulation bound (Z25)
+    assert abs(J - ref["J"]) <= 1e-5 * max(abs(ref["J"]), 1e-2 * S_abs) + lmhead_accum_J_bound(b, X, W, ref)
     for k, rk in (("dz", rr.dlogits), ("dX", ref["dhidden"]), ("dW", ref["dW"])):
         assert _rel_l2(g[k], rk) <= 1e-2, k
 
@@ -257,7 +260,7 @@ def test_lmhead_tp_dx_gemm_reduce_scatter(dev, name, d, R):
     """grpo_async_lmhead_tp_dx: dz_q W_q on the tensor cores (B read MN-major from the
     row-major W shard) with the f32 tiles stored straight into the owner rank's slot; then
     the owner's rank-order sum.  R ranks emulated on one GPU (the slot buffers are local).
-    Against the oracle's dhidden and against the cuBLAS partials summed."""
+    Against the oracle's dhidden and against the plain dX GEMM's partials summed."""
     b, X, W = lmhead_batch(name, 9, d)
     ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
     T, V = b.T, b.V
@@ -274,8 +277,10 @@ def test_lmhead_tp_dx_gemm_reduce_scatter(dev, name, d, R):
     loss.lmhead_fwd(Xd, Wd, 0, T, db.target_ids, db.logp_behav, db.cu_seqlens, adv, inv, ts, st,
                     lse_out=lse, scale_out=scale)
     rpr = -(-T // R)
-    bufs = [torch.full((R, rpr, d), float("nan"), device=dev) for _ in range(R)]
-    cublas_sum = torch.zeros((T, d), device=dev)
+    # two halves per slot buffer; call e writes half e % 2 (epoch double buffering)
+    bufs = [torch.full((2, R, rpr, d), float("nan"), device=dev) for _ in range(R)]
+    gemm_sum = torch.zeros((T, d), device=dev)
+    dzs = []
     for q in range(R):
         off = q * Vs
         Wq = Wd[off:min(off + Vs, V)].contiguous()
@@ -284,20 +289,26 @@ def test_lmhead_tp_dx_gemm_reduce_scatter(dev, name, d, R):
         dz = torch.zeros((T, ld), dtype=torch.bfloat16, device=dev)
         part = torch.empty((T, d), device=dev)
         loss.lmhead_tp_bwd(Xd, Wq, off, T, db.target_ids, lse, scale, dz, dhidden_partial=part)
-        cublas_sum += part
-        L.grpo_async_lmhead_tp_dx(dz, ld, Wq, T, d, Vq, R, q, bufs)
-    outs = []
-    for q in range(R):
-        rows = max(0, min(rpr, T - q * rpr))
-        o = torch.empty((max(rows, 1), d), device=dev)
-        L.grpo_async_lmhead_tp_dx_reduce(bufs[q], R, T, d, q, o)
-        outs.append(o[:rows])
-    torch.cuda.synchronize()
-    dX = torch.cat(outs).cpu().numpy().astype(np.float64)
-    assert dX.shape == (T, d) and np.isfinite(dX).all()
-    assert _rel_l2(dX, ref["dhidden"]) <= 1e-2
-    # two f32 GEMMs summing ~V products in different orders
-    assert _rel_l2(dX, cublas_sum.cpu().numpy().astype(np.float64)) <= 1e-3
+        gemm_sum += part
+        dzs.append((dz, ld, Wq, Vq))
+    for epoch in (1, 0):
+        for q, (dz, ld, Wq, Vq) in enumerate(dzs):
+            L.grpo_async_lmhead_tp_dx(dz, ld, Wq, T, d, Vq, R, q, bufs, epoch)
+        if epoch == 1:  # the other half is untouched
+            torch.cuda.synchronize()
+            assert all(torch.isnan(b_[0]).all().item() for b_ in bufs)
+        outs = []
+        for q in range(R):
+            rows = max(0, min(rpr, T - q * rpr))
+            o = torch.empty((max(rows, 1), d), device=dev)
+            L.grpo_async_lmhead_tp_dx_reduce(bufs[q], R, T, d, q, o, epoch)
+            outs.append(o[:rows])
+        torch.cuda.synchronize()
+        dX = torch.cat(outs).cpu().numpy().astype(np.float64)
+        assert dX.shape == (T, d) and np.isfinite(dX).all()
+        assert _rel_l2(dX, ref["dhidden"]) <= 1e-2
+        # two f32 GEMMs (the plain dX GEMM per shard, summed; the fused one) in different orders
+        assert _rel_l2(dX, gemm_sum.cpu().numpy().astype(np.float64)) <= 1e-3
 
 
 @pytest.mark.parametrize("seed", range(6))
@@ -321,4 +332,4 @@ def test_lmhead_random_shapes(dev, seed, cta_group):
     b = dataclasses.replace(b, logp_behav=lw)
     ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
     gpu = run_gpu_lmhead(b, X, W, dev, chunks=int(rng.integers(1, 4)))
-    _check(gpu, ref, b)
+    _check(gpu, ref, b, X, W)

@@ -256,7 +256,9 @@ def test_gradient_finite_differences(seed):
             num[t, v] = -(_J_of(zp, b, adv, inv) - _J_of(zm, b, adv, inv)) / (2 * h)
     err = np.abs(num - rr.dlogits).max() / max(np.abs(rr.dlogits).max(), 1e-12)
     assert err < 1e-6, err
-    assert rr.clipped.any() or True
+    # with noise 0.25 on the ratios, every seed clips some tokens (zero-gradient rows, whose
+    # finite differences are zero too) and keeps others active
+    assert rr.clipped.any() and (~rr.clipped).any()
 
 
 def test_gradient_vs_torch_autograd():
@@ -404,9 +406,8 @@ def test_validate_injected_faults():
     for gap, bit in ((K, 0), (K + 1, 1 << 0), (-1, 1 << 1), (0, 0)):
         ver = b.version_ids.copy()
         ver[3] = b.v_theta - gap
-        v = _val(b, K=K) if False else O.validate(ver, b.cu_seqlens, b.group_ids, b.target_ids,
-                                                   P=b.P, V=b.V, G=b.G, tbs=b.tbs,
-                                                   v_theta=b.v_theta, K=K)
+        v = O.validate(ver, b.cu_seqlens, b.group_ids, b.target_ids, P=b.P, V=b.V, G=b.G,
+                       tbs=b.tbs, v_theta=b.v_theta, K=K)
         exp = np.zeros(b.N, np.uint32)
         exp[3] = bit
         assert np.array_equal(v["traj_flags"], exp), gap
@@ -440,7 +441,7 @@ def test_validate_injected_faults():
     exp = np.zeros(b.N, np.uint32)
     exp[4] = 1 << 5
     assert np.array_equal(v["traj_flags"], exp)
-    assert v["summary"]["c1_violations" if False else "n_c1_mixed"] == 1
+    assert v["summary"]["n_c1_mixed"] == 1
     # zero-length trajectory, TBS mismatch
     cu = b.cu_seqlens.copy()
     cu[3] = cu[2]
