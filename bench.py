@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--stages", type=int, default=0)
     ap.add_argument("--lag", type=int, default=0, help="grpo_tune_t.lag (kernel 3: free ring slots)")
     ap.add_argument("--chunk-kb", type=int, default=0, help="grpo_tune_t.chunk_kb (kernel 3)")
+    ap.add_argument("--prefetch", type=int, default=0,
+                    help="grpo_tune_t.prefetch (kernel 3: look-ahead chunks, -1 none, 0 default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -296,18 +298,47 @@ def main():
                               dd["tgt_l"], dd["lw_l"], dd.get("tv_l"))
     sb = sharded(d)
 
-    # ---- resident logits buffer (device-generated, bit-identical to synth/gen.py) and dlogits
-    logits = torch.empty((R, ld), dtype=torch.int16, device=dev)
-    dlogits = torch.empty((R, ld), dtype=torch.int16, device=dev)
+    # ---- logits (device-generated, bit-identical to synth/gen.py) and the dlogits buffer.
+    # The recipe: logical row t reads physical row t % chunk_rows.  One rank holds one resident
+    # chunk buffer, which is exactly every chunk's logits.  With N > 1 ranks a rank's rows are
+    # a scattered set of trajectories, so each rank holds all of ITS rows' logits resident
+    # (filled once, trajectory by trajectory, with the same recipe) and writes dlogits through
+    # a chunk buffer sized to the memory left: every rank computes on the batch's own logits
+    # and J is the unsharded batch's at every N.
     spec = batch.logits
-    spec.period = R
-    SG.fill_logits(logits, spec, 0, R, V)
+    resident_ok = world > 1 and T_local * ld * 2 <= torch.cuda.mem_get_info(dev)[0] - (24 << 30)
+    if not resident_ok:   # one rank, or a shard too large to hold (e.g. `large` at N = 2)
+        spec.period = R
+        logits = torch.empty((R, ld), dtype=torch.int16, device=dev)
+        SG.fill_logits(logits, spec, 0, R, V)
+        logits_desc = ("device-generated counter-hash bf16, rows periodic in the chunk buffer "
+                       "(DESIGN.md input recipe)" + ("" if world == 1 else
+                       "; rank-local rows read the chunk buffer periodically, so J is not the "
+                       "batch's at this N"))
+    else:
+        logits = torch.empty((max(T_local, 1), ld), dtype=torch.int16, device=dev)
+        base_dev = None
+        for j, i in enumerate(mine):
+            base_dev = SG.fill_logits(logits[int(local_cu[j]):int(local_cu[j + 1])], spec,
+                                      int(batch.cu_seqlens[i]), int(batch.lengths[i]), V,
+                                      base_dev=base_dev)
+        torch.cuda.synchronize()
+        free = torch.cuda.mem_get_info(dev)[0]
+        R = int(max(1024, min(R, (free - (6 << 30)) // (ld * 2))))
+        n_chunks = (T_local + R - 1) // R
+        logits_desc = ("device-generated counter-hash bf16 (the N=1 recipe); each rank holds its "
+                       "own rows' logits resident, dlogits through a chunk buffer")
+    dlogits = torch.empty((R, ld), dtype=torch.int16, device=dev)
+
+    def logits_of(b, n):
+        return logits[b:b + n] if resident_ok else logits[:n]
 
     tune = None
-    if args.kernel or args.cluster or args.ctas_per_sm or args.stages or args.lag or args.chunk_kb:
+    if (args.kernel or args.cluster or args.ctas_per_sm or args.stages or args.lag or args.chunk_kb
+            or args.prefetch):
         tune = {"kernel": args.kernel, "cluster_size": args.cluster,
                 "ctas_per_sm": args.ctas_per_sm, "stages": args.stages, "lag": args.lag,
-                "chunk_kb": args.chunk_kb}
+                "chunk_kb": args.chunk_kb, "prefetch": args.prefetch}
     loss = G.GrpoAsyncLoss(eps=cfg.eps, std_floor=cfg.std_floor, tune=tune)
     vo = G.ValidateOut(batch.N, batch.P, batch.K, dev)
     adv = torch.empty(batch.N, dtype=torch.float32, device=dev)
@@ -336,7 +367,7 @@ def main():
         for c in range(n_chunks):
             b = c * R
             n = min(R, T_local - b)
-            loss.loss_chunk(logits[:n], b, n, sbx.target_ids[b:b + n], sbx.logp_behav[b:b + n],
+            loss.loss_chunk(logits_of(b, n), b, n, sbx.target_ids[b:b + n], sbx.logp_behav[b:b + n],
                             sbx.local_cu, adv, inv, traj_sum, stats, dlogits=dlogits[:n],
                             traj_index=sbx.traj_index, V=V)
         # the path's one exchange: every rank's packed partials all-gathered, summed in rank
@@ -468,11 +499,10 @@ def main():
             "config": {"workload": args.config, "tokens_per_step": T_total, "vocab": V,
                        "prompts": batch.P, "group_size": batch.G, "K": batch.K,
                        "chunk_rows": R, "n_chunks_per_rank": n_chunks,
-                       "l2": "inputs larger than L2 (logits+dlogits chunk buffers %.1f GB)"
-                             % (2 * R * ld * 2 / 1e9),
+                       "l2": "inputs larger than L2 (logits %.1f GB + dlogits chunk buffer %.1f GB)"
+                             % (logits.numel() * 2 / 1e9, R * ld * 2 / 1e9),
                        "parallelism": f"dp{world} token-balanced LPT over trajectories",
-                       "logits": "device-generated counter-hash bf16, rows periodic in the "
-                                 "chunk buffer (DESIGN.md input recipe)"},
+                       "logits": logits_desc},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "frac_of_spec_8000_gbs": achieved / 8000.0,

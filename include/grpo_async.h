@@ -130,7 +130,8 @@ typedef struct {
                            /* ring slots left free at the end of pass 1 (0 = 3)              */
     int32_t prefetch;      /* kernel 2: 1 = TMA-prefetch each CTA's next row into L2;        */
                            /* kernel 3: chunks of the next row streamed before a row's pass */
-                           /* 2, hiding its epilogue (0 = 2; capped at stages - resident)   */
+                           /* 2, hiding its epilogue (0 = 1, -1 = none; capped at stages -  */
+                           /* resident)                                                      */
     int32_t row_cache;     /* kernel 2: leading vectors per thread of each row kept in shared */
                            /* memory for the second pass (0 auto = 160 KB per SM, -1 none); */
                            /* kernel 3: CTAs per SM, 1 (default) or 2                        */

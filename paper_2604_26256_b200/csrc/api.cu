@@ -462,6 +462,7 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     const int n_vec_row = (V + 7) / 8;
     const bool auto_stream = kernel == 0 && untuned && n_vec_row >= 4250;
     grpo_tune_t stream_tune{};
+    stream_tune.prefetch = tune ? tune->prefetch : 0;  // K3c look-ahead (kept by the auto plan)
     if (auto_stream && n_vec_row >= 11250) {
         stream_tune.kernel = 3;
         stream_tune.chunk_kb = 32;

@@ -116,6 +116,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         if (++spins == (1u << 26)) __trap();
 }
 
+// The same for a warp that has nothing else to do while it waits (the ring's producer, the
+// epilogue warp): after each failed try_wait it sleeps `ns` nanoseconds, so its polling takes
+// fewer issue slots from the consumer warps of its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t spins = 0;
+    while (!mbar_try_wait(a, parity)) {
+        __nanosleep(ns);
+        if (++spins == (1u << 26)) __trap();  // see mbar_wait
+    }
+}
+
 // Same, with cluster-scope acquire (the phase is completed by peer CTAs' st.async).
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);

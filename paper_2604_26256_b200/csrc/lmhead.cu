@@ -73,19 +73,24 @@ struct Geo {
     static constexpr int STAGE = A_BYTES + B_BYTES_CG;
     static constexpr int NSTAGE = CG == 1 ? STAGES : 6;
     static constexpr int SMEM = NSTAGE * STAGE + 1024 + 256;
+    // + the store epilogues' staging (EPI_DZ / EPI_LOGITS): 4 warps x 2 boxes of 32 x 128 B
+    static constexpr int STAGING = 4 * 2 * 4096;
+    static constexpr int SMEM_STORE = SMEM + STAGING;
 };
 
 template <int EPI, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     lmhead_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                  const Params p) {
+                  const __grid_constant__ CUtensorMap tmO, const Params p) {
     using GG = Geo<CG>;
     constexpr int NS = GG::NSTAGE;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem;                             // NS x A_BYTES
     uint8_t *sB = smem + NS * A_BYTES;              // NS x B_BYTES_CG
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * GG::STAGE);
+    // the store epilogues' staging boxes sit between the stages and the barriers
+    uint8_t *staging = smem + NS * GG::STAGE;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * GG::STAGE + (EPI == EPI_STATS ? 0 : GG::STAGING));
     uint64_t *full = bars, *empty = bars + NS, *tfull = bars + 2 * NS, *tempty = bars + 2 * NS + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -106,6 +111,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tc::prefetch_tmap(&tmX);
         tc::prefetch_tmap(&tmW);
+        if (EPI != EPI_STATS) tc::prefetch_tmap(&tmO);
     }
     if (warp == 1) {
         if (CG == 2) tc::tmem_alloc2(tmem_slot, TMEM_COLS);
@@ -192,6 +198,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ------------------------------------------------------------ epilogue (warps 2-5)
         const int q = warp & 3;                 // TMEM lane quarter this warp may access
         const int r_in_tile = q * 32 + lane;
+        uint8_t *wbuf = staging + q * 8192;     // store epilogues: this warp's two boxes
+        int n_boxes = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
@@ -220,6 +228,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tc::fence_after();
                 const int v0 = vt * BN;
                 const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+                if (EPI == EPI_STATS) {
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     tc::tmem_wait_ld();
                     const int cb = v0 + c * 32;          // first vocabulary column of the chunk
                     const int nvalid = min(32, p.V - cb);  // > 0 except in a ragged last tile
-                    if (EPI == EPI_STATS) {
+                    {
                         // exponents z*log2(e) - M with the exact log2 e (two FMAs, common.cuh
                         // kLog2eHi/Lo), the chunk's 32 terms summed in fp32, the row's sum in fp64
                         float zt[32];
@@ -254,36 +263,67 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 if (cb + j == y) zy = __uint_as_float(r[j]);
                             have_y = true;
                         }
-                    } else if (valid && nvalid > 0) {
-                        uint32_t w[16];
-                        if (EPI == EPI_LOGITS) {
+                    }
+                }
+                } else {
+                    // 64 columns per box: 32 rows x 128 B staged with the 128-byte swizzle, then a TMA
+                    // tile store (rows >= n_rows and columns >= V clipped by the tensor map, so the
+                    // padding columns of dz stay untouched) -- coalesced 128-byte rows
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; c += 2) {
+                        const int cb = v0 + c * 32;
+                        if (cb >= p.V) break;  // warp-uniform: the rest of a ragged last tile
+                        uint32_t r[32], r2[32];
+                        tc::tmem_ld32(t_row + (uint32_t)(c * 32), r);
+                        tc::tmem_ld32(t_row + (uint32_t)(c * 32 + 32), r2);
+                        tc::tmem_wait_ld();
+                        // a box that straddles V (the ragged last tile) is stored element by
+                        // element: a TMA store clips at 16-byte granularity and would write the
+                        // padding columns [V, ld) that share the last 16 bytes
+                        const bool ragged = cb + 64 > p.V;
+                        uint8_t *box = wbuf + (n_boxes & 1) * 4096;
+                        if (!ragged && n_boxes >= 2) {  // the store of two boxes ago has read it
+                            if (lane == 0) tc::bulk_wait_read<1>();
+                            __syncwarp();
+                        }
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                w[j] = pack_bf16x2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-                        } else {  // EPI_DZ: s (p - onehot); exact zeros when s == 0
+                        for (int j = 0; j < 8; ++j) {
+                            const uint32_t *src = j < 4 ? r : r2;
+                            uint32_t w[4];
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                float g[2];
-#pragma unroll
-                                for (int h = 0; h < 2; ++h) {
-                                    const int jj = 2 * j + h;
-                                    const float pr = ex2(fmaf(__uint_as_float(r[jj]), kLog2e, -lse2));
-                                    g[h] = sc == 0.0f ? 0.0f : sc * (pr - (cb + jj == y ? 1.0f : 0.0f));
+                            for (int h = 0; h < 4; ++h) {
+                                const int o = (j & 3) * 8 + 2 * h;  // column cb + 8j + 2h within the box
+                                float g0 = __uint_as_float(src[o]), g1 = __uint_as_float(src[o + 1]);
+                                if (EPI == EPI_DZ) {  // s (p - onehot); exact zeros when s == 0
+                                    const int col = cb + 8 * j + 2 * h;
+                                    const float p0 = ex2(fmaf(g0, kLog2e, -lse2));
+                                    const float p1 = ex2(fmaf(g1, kLog2e, -lse2));
+                                    g0 = sc == 0.0f ? 0.0f : sc * (p0 - (col == y ? 1.0f : 0.0f));
+                                    g1 = sc == 0.0f ? 0.0f : sc * (p1 - (col + 1 == y ? 1.0f : 0.0f));
                                 }
-                                w[j] = pack_bf16x2(g[0], g[1]);
+                                w[h] = pack_bf16x2(g0, g1);
                             }
-                        }
-                        uint16_t *dst = p.out + (int64_t)row * p.ld_out + cb;
-                        if (nvalid == 32) {
-                            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+                            if (ragged) {
+                                if (valid) {
+                                    uint16_t *dst = p.out + (int64_t)row * p.ld_out + cb + 8 * j;
 #pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                d4[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (j < nvalid) dst[j] = (uint16_t)(j & 1 ? (w[j >> 1] >> 16) : (w[j >> 1] & 0xFFFFu));
+                                    for (int e = 0; e < 8; ++e)
+                                        if (cb + 8 * j + e < p.V)
+                                            dst[e] = (uint16_t)(e & 1 ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xFFFFu));
+                                }
+                                continue;
+                            }
+                            *reinterpret_cast<uint4 *>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                                make_uint4(w[0], w[1], w[2], w[3]);
                         }
+                        if (ragged) continue;
+                        tc::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tc::tma_store_2d(&tmO, box, cb, m_tile * (BM * CG) + (int)crank * BM + q * 32);
+                            tc::bulk_commit();
+                        }
+                        ++n_boxes;
                     }
                 }
                 tc::fence_before();
@@ -297,6 +337,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (have_y) p.zy[row] = zy;
             }
         }
+        if (EPI != EPI_STATS && lane == 0) tc::bulk_wait_all();  // stores done before smem goes away
     }
     tc::fence_before();
     __syncthreads();
@@ -400,6 +441,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// the store epilogues' output: bf16 [rows, cols] with leading dimension ld, box 32 rows x 64
+// columns (128 B) with the 128-byte swizzle of the staging boxes
+static bool make_out_map(CUtensorMap *m, void *base, int64_t rows, int64_t cols, int64_t ld) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint32_t box[2] = {64u, 32u};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // [rows, d] bf16 row-major, box [box_rows, 64] with the 128-byte swizzle
 static bool make_map(CUtensorMap *m, const void *base, int64_t rows, int32_t d, int box_rows) {
     auto fn = encode_fn();
@@ -434,8 +489,9 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     using namespace lm;
     if (n_rows == 0) return cudaSuccess;
     const int CG = cta_group == 1 ? 1 : 2;
-    CUtensorMap mx, mw;
-    if (!make_map(&mx, X, n_rows, d, BM) || !make_map(&mw, W, V, d, BN / CG)) {
+    CUtensorMap mx, mw, mo;
+    if (!make_map(&mx, X, n_rows, d, BM) || !make_map(&mw, W, V, d, BN / CG) ||
+        (epi != EPI_STATS && !make_out_map(&mo, out, n_rows, V, ld_out))) {
         if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
         return cudaErrorInvalidValue;
     }
@@ -477,11 +533,11 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     cfg.numAttrs = 1;
 #define GRPO_LM_LAUNCH(E, CG_)                                                                         \
     do {                                                                                               \
-        cfg.dynamicSmemBytes = Geo<CG_>::SMEM;                                                         \
+        cfg.dynamicSmemBytes = E == EPI_STATS ? Geo<CG_>::SMEM : Geo<CG_>::SMEM_STORE;                \
         e = cudaFuncSetAttribute(lmhead_kernel<E, CG_>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                 Geo<CG_>::SMEM);                                                      \
+                                 (int)cfg.dynamicSmemBytes);                                           \
         if (e != cudaSuccess) return e;                                                                \
-        e = cudaLaunchKernelEx(&cfg, lmhead_kernel<E, CG_>, mx, mw, p);                                \
+        e = cudaLaunchKernelEx(&cfg, lmhead_kernel<E, CG_>, mx, mw, epi == EPI_STATS ? mx : mo, p);   \
     } while (0)
     if (CG == 1) {
         if (epi == EPI_STATS) GRPO_LM_LAUNCH(EPI_STATS, 1);

@@ -78,20 +78,34 @@ __host__ __device__ constexpr uint32_t idesc_b_mn(int M, int N, bool a_mn) {
 // 2-5 of each CTA drain their 128 TMEM lanes (one thread = one row of D) into the epilogue.
 // CG = 2: a CTA pair (cluster of 2, tcgen05.mma.cta_group::2): each CTA stages its own 128
 // rows of A and half of the tile's BN columns of B.
+// The epilogue of the store variants (EPI_BF16 / EPI_F32 / EPI_F32_ACC) stages each warp's 32
+// rows x 128 bytes (32 f32 or 64 bf16 columns) in shared memory with the 128-byte swizzle (a
+// thread writes its row's 16-byte chunk j at chunk j ^ (row & 7): conflict-free) and one lane
+// issues a TMA tile store -- or, for dW += dz^T X, a TMA reduce-add -- of the box: coalesced
+// 128-byte rows instead of 32 rows written 16 bytes at a time by 32 threads, rows beyond M
+// clipped by the tensor map, and no read-modify-write traffic through the SM for dW.
+// Two 4 KB buffers per warp; the store issued two boxes earlier must have read its buffer.
+template <int EPI, int CG>
+struct Epi {
+    static constexpr int STAGING = EPI == EPI_SLOTS ? 0 : 4 * 2 * 4096;  // 4 warps x 2 buffers
+};
+
 template <bool A_MN, int BN, int CG, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmO, const Params p) {
     constexpr int A_BYTES = BM * BK * 2;          // 16 KB
     constexpr int NB = BN / 64 / CG;              // 64-wide N atoms staged per CTA
     constexpr int ATOM = BK * 64 * 2;             // 8 KB: 64 K-rows x 64 MN elements
     constexpr int STAGE = A_BYTES + NB * ATOM;
-    constexpr int NS = CG == 1 ? STAGES : 6;
+    constexpr int NS = CG == 1 ? STAGES : 6;  // 6 x 32 KB + 32 KB of staging fits in 227 KB
     constexpr uint32_t TMEM_COLS = 2 * BN;
     static_assert(NB >= 1, "BN / CG must be a multiple of 64");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem, *sB = smem + NS * A_BYTES;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * STAGE);
+    uint8_t *staging = smem + NS * STAGE;  // 1 KB aligned (STAGE is a multiple of 8 KB)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * STAGE + Epi<EPI, CG>::STAGING);
     uint64_t *full = bars, *empty = bars + NS, *tfull = bars + 2 * NS, *tempty = bars + 2 * NS + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -112,6 +126,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tc::prefetch_tmap(&tmA);
         tc::prefetch_tmap(&tmB);
+        if (EPI != EPI_SLOTS) tc::prefetch_tmap(&tmO);
     }
     if (warp == 1) {
         if (CG == 2) tc::tmem_alloc2(tmem_slot, TMEM_COLS);
@@ -205,55 +220,75 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else {  // ---- epilogue: each thread one row of the tile
         const int q = warp & 3;
         const int r_in_tile = q * 32 + lane;
+        uint8_t *wbuf = staging + q * 8192;  // this warp's two 4 KB boxes
+        int n_boxes = 0;                     // boxes this warp has handed to TMA
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
             int m_tile, n_tile;
             decode(p, unit, m_tile, n_tile);
-            const int row = m_tile * BM * CG + (int)crank * BM + r_in_tile;
+            const int row0 = m_tile * BM * CG + (int)crank * BM;  // first row of this CTA's 128
+            const int row = row0 + r_in_tile;
             mbar_wait(tfull + acc, acc_phase);
             tc::fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
-            const bool valid = row < p.M;
-            int64_t off = 0;  // element offset of this row's first column of the tile
-            float *slot_dst = nullptr;
-            if (EPI == EPI_SLOTS && valid) {
-                const int owner = row / p.rows_per_rank;
-                slot_dst = p.slots[owner] + ((int64_t)p.rank * p.rows_per_rank + (row - owner * p.rows_per_rank)) *
-                                                p.N + n_tile * BN;
-            } else {
-                off = (int64_t)row * p.ldo + (int64_t)n_tile * BN;
-            }
+            if (EPI == EPI_SLOTS) {
+                const bool valid = row < p.M;
+                float *slot_dst = nullptr;
+                if (valid) {
+                    const int owner = row / p.rows_per_rank;
+                    slot_dst = p.slots[owner] +
+                               ((int64_t)p.rank * p.rows_per_rank + (row - owner * p.rows_per_rank)) * p.N +
+                               n_tile * BN;
+                }
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tc::tmem_ld32(t_row + (uint32_t)(c * 32), r);
-                tc::tmem_wait_ld();
-                if (!valid) continue;
-                if (EPI == EPI_SLOTS || EPI == EPI_F32) {
-                    float *dst = EPI == EPI_SLOTS ? slot_dst + c * 32 : static_cast<float *>(p.out) + off + c * 32;
-                    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tc::tmem_ld32(t_row + (uint32_t)(c * 32), r);
+                    tc::tmem_wait_ld();
+                    if (!valid) continue;
+                    uint4 *d4 = reinterpret_cast<uint4 *>(slot_dst + c * 32);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) d4[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-                } else if (EPI == EPI_F32_ACC) {
-                    float4 *d4 = reinterpret_cast<float4 *>(static_cast<float *>(p.out) + off + c * 32);
+                }
+            } else {
+                // one box = 32 rows x 128 bytes: 32 f32 columns, or 64 bf16 columns (two loads)
+                constexpr int COLS = EPI == EPI_BF16 ? 64 : 32;
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += COLS) {
+                    uint32_t r[32], r2[32];
+                    tc::tmem_ld32(t_row + (uint32_t)c0, r);
+                    if (EPI == EPI_BF16) tc::tmem_ld32(t_row + (uint32_t)(c0 + 32), r2);
+                    tc::tmem_wait_ld();
+                    uint8_t *box = wbuf + (n_boxes & 1) * 4096;
+                    if (n_boxes >= 2) {  // the store of two boxes ago has read this buffer
+                        if (lane == 0) tc::bulk_wait_read<1>();
+                        __syncwarp();
+                    }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        float4 v = d4[j];
-                        v.x += __uint_as_float(r[4 * j]);
-                        v.y += __uint_as_float(r[4 * j + 1]);
-                        v.z += __uint_as_float(r[4 * j + 2]);
-                        v.w += __uint_as_float(r[4 * j + 3]);
-                        d4[j] = v;
+                        uint4 v;
+                        if (EPI == EPI_BF16) {
+                            const uint32_t *src = j < 4 ? r : r2;
+                            const int o = (j & 3) * 8;
+                            v = make_uint4(pack_bf16x2(__uint_as_float(src[o]), __uint_as_float(src[o + 1])),
+                                           pack_bf16x2(__uint_as_float(src[o + 2]), __uint_as_float(src[o + 3])),
+                                           pack_bf16x2(__uint_as_float(src[o + 4]), __uint_as_float(src[o + 5])),
+                                           pack_bf16x2(__uint_as_float(src[o + 6]), __uint_as_float(src[o + 7])));
+                        } else {
+                            v = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+                        }
+                        *reinterpret_cast<uint4 *>(box + lane * 128 + ((j ^ (lane & 7)) << 4)) = v;
                     }
-                } else {  // EPI_BF16
-                    uint4 *d4 = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(p.out) + off + c * 32);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        d4[j] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * j]), __uint_as_float(r[8 * j + 1])),
-                                           pack_bf16x2(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3])),
-                                           pack_bf16x2(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5])),
-                                           pack_bf16x2(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7])));
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int col = n_tile * BN + c0, rr = row0 + q * 32;
+                        if (EPI == EPI_F32_ACC) tc::tma_reduce_add_2d(&tmO, box, col, rr);
+                        else tc::tma_store_2d(&tmO, box, col, rr);
+                        tc::bulk_commit();
+                    }
+                    ++n_boxes;
                 }
             }
             tc::fence_before();
@@ -262,6 +297,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1u;
         }
+        if (EPI != EPI_SLOTS && lane == 0) tc::bulk_wait_all();  // stores done before smem goes away
     }
     tc::fence_before();
     __syncthreads();
@@ -328,10 +364,11 @@ namespace lmdx {
 
 // launch gemm_kernel<A_MN, BN, CG, EPI> persistently: one CTA (pair) per SM (pair)
 template <bool A_MN, int BN, int CG, int EPI>
-static cudaError_t launch_gemm(const CUtensorMap &ma, const CUtensorMap &mb, Params &p, cudaStream_t s) {
+static cudaError_t launch_gemm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, Params &p,
+                               cudaStream_t s) {
     constexpr int NB = BN / 64 / CG;
-    constexpr int NS = CG == 1 ? STAGES : 6;
-    constexpr int SMEM = NS * (BM * BK * 2 + NB * BK * 64 * 2) + 1024 + 256;
+    constexpr int NS = CG == 1 ? STAGES : 6;  // 6 x 32 KB + 32 KB of staging fits in 227 KB
+    constexpr int SMEM = NS * (BM * BK * 2 + NB * BK * 64 * 2) + Epi<EPI, CG>::STAGING + 1024 + 256;
     p.m_tiles = (p.M + BM * CG - 1) / (BM * CG);
     p.n_tiles = p.N / BN;
     p.n_units = p.m_tiles * p.n_tiles;
@@ -354,17 +391,33 @@ static cudaError_t launch_gemm(const CUtensorMap &ma, const CUtensorMap &mb, Par
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, p);
+    e = cudaLaunchKernelEx(&cfg, kfn, ma, mb, mo, p);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 // the N tile by the GEMM's N (= d): 256 with CTA pairs, 128 with pairs, 64 on one CTA
 template <bool A_MN, int EPI>
-static cudaError_t launch_by_n(const CUtensorMap &ma, const CUtensorMap &mb, Params &p, cudaStream_t s) {
-    if (p.N % 256 == 0) return launch_gemm<A_MN, 256, 2, EPI>(ma, mb, p, s);
-    if (p.N % 128 == 0) return launch_gemm<A_MN, 128, 2, EPI>(ma, mb, p, s);
-    return launch_gemm<A_MN, 64, 1, EPI>(ma, mb, p, s);
+static cudaError_t launch_by_n(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, Params &p,
+                               cudaStream_t s) {
+    if (p.N % 256 == 0) return launch_gemm<A_MN, 256, 2, EPI>(ma, mb, mo, p, s);
+    if (p.N % 128 == 0) return launch_gemm<A_MN, 128, 2, EPI>(ma, mb, mo, p, s);
+    return launch_gemm<A_MN, 64, 1, EPI>(ma, mb, mo, p, s);
+}
+
+// the output of the store epilogues: [rows, cols] row-major (leading dimension ld elements),
+// box = 32 rows x 128 bytes, 128-byte swizzle (the staging layout of the epilogue)
+static bool make_out_map(CUtensorMap *m, void *base, int64_t rows, int64_t cols, int64_t ld, bool bf16) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const int esz = bf16 ? 2 : 4;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * esz};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32u};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace lmdx
@@ -387,8 +440,8 @@ cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *
     p.rank = rank;
     p.rows_per_rank = (int32_t)((n_rows + world - 1) / world);
     for (int q = 0; q < world; ++q) p.slots[q] = slots[q];
-    cudaError_t e = d % 256 == 0 ? launch_gemm<false, 256, 2, EPI_SLOTS>(ma, mb, p, s)
-                                 : launch_gemm<false, 128, 2, EPI_SLOTS>(ma, mb, p, s);
+    cudaError_t e = d % 256 == 0 ? launch_gemm<false, 256, 2, EPI_SLOTS>(ma, mb, ma, p, s)
+                                 : launch_gemm<false, 128, 2, EPI_SLOTS>(ma, mb, ma, p, s);
     if (e != cudaSuccess) return e;
     *launches += 1;
     return cudaSuccess;
@@ -400,8 +453,9 @@ cudaError_t launch_lmhead_gemm_dx(const uint16_t *dz, int64_t ld_dz, const uint1
                                   char *why, size_t why_len) {
     using namespace lmdx;
     if (n_rows == 0) return cudaSuccess;
-    CUtensorMap ma, mb;
-    if (!make_map(&ma, dz, n_rows, V, ld_dz, BM) || !make_map(&mb, W, V, d, d, BK)) {
+    CUtensorMap ma, mb, mo;
+    if (!make_map(&ma, dz, n_rows, V, ld_dz, BM) || !make_map(&mb, W, V, d, d, BK) ||
+        !make_out_map(&mo, out, n_rows, d, d, out_bf16 != 0)) {
         if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
         return cudaErrorInvalidValue;
     }
@@ -411,7 +465,8 @@ cudaError_t launch_lmhead_gemm_dx(const uint16_t *dz, int64_t ld_dz, const uint1
     p.K = V;
     p.out = out;
     p.ldo = d;
-    const cudaError_t e = out_bf16 ? launch_by_n<false, EPI_BF16>(ma, mb, p, s) : launch_by_n<false, EPI_F32>(ma, mb, p, s);
+    const cudaError_t e = out_bf16 ? launch_by_n<false, EPI_BF16>(ma, mb, mo, p, s)
+                                   : launch_by_n<false, EPI_F32>(ma, mb, mo, p, s);
     if (e != cudaSuccess) return e;
     *launches += 1;
     return cudaSuccess;
@@ -424,8 +479,9 @@ cudaError_t launch_lmhead_gemm_dw(const uint16_t *dz, int64_t ld_dz, const uint1
                                   size_t why_len) {
     using namespace lmdx;
     if (n_rows == 0) return cudaSuccess;
-    CUtensorMap ma, mb;
-    if (!make_map(&ma, dz, n_rows, V, ld_dz, BK) || !make_map(&mb, X, n_rows, d, d, BK)) {
+    CUtensorMap ma, mb, mo;
+    if (!make_map(&ma, dz, n_rows, V, ld_dz, BK) || !make_map(&mb, X, n_rows, d, d, BK) ||
+        !make_out_map(&mo, dW, V, d, d, false)) {
         if (why) snprintf(why, why_len, "cuTensorMapEncodeTiled failed (alignment / driver entry point)");
         return cudaErrorInvalidValue;
     }
@@ -436,7 +492,7 @@ cudaError_t launch_lmhead_gemm_dw(const uint16_t *dz, int64_t ld_dz, const uint1
     p.raster_n = 1;
     p.out = dW;
     p.ldo = d;
-    const cudaError_t e = launch_by_n<true, EPI_F32_ACC>(ma, mb, p, s);
+    const cudaError_t e = launch_by_n<true, EPI_F32_ACC>(ma, mb, mo, p, s);
     if (e != cudaSuccess) return e;
     *launches += 1;
     return cudaSuccess;

@@ -8,7 +8,7 @@
 // shared memory holds row data.  Three roles:
 //
 //   producer (one thread)   loads, per row k, the pass-1 chunks of row k, then the first
-//                           LA chunks of row k+1 (the look-ahead), then the re-loads of
+//                           LA (= 1) chunks of row k+1 (the look-ahead), then the re-loads of
 //                           row k's chunks 0..n-R-1 (the part that did not stay resident)
 //                           for pass 2, slot j % NS for the j-th load;
 //   consumers (NT threads)  pass 1 of row k (log2-domain max / sum; the first LA chunks
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
             uint32_t par = 0;  // parity of the slot's current use
             auto load = [&](int64_t row, int c, bool reload) {
                 const uint8_t *src = reinterpret_cast<const uint8_t *>(p.logits + row * p.ld + col0);
-                mbar_wait(empty + slot, par ^ 1u);
+                mbar_wait_sleep(empty + slot, par ^ 1u, 64);
                 const int64_t off = (int64_t)c * CHUNK_BYTES;
                 const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
                 // chunks read again from L2 in pass 2 stay; the rest streams through
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                 ri = p.rowinfo[row];
                 if (ri.target >= 0 && ri.target < p.V) zy_bits = p.logits[row * p.ld + ri.target];
             }
-            mbar_wait(part_bar + b, ph);
+            mbar_wait_sleep(part_bar + b, ph, 256);  // a row's pass 1 takes ~7 us
             float cm = lane < NW ? red[b][lane].a : -INFINITY;
             double cs = lane < NW ? red[b][lane].s : 0.0;
             warp_lse2_combine(cm, cs);
@@ -345,8 +345,11 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
     p.flag_ws = a.flag_ws;
     p.ns = (tune && tune->stages > 0) ? tune->stages : 0;
     p.pf = (tune && tune->lag > 0) ? tune->lag : 3;
-    // look-ahead chunks of the next row before a row's pass 2 (tune->prefetch; 0 = 2)
-    p.la = (tune && tune->prefetch > 0) ? tune->prefetch : 2;
+    // look-ahead chunks of the next row before a row's pass 2 (tune->prefetch; 0 = 1, -1 = none).
+    // A look-ahead chunk is loaded a whole row before its pass-2 re-load, so each one costs
+    // L2 hits: DRAM reads 1.008x / 1.04x / 1.13x the logits for 0 / 1 / 2 chunks (ncu, 131072
+    // rows of prod), launch 12.86 / 12.72 / 12.92 ms: one chunk hides the epilogue warp's work
+    p.la = (tune && tune->prefetch != 0) ? (tune->prefetch < 0 ? 0 : tune->prefetch) : 1;
     // consumer threads (ctas_per_sm 256 / 512), CTAs per SM (row_cache 1 / 2), slot size
     const int nt = (tune && tune->ctas_per_sm == 256) ? 256 : 512;
     const int cps = (tune && tune->row_cache == 2) ? 2 : 1;

@@ -292,16 +292,20 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 1024 / NT)) vp_kernel(co
     }
 }
 
-// The same exchange inside the streamed ring kernel (K3c, loss_stream.cu): one producer
-// thread per CTA moves the local shard's rows with bulk copies into a FIFO ring of NS
-// slots; the consumers run pass 1, post the row's partial to every rank and wait for the
-// group's partials (warp 0) while the producer already streams the next row into the
-// free slots, then run pass 2 over the resident chunks and the re-loads.  Static rows
-// only (CTA g of every rank takes rows g, g + g_per, ...); lag and dynamic_rows select
-// vp_kernel above.
+// The same exchange inside the streamed ring kernel (K3c, loss_stream.cu), with K3c's three
+// roles: one producer thread per CTA moves the local shard's rows with bulk copies into a
+// FIFO ring of NS slots (pass-1 chunks of row k, the first LA chunks of row k+1, the
+// re-loads of row k); the consumers run pass 1, publish their warp partials on an mbarrier,
+// stream row k+1's first LA chunks and then run pass 2 of row k; the epilogue warp combines
+// the warp partials, posts the row's partial to every rank, polls its own buffer for the
+// group's partials (sleeping between polls), combines them in rank order, runs the fp64
+// epilogue and hands (lse2, s, g_y, y) to pass 2.  The wait for the peers thus sits in the
+// epilogue warp, overlapped with the look-ahead, instead of stopping the consumers after
+// every row's pass 1.  Static rows only (CTA g of every rank takes rows g, g + g_per, ...);
+// lag and dynamic_rows select the row-wise kernel.
 template <int NT, int MINB, int CHUNK_VECS>
-__global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams p, const int ns,
-                                                                   const int pf) {
+__global__ void __launch_bounds__(NT + 64, MINB) vp_stream_kernel(const VpParams p, const int ns,
+                                                                   const int pf, const int la) {
     constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr int U = CHUNK_VECS / NT;
     constexpr int NW = NT / 32;
@@ -310,8 +314,10 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
     uint4 *ring = reinterpret_cast<uint4 *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)ns * CHUNK_BYTES);
     uint64_t *empty = full + ns;
-    __shared__ RowPart red[NW];
-    __shared__ float row_scalars[4];
+    __shared__ RowPart red[2][NW];
+    __shared__ float4 scal[2];
+    __shared__ __align__(8) uint64_t part_bar[2];
+    __shared__ __align__(8) uint64_t scal_bar[2];
     const int g_per = gridDim.x / p.n_local;
     const int lr = blockIdx.x / g_per;  // local rank of this CTA
     const int g = blockIdx.x - lr * g_per;
@@ -324,7 +330,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
     uint16_t *dshard = p.dlogits[lr];
     const bool two_pass = dshard != nullptr;
     const int R = two_pass ? min(n, max(0, ns - pf)) : 0;  // chunks resident after pass 1
-    const int loads = two_pass ? 2 * n - R : n;
+    const int LA = two_pass ? max(0, min(la, min(ns - R, n - R))) : 0;
     const int tail_valid = vc - (n_vec - 1) * 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -333,91 +339,64 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
             mbar_init(full + q, 1);
             mbar_init(empty + q, NW);
         }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(part_bar + b, NW);
+            mbar_init(scal_bar + b, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     if (warp == NW) {
         // ------------------------------------------------------------ producer
-        if (lane == 0) {
+        if (lane == 0 && n > 0) {
             const uint64_t pol_keep = policy_evict_last(), pol_once = policy_evict_first();
             const int64_t row_bytes = (int64_t)n_vec * 16;
             int slot = 0;
             uint32_t par = 0;
-            for (int64_t row = g; row < p.n_rows; row += g_per) {
+            auto load = [&](int64_t row, int c, bool reload) {
                 const uint8_t *src = reinterpret_cast<const uint8_t *>(shard + row * p.ld);
-                for (int i = 0; i < loads; ++i) {
-                    const int c = i < n ? i : i - n;
-                    mbar_wait(empty + slot, par ^ 1u);
-                    const int64_t off = (int64_t)c * CHUNK_BYTES;
-                    const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
-                    const uint64_t pol = (i < n && c < n - R && two_pass) ? pol_keep : pol_once;
-                    mbar_arrive_expect_tx(full + slot, bytes);
-                    bulk_g2s(ring + (size_t)slot * CHUNK_VECS, src + off, bytes, full + slot, pol);
-                    if (++slot == ns) {
-                        slot = 0;
-                        par ^= 1u;
-                    }
+                mbar_wait_sleep(empty + slot, par ^ 1u, 64);
+                const int64_t off = (int64_t)c * CHUNK_BYTES;
+                const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
+                const uint64_t pol = (!reload && c < n - R && two_pass) ? pol_keep : pol_once;
+                mbar_arrive_expect_tx(full + slot, bytes);
+                bulk_g2s(ring + (size_t)slot * CHUNK_VECS, src + off, bytes, full + slot, pol);
+                if (++slot == ns) {
+                    slot = 0;
+                    par ^= 1u;
                 }
+            };
+            for (int64_t row = g; row < p.n_rows; row += g_per) {
+                for (int c = (row == g ? 0 : LA); c < n; ++c) load(row, c, false);
+                if (row + g_per < p.n_rows)
+                    for (int c = 0; c < LA; ++c) load(row + g_per, c, false);
+                if (two_pass)
+                    for (int c = 0; c < n - R; ++c) load(row, c, true);
             }
         }
         return;
     }
 
-    // ---------------------------------------------------------------- consumers
-    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
-    int slot = 0;
-    uint32_t par = 0;
-    for (int64_t row = g; row < p.n_rows; row += g_per) {
-        const int base_slot = slot;
-        // the epilogue's dependent global reads, issued before pass 1
-        RowInfo ri;
-        uint16_t zy_bits = 0;
-        bool mine = false;
-        int32_t y_loc = -1;
-        if (threadIdx.x == 0) {
-            ri = p.rowinfo[row];
-            y_loc = ri.target - c0;
-            mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
-            if (mine) zy_bits = shard[row * p.ld + y_loc];
-        }
-        // ---- pass 1 over the local shard (full chunks, then the ragged last one)
-        float a = -INFINITY;
-        double s = 0.0;
-        auto pass1_chunk = [&](int c, bool last) {
-            const int sl = slot;
-            mbar_wait(full + sl, par);
-            if (++slot == ns) {
-                slot = 0;
-                par ^= 1u;
+    if (warp == NW + 1) {
+        // ------------------------------------------------------------ epilogue warp
+        uint32_t rowk = 0;
+        for (int64_t row = g; row < p.n_rows; row += g_per, ++rowk) {
+            const int b = rowk & 1;
+            const uint32_t ph = (rowk >> 1) & 1u;
+            RowInfo ri;
+            uint16_t zy_bits = 0;
+            int32_t y_loc = -1;
+            bool mine = false;
+            if (lane == 0) {
+                ri = p.rowinfo[row];
+                y_loc = ri.target - c0;
+                mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
+                if (mine) zy_bits = shard[row * p.ld + y_loc];
             }
-            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
-            uint4 x[U];
-#pragma unroll
-            for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
-            if (last) {
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
-                    if (vi >= n_vec) x[j] = neg_inf;
-                    else if (vi == n_vec - 1 && tail_valid < 8) x[j] = mask_tail(x[j], tail_valid);
-                }
-            }
-            B::reduce(x, a, s);
-            if (c < n - R) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty + sl);
-            }
-        };
-#pragma unroll 1
-        for (int c = 0; c < n - 1; ++c) pass1_chunk(c, false);
-        if (n > 0) pass1_chunk(n - 1, true);
-        warp_lse2_combine(a, s);
-        if (lane == 0) red[warp] = RowPart{a, 0.0f, s};
-        named_bar_sync(1, NT);
-        if (warp == 0) {
-            float cm = lane < NW ? red[lane].a : -INFINITY;
-            double cs = lane < NW ? red[lane].s : 0.0;
+            if (n > 0) mbar_wait_sleep(part_bar + b, ph, 128);
+            float cm = (n > 0 && lane < NW) ? red[b][lane].a : -INFINITY;
+            double cs = (n > 0 && lane < NW) ? red[b][lane].s : 0.0;
             warp_lse2_combine(cm, cs);
             const bool own_y = __shfl_sync(0xFFFFFFFFu, mine, 0);
             const float zy = own_y ? __uint_as_float(((uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)zy_bits, 0)) << 16)
@@ -471,18 +450,71 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
                     p.logp_ws[row] = logp;
                     p.flag_ws[row] = o.flags;
                 }
-                row_scalars[0] = lse2;
-                row_scalars[1] = o.s;
-                row_scalars[2] = o.gy;
-                row_scalars[3] = __int_as_float(mine ? y_loc : -1);
+                scal[b] = make_float4(lse2, o.s, o.gy, __int_as_float(mine ? y_loc : -1));
+                mbar_arrive(scal_bar + b);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
+    int slot = 0;
+    uint32_t par = 0;
+    auto pass1_chunk = [&](int c, bool last, float &a, double &s) {
+        const int sl = slot;
+        mbar_wait(full + sl, par);
+        if (++slot == ns) {
+            slot = 0;
+            par ^= 1u;
+        }
+        const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+        uint4 x[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+        if (last) {
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
+                if (vi >= n_vec) x[j] = neg_inf;
+                else if (vi == n_vec - 1 && tail_valid < 8) x[j] = mask_tail(x[j], tail_valid);
             }
         }
-        named_bar_sync(1, NT);
+        B::reduce(x, a, s);
+        if (c < n - R) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + sl);
+        }
+    };
+    float a = -INFINITY;
+    double s = 0.0;
+    if (g < p.n_rows)
+        for (int c = 0; c < LA; ++c) pass1_chunk(c, c == n - 1, a, s);
+    uint32_t rowk = 0;
+    for (int64_t row = g; row < p.n_rows; row += g_per, ++rowk) {
+        const int b = rowk & 1;
+        const int res_base = slot;  // slot of this row's chunk LA (chunks LA..n-1 are contiguous loads)
+#pragma unroll 1
+        for (int c = LA; c < n - 1; ++c) pass1_chunk(c, false, a, s);
+        if (n - 1 >= LA && n > 0) pass1_chunk(n - 1, true, a, s);
+        warp_lse2_combine(a, s);
+        if (!two_pass && rowk >= 2) mbar_wait(scal_bar + b, ((rowk - 2) >> 1) & 1u);
+        if (lane == 0 && n > 0) {
+            red[b][warp] = RowPart{a, 0.0f, s};
+            mbar_arrive(part_bar + b);
+        }
+        a = -INFINITY;
+        s = 0.0;
+        if (row + g_per < p.n_rows)
+            for (int c = 0; c < LA; ++c) pass1_chunk(c, c == n - 1, a, s);
         if (!two_pass) continue;
         // ---- pass 2: resident chunks n-R..n-1, then the re-loads
-        const float lse2 = row_scalars[0], sc = row_scalars[1], gy = row_scalars[2];
+        mbar_wait(scal_bar + b, (rowk >> 1) & 1u);
+        const float4 sc4 = scal[b];
+        const float lse2 = sc4.x, sc = sc4.y, gy = sc4.z;
         const auto gref = B::grad_ref(sc, lse2);
-        const int32_t y = __float_as_int(row_scalars[3]);
+        const int32_t y = __float_as_int(sc4.w);
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
         uint16_t *drow = dshard + row * p.ld;
         uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
@@ -491,7 +523,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) vp_stream_kernel(const VpParams
             const int c = resident ? n - R + i : i - R;
             int sl;
             if (resident) {
-                sl = (base_slot + c) % ns;
+                sl = (res_base + (c - LA)) % ns;
             } else {
                 sl = slot;
                 mbar_wait(full + sl, par);
@@ -544,7 +576,7 @@ static cudaError_t launch_vp_stream(VpParams p, const grpo_vp_comm_t *comm, int 
     int dev = 0, n_sm = 148, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 64, smem);
     if (e != cudaSuccess) return e;
     // every CTA must be resident (a CTA may wait for a peer rank's CTA of the same index)
     int64_t g_per = (int64_t)n_sm * (occ < MINB ? occ : MINB) / comm->n_local;
@@ -558,12 +590,13 @@ static cudaError_t launch_vp_stream(VpParams p, const grpo_vp_comm_t *comm, int 
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.gridDim = dim3((unsigned)(g_per * comm->n_local));
-    cfg.blockDim = dim3(NT + 32);
+    cfg.blockDim = dim3(NT + 64);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, p, ns, pf);
+    const int la = 1;  // look-ahead chunks (K3c's default)
+    e = cudaLaunchKernelEx(&cfg, kern, p, ns, pf, la);
     if (e != cudaSuccess) return e;
     if (plan) {
         *plan = grpo_plan_t{};

@@ -163,7 +163,7 @@ def main():
     torch.cuda.synchronize(dev)
     out["ms_fused_path_parts"] = {"dz": TIMERS[0].elapsed_time(TIMERS[1]),
                                   "dx_gemm_reduce_scatter": TIMERS[1].elapsed_time(TIMERS[2]),
-                                  "cublas_dW": TIMERS[2].elapsed_time(TIMERS[3]),
+                                  "dW_gemm": TIMERS[2].elapsed_time(TIMERS[3]),
                                   "flag_allreduce": TIMERS[3].elapsed_time(TIMERS[4]),
                                   "slot_sum": TIMERS[4].elapsed_time(TIMERS[5])}
     out["timing"] = {"rows": n, "d": d, "V": V, "shard_cols": Vs, "ms_fwd_bwd_step": ms,
