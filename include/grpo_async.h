@@ -113,12 +113,12 @@ typedef struct {
 typedef struct {
     int32_t kernel;        /* 0 auto: 2 for V < 34000; 3 with 2 CTAs x 6 x 16 KB up to 90000, */
                            /* else 3 with 1 CTA x 6 x 32 KB slots per SM, rows split over 2 */
-                           /* SMs from V = 200000 (an explicit                               */
+                           /* SMs from V = 240000 (an explicit                               */
                            /* tune with other fields set is never redirected); 1 cluster-    */
                            /* resident; 2 row-wise; 3 one row per SM through a bulk-copy ring */
     int32_t cluster_size;  /* 0 auto, else 1,2,4,8,16: CTAs sharing one row (kernel 1);      */
                            /* kernel 3: 2 = each row split over a 2-CTA cluster (the auto  */
-                           /* plan for V >= 200000; 512 threads, 1 CTA/SM, 16/32 KB slots, */
+                           /* plan for V >= 240000; 512 threads, 1 CTA/SM, 16/32 KB slots, */
                            /* V >= 16384, else GRPO_ERR_CUDA)                               */
     int32_t ctas_per_sm;   /* 0 auto, else 1..4 (kernel 1); 1,2,4,8 (kernel 2: 1024/512/256/256 threads); */
                            /* kernel 3: 256 consumer threads (default 512)                     */

@@ -451,11 +451,12 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     //   34000 <= V < 90000  K3c, two CTAs per SM of 256 consumer threads, 6 x 16 KB slots
     //                       each (V = 50688: 0.89 vs 0.84; 76032: 0.93 vs 0.87);
     //   below               the row-wise two-pass kernel K3b (V = 30000: 0.81 vs 0.80);
-    //   V >= 200000         K3c with every row split over a cluster of two SMs
+    //   V >= 240000         K3c with every row split over a cluster of two SMs
     //                       (cluster_size 2): at V = 262144 the one-SM row's pass-2
     //                       re-loads miss L2 (DRAM reads 1.185x the row, ncu) and the split
-    //                       brings them to 1.005x: 0.889-0.890 vs 0.880-0.881 in the bench;
-    //                       at V = 152064 the pair's per-row exchange costs 10 %.
+    //                       brings them to 1.005x; with the partner exchange in the epilogue
+    //                       warp a launch runs at 0.943 vs 0.844 on one SM; below 240000 the
+    //                       one-SM plan wins (the halves' ragged last chunks).
     const bool untuned = !tune || (tune->ctas_per_sm == 0 && tune->stages == 0 && tune->lag == 0 &&
                                    tune->row_cache == 0 && tune->cluster_size == 0 &&
                                    tune->chunk_kb == 0);
@@ -467,10 +468,14 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
         stream_tune.kernel = 3;
         stream_tune.chunk_kb = 32;
         stream_tune.stages = 6;
-        // free slots at the end of pass 1: 3, or 1 on very long rows (> 14 slots of
-        // 32 KB) where the re-read part of every SM's row would crowd L2
-        stream_tune.lag = (n_vec_row + 2047) / 2048 > 14 ? 1 : 3;
-        if (V >= 200000) {
+        // free slots at the end of pass 1: 3, or 1 on long rows (> 10 slots of 32 KB) where
+        // the re-read part of every SM's row would crowd L2; rows split over a two-SM cluster
+        // from V = 240000 (profiles/r02_split_sweep.jsonl, 65536-row launches, fraction of the
+        // measured copy bandwidth: V = 152064 lag 3 0.955 / lag 1 0.946 / split 0.847;
+        // 180000 0.933 / 0.951 / 0.859; 200000 0.878 / 0.912 / 0.845; 230000 0.829 / 0.856 /
+        // 0.860; 262144 0.805 / 0.844 / 0.943)
+        stream_tune.lag = (n_vec_row + 2047) / 2048 > 10 ? 1 : 3;
+        if (V >= 240000) {
             stream_tune.cluster_size = 2;
             stream_tune.lag = 3;
         }

@@ -350,8 +350,23 @@ __device__ __forceinline__ void store_tail(uint16_t *dst, const uint4 &d, int va
 // (no overflow for any finite logit) and the per-element exponent is one FFMA.
 // The same reference is used when partials merge and when the backward
 // recomputes p = 2^(z*log2e - lse2), so forward and backward agree exactly.
+// The reference is also rounded up to an INTEGER, so that every rescale between two partials,
+// 2^(a - b), is an exact power of two applied to the fp64 sum's exponent field (scale_pow2): no
+// MUFU, no conversion, no rounding, and no lane-divergent fp64 multiply in the hot loop.  The
+// row's largest element then has an exponent in (-1, 0], where fp32 still rounds it finely.
 __device__ __forceinline__ float log2_ref(float m) {
-    return m == -INFINITY ? -INFINITY : __fmul_ru(m, kLog2e);
+    return m == -INFINITY ? -INFINITY : ceilf(__fmul_ru(m, kLog2e));
+}
+
+// s * 2^k for an integer-valued k <= 0 (a difference of two log2_ref references), exactly, by
+// exponent arithmetic on the fp64 bits; 0 when the result would leave the normal range (or
+// k = -inf, s = 0)
+__device__ __forceinline__ double scale_pow2(double s, float k) {
+    if (!(k > -2000.0f)) return 0.0;
+    const long long b = __double_as_longlong(s);
+    const int e = (int)((b >> 52) & 0x7FF);
+    const int kk = (int)k;
+    return e + kk > 0 ? __longlong_as_double(b + ((long long)kk << 52)) : 0.0;
 }
 
 // Merge (a, s) with (b, t).  Symmetric in its two arguments bit for bit, so
@@ -399,9 +414,9 @@ __device__ __forceinline__ void warp_lse2_combine(float &a, float &s) {
 
 // The same with the sums held in fp64 (the row-wise kernels accumulate every thread's
 // batch sums in fp64, so a row's sum carries no fp32 rounding beyond the 32-element
-// batches).  The rescale factors 2^(a - amax) are exact powers
-// of the references' difference through ex2; the fp64 sums run in a fixed butterfly,
-// so every lane holds identical bits.
+// batches).  The rescale factors 2^(a - amax) are exact powers of two
+// (integer references, scale_pow2); the fp64 sums run in a fixed butterfly, so every lane
+// holds identical bits.
 __device__ __forceinline__ double warp_sum_all(double x) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, off);
@@ -409,7 +424,7 @@ __device__ __forceinline__ double warp_sum_all(double x) {
 }
 __device__ __forceinline__ void warp_lse2_combine(float &a, double &s) {
     const float amax = warp_max_all(a);
-    s = (amax == -INFINITY) ? 0.0 : s * (double)ex2(a - amax);
+    s = (amax == -INFINITY) ? 0.0 : scale_pow2(s, a - amax);
     s = warp_sum_all(s);
     a = amax;
 }
@@ -421,7 +436,7 @@ __device__ __forceinline__ void lse2_merge(float &a, double &s, float b, double 
         s = 0.0;
         return;
     }
-    s = s * (double)ex2(a - mn) + t * (double)ex2(b - mn);
+    s = scale_pow2(s, a - mn) + scale_pow2(t, b - mn);
     a = mn;
 }
 

@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                         const float cm = log2_ref(zm);
                         if (cm > M) {
-                            S = (M == -INFINITY) ? 0.0 : S * (double)ex2(M - cm);
+                            S = (M == -INFINITY) ? 0.0 : scale_pow2(S, M - cm);
                             M = cm;
                         }
                         if (M != -INFINITY) {

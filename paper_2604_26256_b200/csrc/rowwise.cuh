@@ -31,11 +31,12 @@ struct RowwiseBatch {
 #pragma unroll
         for (int j = 0; j < U; ++j)
             mx2 = bmax2(bmax2(mx2, bmax2(x[j].x, x[j].y)), bmax2(x[j].z, x[j].w));
-        const float va = log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2)));
-        if (va > a) {
-            s = (a == -INFINITY) ? 0.0 : s * (double)ex2(a - va);
-            a = va;
-        }
+        // the new reference (integer-valued) and the exact power-of-two rescale of the sum so
+        // far, branch-free: a warp's lanes raise their maxima in different batches, and a
+        // divergent rescale block would run for the whole warp in nearly every batch
+        const float va = fmaxf(a, log2_ref(fmaxf(bf_lo(mx2), bf_hi(mx2))));
+        s = scale_pow2(s, a - va);  // a = va: s unchanged; a = -inf: s (= 0) stays 0
+        a = va;
         // with a = -inf every element so far is -inf: reference 0 keeps the terms 0
         s += (double)sum_exp2(x, a == -INFINITY ? 0.0f : a);
     }

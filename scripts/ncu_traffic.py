@@ -34,7 +34,7 @@ def get(name):
 
 
 rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
-alg = 4 * args.V + 25
+alg = 4 * args.V + 29  # 2V read, 2V write, 16 B row info, fp64 term + logp + flag
 out = {
     "kernel": vals[hdr.index("Kernel Name")],
     "plan_kernel": args.plan_kernel,

@@ -1,7 +1,8 @@
 """Per-kernel SASS instruction histogram of the shipped library (cuobjdump -sass), the
 evidence that the hot kernels are what DESIGN.md says they are: UBLKCP (bulk copy) + MUFU.EX2
-+ FFMA2/FADD2 + HMNMX2 in the K3c ring kernel, UTCHMMA/UTCQMMA (tcgen05.mma) + UTMALDG (TMA)
-+ LDTM (tcgen05.ld) in the LM-head GEMMs.
++ FFMA2/FADD2 + VHMNMX (bf16x2 max) in the K3c ring kernel, UTCHMMA (tcgen05.mma) + UTMALDG
+(TMA load) + LDTM (tcgen05.ld) + UTMASTG / UTMAREDG (TMA store / reduce-add) in the LM-head
+GEMMs.
 
     python scripts/sass_histogram.py [lib] > profiles/r02_sass_histogram.txt
 """
@@ -25,8 +26,8 @@ for line in sass.splitlines():
     if cur and m:
         op = m.group(2) + (m.group(3) or "")
         funcs[cur][op] += 1
-KEY = ("UBLKCP", "UTMALDG", "UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "MUFU.EX2", "FFMA2", "FADD2",
-       "HMNMX2", "F2FP", "DADD", "DFMA", "SYNCS", "STG", "LDS", "LDG", "BAR")
+KEY = ("UBLKCP", "UTMALDG", "UTMASTG", "UTMAREDG", "UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "MUFU.EX2",
+       "FFMA2", "FADD2", "VHMNMX", "F2FP", "DADD", "DFMA", "SYNCS", "STG", "LDS", "LDG", "BAR")
 for f, c in funcs.items():
     name = demangle(f)
     if not any(k in name for k in ("stream_kernel", "rowwise_kernel", "gemm_kernel", "lmhead_kernel",

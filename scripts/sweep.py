@@ -16,6 +16,11 @@ ap.add_argument("--fwd-only", action="store_true")
 ap.add_argument("--vocab", type=int, default=0, help="override the config's V (e.g. a vocab shard)")
 args = ap.parse_args()
 dev = torch.device("cuda:0")
+try:  # the measured copy bandwidth (MEASURED_PEAKS.json), else the profiling guide's fallback
+    PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "MEASURED_PEAKS.json")))["hbm_gbs"]
+except Exception:
+    PEAK = 6650.0
 import dataclasses
 cfg = CONFIGS[args.config]
 if args.vocab:
@@ -34,7 +39,7 @@ st = torch.zeros(G.NUM_STATS, dtype=torch.float64, device=dev)
 plans = [json.loads(p) for p in args.plans.split(";")] if args.plans else [
     {}, {"kernel": 2}, {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 3},
 ]
-bytes_row = 4 * V + 25 if not args.fwd_only else 2 * V + 25
+bytes_row = 4 * V + 29 if not args.fwd_only else 2 * V + 29
 def run_once(plan):
     plan = dict(plan)
     for k, v in plan.pop("env", {}).items():  # launch-time environment knobs (experiments)
@@ -72,5 +77,5 @@ for i, plan in enumerate(plans):
     ms = float(np.median(times[i]))
     print(json.dumps({"tune": plan, "plan": plans_used[i], "ms": round(ms, 3),
                       "GBps": round(bytes_row * R / ms / 1e6, 1),
-                      "frac": round(bytes_row * R / ms / 1e6 / 6546.6, 3)}), flush=True)
+                      "frac": round(bytes_row * R / ms / 1e6 / PEAK, 3)}), flush=True)
 G.grpo_profile_enable(False)

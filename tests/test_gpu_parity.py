@@ -313,11 +313,13 @@ def test_odd_vocabulary_sizes(dev, V):
 def test_auto_plan_choice(dev):
     """The auto plan (tune kernel 0): K3b below V = 34000, K3c with two 256-thread CTAs per
     SM and 16 KB slots up to V = 90000, K3c with one CTA per SM and 32 KB slots from there
-    on, each row split over a two-CTA cluster from V = 200000 (DESIGN.md section 8
-    measurements); an explicitly tuned call is never redirected."""
+    on (one free ring slot past 10 slots of row), each row split over a two-CTA cluster from
+    V = 240000 (DESIGN.md section 8 measurements); an explicitly tuned call is never
+    redirected."""
     import paper_2604_26256_b200 as Gp
     for V, kernel, cps in ((30000, 2, None), (34000, 3, 2), (76032, 3, 2), (89990, 3, 2),
-                           (90000, 3, 1), (152064, 3, 1), (199999, 3, 1), (200000, 3, 1), (262144, 3, 1)):
+                           (90000, 3, 1), (152064, 3, 1), (163840, 3, 1), (163848, 3, 1), (239999, 3, 1),
+                           (240000, 3, 1), (262144, 3, 1)):
         rows = [(np.random.default_rng(V).normal(size=V), 3) for _ in range(4)]
         b, bits = _adversarial_batch(V, rows)
         ref = run_oracle(b, bits)
@@ -328,7 +330,9 @@ def test_auto_plan_choice(dev):
             assert plan["stages"] == 6 and plan["ctas_per_sm"] == cps, (V, plan)
             assert plan["smem_bytes"] >= 6 * (32768 if cps == 1 else 16384)
             assert plan["vec_per_thread"] == (512 if cps == 1 else 256), (V, plan)
-            assert plan["cluster_size"] == (2 if V >= 200000 else 1), (V, plan)
+            assert plan["cluster_size"] == (2 if V >= 240000 else 1), (V, plan)
+            if cps == 1:
+                assert plan["lag"] == (1 if 163840 < V < 240000 else 3), (V, plan)
         compare(gpu, ref, b, logits_pad=bits[:, b.V:])
     run_gpu(b, bits, dev, tune={"kernel": 2, "stages": 8})
     assert Gp.grpo_async_last_plan()["kernel"] == 2
