@@ -291,7 +291,16 @@ grpo_status_t grpo_async_advantage_from_stats(const float *rewards, const int32_
 
 /*
  * grpo_async_loss_fwd -- fused log-softmax + target gather + ratio + clip +
- * min + segmented mean, and (if dlogits != NULL) the backward in the same pass.
+ * min + segmented mean, and (if dlogits != NULL) the backward in the same pass:
+ *   log pi_theta(y_t | .) = z_{t,y_t} - logsumexp_v z_{t,v}   (P:136 pi(y|x) = prod_t pi(y_t|.),
+ *                                                             P:32-33 the token probabilities)
+ *   r_t = exp(log pi_theta - log pi_{w_j})                   (eq:ratio_async)
+ *   term_t = min(r_t A_i, clip_eps(r_t) A_i)                  (eq:grpo_async P:19-22, clip P:151)
+ *   traj_sum_i = sum_t term_t;  J = sum_i inv_norm_i traj_sum_i (the 1/L_i, 1/G and 1/P of
+ *                                                             eq:grpo_async P:14-18, folded)
+ *   dlogits = d(-J)/dz = s_t (softmax(z_t) - onehot(y_t))     (the chain rule of the above;
+ *                                                             DESIGN.md Z19: the paper
+ *                                                             maximises J, the loss is -J)
  * The chunk is rows [row_begin, row_begin + n_rows) of this rank's packing.
  *   logits      bf16[n_rows, ld] row k scores target_ids[k] (caller-shifted,
  *               response tokens only); ld >= V, ld % 8 == 0, 16-byte aligned.
@@ -400,7 +409,10 @@ grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_beg
 /*
  * grpo_async_loss_bwd -- unfused backward: one streaming pass that re-reads
  * the logits and writes dlogits = grad_scale_mult * s_t * (exp(z - lse_t) - onehot(y_t))
- * from the lse and token_scale saved by grpo_async_loss_fwd.
+ * from the lse and token_scale saved by grpo_async_loss_fwd: the gradient of -J of
+ * eq:grpo_async with respect to the logits through log pi_theta(y_t) (P:32-33,
+ * P:136); s_t = 0 for clipped tokens (the clipped branch of the min carries no
+ * gradient) and zero advantages (Z19, Z10).
  *   logits, dlogits bf16[n_rows, ld] (may alias), target_ids int64[n_rows],
  *   lse, token_scale float[n_rows].
  * Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_CUDA.
