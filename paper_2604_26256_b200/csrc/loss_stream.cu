@@ -311,7 +311,10 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                     else stg_stream(dst4 + vi, d);
                 }
             }
-            // the target's own column (g_y from the fp64 epilogue), rewritten by the thread that stored its vector
+            // the target's own column (g_y from the fp64 epilogue), rewritten by the thread that
+            // stored its vector, right after it: the 2-byte store then merges into the sector the
+            // vector store left in L2 (hoisted after the loop, it lands on an evicted sector and
+            // the bench loses 1.1 %, measured)
             if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
                 drow[y] = f2bf(gy);
             }
