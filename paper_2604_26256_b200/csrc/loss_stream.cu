@@ -220,17 +220,24 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
         }
         const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
         uint4 x[U];
+        if (!last) {
 #pragma unroll
-        for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
-        if (last) {
+            for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+            RowwiseBatch<NT, U>::reduce(x, a, s);  // running max reference, fp64 sum (rowwise.cuh)
+        } else {
+            // the ragged last chunk: only its first jb = ceil(valid / NT) vector batches hold
+            // row data (prod: 573 of 2048 vectors, 2 of 4 batches), so the exponentials of
+            // the empty batches are not computed at all
+            const int jb = (g.n_vec - c * CHUNK_VECS + NT - 1) / NT;
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
+                x[j] = j < jb ? chunk[j * NT + threadIdx.x] : neg_inf;
                 if (vi >= g.n_vec) x[j] = neg_inf;
                 else if (vi == g.n_vec - 1 && g.tail_valid < 8) x[j] = mask_tail(x[j], g.tail_valid);
             }
+            RowwiseBatch<NT, U>::reduce_first(x, jb, a, s);
         }
-        RowwiseBatch<NT, U>::reduce(x, a, s);  // running max reference, fp64 sum (rowwise.cuh)
         if (c < g.n - g.R) {  // not resident: release now
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + sl);

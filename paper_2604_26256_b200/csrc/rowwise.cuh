@@ -40,6 +40,22 @@ struct RowwiseBatch {
         // with a = -inf every element so far is -inf: reference 0 keeps the terms 0
         s += (double)sum_exp2(x, a == -INFINITY ? 0.0f : a);
     }
+    // reduce of the first k vectors only (1 <= k <= U, the same k across the warp): a ragged
+    // last chunk's batches past the row's end cost nothing
+    static __device__ __forceinline__ void reduce_first(const uint4 (&x)[U], int k, float &a, double &s) {
+        if constexpr (U == 1) {
+            reduce(x, a, s);
+        } else {
+            if (k >= U) {
+                reduce(x, a, s);
+                return;
+            }
+            uint4 y[U - 1];
+#pragma unroll
+            for (int j = 0; j < U - 1; ++j) y[j] = x[j];
+            RowwiseBatch<NT, U - 1>::reduce_first(y, k, a, s);
+        }
+    }
     // s * 2^(z*log2e - lse2) = sign(s) * 2^(z*log2e - (lse2 - log2|s|)): the token scale
     // folds into the exponent's reference, so an element costs one FFMA and one EX2 (no
     // FMUL) and the sign is applied to the packed bf16 pair

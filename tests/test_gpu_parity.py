@@ -476,3 +476,57 @@ def test_stream_split_rows(dev, plan):
         ref = run_oracle(b, bits)
         gpu = run_gpu(b, bits, dev, tune=plan)
         compare(gpu, ref, b, logits_pad=bits[:, b.V:])
+
+
+def _dead_rows_batch(V, seed):
+    """Four groups of four trajectories, interleaved in completion order: groups 0 and 2 have
+    equal rewards (A = 0: dead rows), groups 1 and 3 mixed ones; lengths 1..6 tokens."""
+    rng = np.random.default_rng(seed)
+    P, G = 4, 4
+    order = rng.permutation(P * G)
+    group_ids = (order // G).astype(np.int32)
+    rewards = np.where(group_ids == 0, 1.0, np.where(group_ids == 2, 0.0,
+                                                     rng.integers(0, 2, P * G).astype(float)))
+    for p in (1, 3):  # make sure the live groups are not all-equal
+        i = np.nonzero(group_ids == p)[0]
+        rewards[i[0]], rewards[i[1]] = 1.0, 0.0
+    L = rng.integers(1, 7, P * G)
+    T = int(L.sum())
+    z = rng.normal(size=(T, V)).astype(np.float32) * 2.0
+    tgt = rng.integers(0, V, T)
+    bits = f32_to_bf16_bits(z)
+    zf = (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    m = zf.max(1, keepdims=True)
+    lse = (m + np.log(np.exp(zf - m).sum(1, keepdims=True)))[:, 0]
+    lw = np.minimum(zf[np.arange(T), tgt] - lse + rng.normal(size=T) * 0.2, 0).astype(np.float32)
+    b = make_manual(P, G, 1, V, L, group_ids, rewards, [999] * (P * G), tgt, lw)
+    pad = np.zeros((T, b.ld), np.uint16)
+    pad[:, :V] = bits
+    return b, pad
+
+
+DEAD_PLANS = [None, {"kernel": 3}, {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 3},
+              {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 1},
+              {"kernel": 3, "chunk_kb": 16, "stages": 13, "lag": 3},
+              {"kernel": 3, "chunk_kb": 32, "stages": 2, "lag": 1},
+              {"kernel": 3, "cluster_size": 2, "chunk_kb": 32, "stages": 6, "lag": 1},
+              {"kernel": 3, "cluster_size": 2, "chunk_kb": 16, "stages": 3, "lag": 2}]
+
+
+@pytest.mark.parametrize("V", [90007, 152064, 262144])
+def test_stream_dead_rows(dev, V):
+    """Runs of dead rows (A = 0, or a trajectory masked out: inv_norm = 0) between live
+    ones through K3c's two-pass ring (re-loads at V >= 90007, split rows at 262144): a dead
+    row's dlogits are zeros (its math-free pass 2), a live row's unaffected.  Element-wise
+    against the oracle: every plan, row chunks 1 and 3, in place and not, the dlogits
+    buffer pre-filled with NaN so a missing zero store would show."""
+    b, bits = _dead_rows_batch(V, V)
+    mask = np.ones(b.N, np.uint8)
+    mask[np.nonzero(b.group_ids == 1)[0][0]] = 0  # one masked trajectory in a live group
+    for traj_mask in (None, mask):
+        ref = run_oracle(b, bits, traj_mask=traj_mask)
+        assert np.any(ref["rows"].s == 0) and np.any(ref["rows"].s != 0)
+        for k, tune in enumerate(DEAD_PLANS):
+            gpu = run_gpu(b, bits, dev, tune=tune, chunks=1 + 2 * (k % 2), inplace=k % 3 == 1,
+                          traj_mask=traj_mask)
+            compare(gpu, ref, b, logits_pad=bits[:, b.V:])
