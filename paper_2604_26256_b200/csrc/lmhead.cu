@@ -36,6 +36,7 @@ struct Params {
     int32_t n_rows, V, d;
     int32_t m_tiles, n_vt, vt_per_unit, n_units, group_m;
     int32_t col_offset;  // first vocabulary id of this W shard (tensor-parallel head), else 0
+    int32_t pol_x, pol_w;  // L2 policies of the X / W loads: 0 normal, 1 evict_first, 2 evict_last
     // EPI_STATS
     const RowInfo *rowinfo;
     RowPart *part;  // [n_split][n_rows] log2-domain (max, sum fp64)
@@ -126,7 +127,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            const uint64_t pol_a = policy_evict_last(), pol_b = policy_evict_normal();
+            auto mkpol = [](int c) {
+                return c == 1 ? policy_evict_first() : c == 2 ? policy_evict_last() : policy_evict_normal();
+            };
+            const uint64_t pol_a = mkpol(p.pol_x), pol_b = mkpol(p.pol_w);
             int stage = 0;
             uint32_t phase = 0;
             for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
@@ -504,7 +508,13 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     p.vt_per_unit = lmhead_vt_per_unit(n_rows);
     const int32_t n_split = (p.n_vt + p.vt_per_unit - 1) / p.vt_per_unit;
     p.n_units = p.m_tiles * n_split;
-    p.group_m = 16 / CG;  // 16 x 128 rows of X per raster group (measured: 2-4 pair tiles is worse)
+    // 32 x 128 rows of X per raster group (42 MB at d = 5120), X kept in L2 (evict_last), W
+    // streamed (evict_first): at 8190 x 5120 x 152064 DRAM reads 14.6 GB vs 17.2 GB for 16 x 128
+    // rows with W evict_normal, the launch -3.5 % in the back-to-back loop; 2 and 4 pair tiles
+    // per group, or all 32, are worse (profiles/r02_lmhead_raster.txt)
+    p.group_m = 32 / CG;
+    p.pol_x = 2;
+    p.pol_w = 1;
     p.rowinfo = rowinfo;
     p.part = part;
     p.zy = zy;

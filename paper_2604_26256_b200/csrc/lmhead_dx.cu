@@ -29,21 +29,35 @@ enum { EPI_SLOTS = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_F32_ACC = 3 };
 struct Params {
     int32_t M, N, K;                  // D[M, N] = A[M, K] * B[K, N]
     int32_t m_tiles, n_tiles, n_units;
-    int32_t raster_n;                 // 1: n tile fastest (dW: the small B stays in L2)
+    int32_t raster_n;                 // 0: row-tile groups, 1: column tile fastest, 2: column-tile groups
+    int32_t gm;                       // raster_n = 0: row tiles per raster group
+    int32_t pol_a, pol_b;             // L2 policies of the A / B loads: 0 normal, 1 evict_first, 2 evict_last
     int32_t world, rank, rows_per_rank;
     float *slots[GRPO_VP_MAX_RANKS];  // EPI_SLOTS: slot buffers of every rank [world][rows_per_rank][N]
     void *out;                        // EPI_BF16 / EPI_F32 / EPI_F32_ACC: [M][ldo]
     int64_t ldo;
 };
 
-// Units (m_tile, n_tile).  raster_n = 0: groups of GM row tiles, row tile fastest -- the pairs
+// Units (m_tile, n_tile).  raster_n = 0: groups of p.gm row tiles, row tile fastest -- the pairs
 // running at the same time cover ~GM row tiles x ~grid/GM column tiles and, moving through K
 // at about the same pace, share each A and B k-block in L2 instead of re-reading the long-K
 // operands (dX: K = the vocabulary, tens of MB per row tile) from HBM.  raster_n = 1: column
 // tile fastest -- dW = dz^T X has K = the row count and a small B (X, ~84 MB at 8190 x 5120),
 // so the column tiles of one row tile (one dz column block) run together and dz streams once.
-constexpr int GM = 8;
+// raster_n = 2: groups of p.gm column tiles, column tile fastest inside the group (dW: a group's
+// share of B stays in L2 -- shared operands are cached per die in effect, ~60 MB before they
+// thrash, scripts/probes/l2_probe.cu -- while A streams once per group).
 __device__ __forceinline__ void decode(const Params &p, int unit, int &m_tile, int &n_tile) {
+    const int GM = p.gm;
+    if (p.raster_n == 2) {  // groups of GM column tiles, column tile fastest inside a group
+        const int per_group = GM * p.m_tiles;
+        const int grp = unit / per_group;
+        const int rem = unit - grp * per_group;
+        const int gn = min(GM, p.n_tiles - grp * GM);
+        m_tile = rem / gn;
+        n_tile = grp * GM + (rem - m_tile * gn);
+        return;
+    }
     if (p.raster_n) {
         m_tile = unit / p.n_tiles;
         n_tile = unit - m_tile * p.n_tiles;
@@ -140,7 +154,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ---- TMA producer
-            const uint64_t pol = policy_evict_normal();
+            auto mkpol = [](int c) {
+                return c == 1 ? policy_evict_first() : c == 2 ? policy_evict_last() : policy_evict_normal();
+            };
+            const uint64_t pol_a = mkpol(p.pol_a), pol_b = mkpol(p.pol_b);
             int stage = 0;
             uint32_t phase = 0;
             for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
@@ -155,25 +172,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     if (CG == 1) {
                         mbar_arrive_expect_tx(full + stage, STAGE);
                         if (A_MN) {
-                            tc::tma_load_2d(dA, &tmA, a_row, kb * BK, full + stage, pol);
-                            tc::tma_load_2d(dA + ATOM, &tmA, a_row + 64, kb * BK, full + stage, pol);
+                            tc::tma_load_2d(dA, &tmA, a_row, kb * BK, full + stage, pol_a);
+                            tc::tma_load_2d(dA + ATOM, &tmA, a_row + 64, kb * BK, full + stage, pol_a);
                         } else {
-                            tc::tma_load_2d(dA, &tmA, kb * BK, a_row, full + stage, pol);
+                            tc::tma_load_2d(dA, &tmA, kb * BK, a_row, full + stage, pol_a);
                         }
 #pragma unroll
                         for (int j = 0; j < NB; ++j)
-                            tc::tma_load_2d(dB + j * ATOM, &tmB, b_col + j * 64, kb * BK, full + stage, pol);
+                            tc::tma_load_2d(dB + j * ATOM, &tmB, b_col + j * 64, kb * BK, full + stage, pol_b);
                     } else {
                         if (crank == 0) mbar_arrive_expect_tx(full + stage, 2 * STAGE);
                         if (A_MN) {
-                            tc::tma_load_2d_pair(dA, &tmA, a_row, kb * BK, full + stage, pol);
-                            tc::tma_load_2d_pair(dA + ATOM, &tmA, a_row + 64, kb * BK, full + stage, pol);
+                            tc::tma_load_2d_pair(dA, &tmA, a_row, kb * BK, full + stage, pol_a);
+                            tc::tma_load_2d_pair(dA + ATOM, &tmA, a_row + 64, kb * BK, full + stage, pol_a);
                         } else {
-                            tc::tma_load_2d_pair(dA, &tmA, kb * BK, a_row, full + stage, pol);
+                            tc::tma_load_2d_pair(dA, &tmA, kb * BK, a_row, full + stage, pol_a);
                         }
 #pragma unroll
                         for (int j = 0; j < NB; ++j)
-                            tc::tma_load_2d_pair(dB + j * ATOM, &tmB, b_col + j * 64, kb * BK, full + stage, pol);
+                            tc::tma_load_2d_pair(dB + j * ATOM, &tmB, b_col + j * 64, kb * BK, full + stage, pol_b);
                     }
                     if (++stage == NS) {
                         stage = 0;
@@ -366,6 +383,7 @@ namespace lmdx {
 template <bool A_MN, int BN, int CG, int EPI>
 static cudaError_t launch_gemm(const CUtensorMap &ma, const CUtensorMap &mb, const CUtensorMap &mo, Params &p,
                                cudaStream_t s) {
+    if (p.gm <= 0) p.gm = 8;
     constexpr int NB = BN / 64 / CG;
     constexpr int NS = CG == 1 ? STAGES : 6;  // 6 x 32 KB + 32 KB of staging fits in 227 KB
     constexpr int SMEM = NS * (BM * BK * 2 + NB * BK * 64 * 2) + Epi<EPI, CG>::STAGING + 1024 + 256;
@@ -439,6 +457,8 @@ cudaError_t launch_lmhead_dx(const uint16_t *dz, int64_t ld_dz, const uint16_t *
     p.world = world;
     p.rank = rank;
     p.rows_per_rank = (int32_t)((n_rows + world - 1) / world);
+    p.gm = 16;    // as launch_lmhead_gemm_dx
+    p.pol_a = 1;
     for (int q = 0; q < world; ++q) p.slots[q] = slots[q];
     cudaError_t e = d % 256 == 0 ? launch_gemm<false, 256, 2, EPI_SLOTS>(ma, mb, ma, p, s)
                                  : launch_gemm<false, 128, 2, EPI_SLOTS>(ma, mb, ma, p, s);
@@ -463,6 +483,10 @@ cudaError_t launch_lmhead_gemm_dx(const uint16_t *dz, int64_t ld_dz, const uint1
     p.M = (int32_t)n_rows;
     p.N = d;
     p.K = V;
+    // 16 pair tiles of rows per raster group, dz streamed (evict_first): back-to-back 9.9 vs
+    // 10.3 ms at 8190 x 5120 x 152064 for 8 and evict_normal (profiles/r02_lmhead_raster.txt)
+    p.gm = 16;
+    p.pol_a = 1;
     p.out = out;
     p.ldo = d;
     const cudaError_t e = out_bf16 ? launch_by_n<false, EPI_BF16>(ma, mb, mo, p, s)
@@ -489,7 +513,11 @@ cudaError_t launch_lmhead_gemm_dw(const uint16_t *dz, int64_t ld_dz, const uint1
     p.M = V;
     p.N = d;
     p.K = (int32_t)n_rows;
-    p.raster_n = 1;
+    // groups of 10 column tiles (half of X, 42 MB at 8190 x 5120: it stays in L2 while the
+    // group's dz blocks stream twice), column tile fastest: DRAM reads 21 vs 27 GB for the
+    // whole of X per row tile, back-to-back 10.3 vs 10.5 ms (profiles/r02_lmhead_raster.txt)
+    p.raster_n = 2;
+    p.gm = 10;
     p.out = dW;
     p.ldo = d;
     const cudaError_t e = launch_by_n<true, EPI_F32_ACC>(ma, mb, mo, p, s);
