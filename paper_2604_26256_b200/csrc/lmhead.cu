@@ -20,12 +20,14 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "sched.cuh"
 #include "tc.cuh"
 
 namespace grpo {
 namespace lm {
 
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+__device__ int32_t g_units[sched::N_COUNTERS];  // unit counters of the launches (sched.cuh)
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int NUM_THREADS = 192;
 constexpr uint32_t TMEM_COLS = 2 * BN;
@@ -37,6 +39,7 @@ struct Params {
     int32_t m_tiles, n_vt, vt_per_unit, n_units, group_m;
     int32_t col_offset;  // first vocabulary id of this W shard (tensor-parallel head), else 0
     int32_t pol_x, pol_w;  // L2 policies of the X / W loads: 0 normal, 1 evict_first, 2 evict_last
+    int32_t *counter;      // the launch's unit counter, 0 at launch (sched.cuh)
     // EPI_STATS
     const RowInfo *rowinfo;
     RowPart *part;  // [n_split][n_rows] log2-domain (max, sum fp64)
@@ -94,11 +97,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * GG::STAGE + (EPI == EPI_STATS ? 0 : GG::STAGING));
     uint64_t *full = bars, *empty = bars + NS, *tfull = bars + 2 * NS, *tempty = bars + 2 * NS + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 4);
+    sched::Queue *uq = reinterpret_cast<sched::Queue *>(bars + 2 * NS + 6);  // dynamic units (sched.cuh)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = p.d / BK;
     const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;        // 0 = the pair's leader
-    const int cta_id = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
-    const int n_ctas = CG == 2 ? (int)ncluster_x() : (int)gridDim.x;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 128 * CG);  // every epilogue thread of the pair
         }
+        sched::init<CG>(uq);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tc::prefetch_tmap(&tmX);
         tc::prefetch_tmap(&tmW);
@@ -133,7 +136,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t pol_a = mkpol(p.pol_x), pol_b = mkpol(p.pol_w);
             int stage = 0;
             uint32_t phase = 0;
-            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+            for (int i = 0;; ++i) {
+                const int unit = crank == 0 ? sched::fetch<CG>(uq, i, p.counter, p.n_units)
+                                            : sched::next<CG>(uq, i, crank);
+                if (unit < 0) break;
                 int m_tile, split;
                 decode(p, unit, m_tile, split);
                 const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
@@ -166,7 +172,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             constexpr uint32_t idesc = tc::idesc_bf16_f32(BM * CG, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+            for (int i = 0;; ++i) {
+                const int unit = sched::next<CG>(uq, i, 0u);
+                if (unit < 0) break;
                 int m_tile, split;
                 decode(p, unit, m_tile, split);
                 const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
@@ -206,7 +214,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int n_boxes = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+        for (int i = 0;; ++i) {
+            int unit = 0;
+            if (lane == 0) unit = sched::next<CG>(uq, i, crank);
+            unit = __shfl_sync(0xffffffffu, unit, 0);
+            if (unit < 0) break;
             int m_tile, split;
             decode(p, unit, m_tile, split);
             const int vt0 = split * p.vt_per_unit, vt1 = min(vt0 + p.vt_per_unit, p.n_vt);
@@ -525,6 +537,12 @@ cudaError_t launch_lmhead(int epi, const void *X, const void *W, int64_t n_rows,
     p.scale = scale;
     p.mult = mult;
     p.col_offset = col_offset;
+    {
+        int32_t *base = nullptr;
+        cudaError_t ec = cudaGetSymbolAddress(reinterpret_cast<void **>(&base), g_units);
+        if (ec == cudaSuccess) ec = sched::take_counter(base, s, &p.counter);
+        if (ec != cudaSuccess) return ec;
+    }
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);

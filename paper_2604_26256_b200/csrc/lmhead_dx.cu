@@ -15,12 +15,14 @@
 #include <cstdio>
 
 #include "common.cuh"
+#include "sched.cuh"
 #include "tc.cuh"
 
 namespace grpo {
 namespace lmdx {
 
 constexpr int BM = 128, BK = 64, STAGES = 4, NUM_THREADS = 192;
+__device__ int32_t g_units[sched::N_COUNTERS];  // unit counters of the launches (sched.cuh)
 
 // Epilogues: EPI_SLOTS stores f32 tiles into the owner rank's slot (the tensor-parallel
 // dX reduce-scatter); EPI_BF16 / EPI_F32 store D; EPI_F32_ACC adds D into an f32 array.
@@ -32,6 +34,7 @@ struct Params {
     int32_t raster_n;                 // 0: row-tile groups, 1: column tile fastest, 2: column-tile groups
     int32_t gm;                       // raster_n = 0: row tiles per raster group
     int32_t pol_a, pol_b;             // L2 policies of the A / B loads: 0 normal, 1 evict_first, 2 evict_last
+    int32_t *counter;                 // the launch's unit counter, 0 at launch (sched.cuh)
     int32_t world, rank, rows_per_rank;
     float *slots[GRPO_VP_MAX_RANKS];  // EPI_SLOTS: slot buffers of every rank [world][rows_per_rank][N]
     void *out;                        // EPI_BF16 / EPI_F32 / EPI_F32_ACC: [M][ldo]
@@ -122,11 +125,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NS * STAGE + Epi<EPI, CG>::STAGING);
     uint64_t *full = bars, *empty = bars + NS, *tfull = bars + 2 * NS, *tempty = bars + 2 * NS + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 4);
+    sched::Queue *uq = reinterpret_cast<sched::Queue *>(bars + 2 * NS + 6);  // dynamic units (sched.cuh)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (p.K + BK - 1) / BK;
     const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;
-    const int cta_id = CG == 2 ? (int)cluster_id_x() : (int)blockIdx.x;
-    const int n_ctas = CG == 2 ? (int)ncluster_x() : (int)gridDim.x;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 128 * CG);
         }
+        sched::init<CG>(uq);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         tc::prefetch_tmap(&tmA);
         tc::prefetch_tmap(&tmB);
@@ -160,7 +163,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t pol_a = mkpol(p.pol_a), pol_b = mkpol(p.pol_b);
             int stage = 0;
             uint32_t phase = 0;
-            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+            for (int i = 0;; ++i) {
+                const int unit = crank == 0 ? sched::fetch<CG>(uq, i, p.counter, p.n_units)
+                                            : sched::next<CG>(uq, i, crank);
+                if (unit < 0) break;
                 int m_tile, n_tile;
                 decode(p, unit, m_tile, n_tile);
                 const int a_row = m_tile * BM * CG + (int)crank * BM;
@@ -204,7 +210,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             constexpr uint32_t idesc = idesc_b_mn(BM * CG, BN, A_MN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+            for (int i = 0;; ++i) {
+                const int unit = sched::next<CG>(uq, i, 0u);
+                if (unit < 0) break;
                 mbar_wait(tempty + acc, acc_phase ^ 1u);
                 tc::fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -241,7 +249,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int n_boxes = 0;                     // boxes this warp has handed to TMA
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int unit = cta_id; unit < p.n_units; unit += n_ctas) {
+        for (int i = 0;; ++i) {
+            int unit = 0;
+            if (lane == 0) unit = sched::next<CG>(uq, i, crank);
+            unit = __shfl_sync(0xffffffffu, unit, 0);
+            if (unit < 0) break;
             int m_tile, n_tile;
             decode(p, unit, m_tile, n_tile);
             const int row0 = m_tile * BM * CG + (int)crank * BM;  // first row of this CTA's 128
@@ -390,6 +402,12 @@ static cudaError_t launch_gemm(const CUtensorMap &ma, const CUtensorMap &mb, con
     p.m_tiles = (p.M + BM * CG - 1) / (BM * CG);
     p.n_tiles = p.N / BN;
     p.n_units = p.m_tiles * p.n_tiles;
+    if (p.raster_n) {  // dW (K = the row count): dynamic units; dX (K = V): static (sched.cuh)
+        int32_t *base = nullptr;
+        cudaError_t ec = cudaGetSymbolAddress(reinterpret_cast<void **>(&base), g_units);
+        if (ec == cudaSuccess) ec = sched::take_counter(base, s, &p.counter);
+        if (ec != cudaSuccess) return ec;
+    }
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
