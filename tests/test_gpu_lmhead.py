@@ -333,3 +333,33 @@ def test_lmhead_random_shapes(dev, seed, cta_group):
     ref = O.run_batch_lmhead(b, X, W, std_floor=float(np.float32(1e-8)))
     gpu = run_gpu_lmhead(b, X, W, dev, chunks=int(rng.integers(1, 4)))
     _check(gpu, ref, b, X, W)
+
+
+def test_lmhead_dynamic_units_concurrent_streams(dev):
+    """The dynamic unit counters (csrc/sched.cuh): 96 LM-head GEMM launches -- logits (forward
+    kernel) and dW (gemm_kernel) -- spread over four streams at once, more launches than the
+    64 counter slots, each result bit-identical to the same launch run alone.  A counter
+    shared by two running launches or not zeroed would drop or repeat units."""
+    n, d, V = 700, 128, 3001
+    rng = np.random.default_rng(7)
+    from synth.gen import f32_to_bf16_bits
+    X = to_dev_bits(f32_to_bf16_bits(rng.standard_normal((n, d), dtype=np.float32)), dev).view(torch.bfloat16)
+    W = to_dev_bits(f32_to_bf16_bits(rng.standard_normal((V, d), dtype=np.float32) * np.float32(0.2)),
+                    dev).view(torch.bfloat16)
+    ld = (V + 7) // 8 * 8
+    ref = torch.empty((n, ld), dtype=torch.bfloat16, device=dev)
+    L.grpo_async_lmhead_logits(X, W, n, d, V, ref, ld)
+    dW_ref = torch.zeros((V, d), dtype=torch.float32, device=dev)
+    L.grpo_async_lmhead_dw(X, n, d, V, ref, ld, dW_ref)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(device=dev) for _ in range(4)]
+    outs = [torch.empty((n, ld), dtype=torch.bfloat16, device=dev) for _ in range(48)]
+    dws = [torch.zeros((V, d), dtype=torch.float32, device=dev) for _ in range(48)]
+    for k in range(48):
+        s = streams[k % 4]
+        L.grpo_async_lmhead_logits(X, W, n, d, V, outs[k], ld, stream=s)
+        L.grpo_async_lmhead_dw(X, n, d, V, ref, ld, dws[k], stream=s)
+    torch.cuda.synchronize()
+    for k in range(48):
+        assert torch.equal(outs[k][:, :V], ref[:, :V]), k
+        assert torch.equal(dws[k], dW_ref), k
