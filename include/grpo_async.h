@@ -359,8 +359,11 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
  * The per-row logsumexp needs all R shards: the kernel exchanges one 32-byte partial
  * per row and rank through peer memory (NVLink P2P stores of 64-bit words tagged with
  * the call's epoch) inside the loss kernel, then writes this rank's slice of dlogits.
- * Shards of >= 60000 columns with lag 0 and static rows run the streamed ring kernel
- * (plan kernel 8), others the row-wise one (plan kernel 7); same results.  Every
+ * With lag 0 and static rows, shards of >= 90000 columns run the streamed ring kernel
+ * (plan kernel 8), shards of 16384..89999 columns the ring kernel with pass 2 delayed by
+ * one row (plan kernel 9), narrower shards or lag 1 / dynamic rows the row-wise kernel
+ * (plan kernel 7); lag 2..4 forces kernel 9 with pass 2 delayed by lag - 1 rows; same
+ * results.  Every
  * rank computes identical per-row outputs, traj_sum and stats (no further reduction).
  * comm describes the group (host struct of device pointers):
  *   world R <= GRPO_VP_MAX_RANKS; the call computes ranks [rank_begin, rank_begin+n_local)
@@ -389,8 +392,11 @@ typedef struct {
     uint16_t *dlogits[GRPO_VP_MAX_RANKS];
     void *xbuf[GRPO_VP_MAX_RANKS];
     uint32_t epoch;
-    int32_t lag;          /* 0 (default): wait for a row's partials right after its pass 1; */
-                          /* 1: after pass 1 of the next row (same results, bit for bit)     */
+    int32_t lag;          /* 0 (default): the plan by shard width (see above);              */
+                          /* 1: row-wise, wait after pass 1 of the next row (same results);  */
+                          /* 2..4: the streamed ring kernel with pass 2 of row k run after   */
+                          /* pass 1 of row k + lag - 1, the row re-read from L2 (plan kernel */
+                          /* 9; static rows only; same results); else GRPO_ERR_INVALID_ARG   */
     int32_t dynamic_rows; /* 0 (default): CTA g takes rows g, g + grid, ...; 1: CTAs take     */
                           /* rows in the order they ask for them (same results)             */
 } grpo_vp_comm_t;
@@ -553,7 +559,8 @@ grpo_status_t grpo_async_lmhead_logits(const uint16_t *hidden, const uint16_t *W
 typedef struct {
     int32_t kernel;        /* 1 cluster-resident, 2 row-wise, 3 streamed ring, 4/5/6 LM-head */
                            /* (tcgen05) loss partials / logits gradient / logits, 7 vocab-  */
-                           /* parallel row-wise, 8 vocab-parallel streamed ring              */
+                           /* parallel row-wise, 8 vocab-parallel streamed ring, 9 the same  */
+                           /* with pass 2 delayed by lag - 1 rows                            */
     int32_t cluster_size;  /* CTAs per row (kernel 1); CTAs per MMA (4-6)                     */
     int32_t ctas_per_sm;   /* requested residency                                            */
     int32_t stages;        /* kernel 1: row stages per CTA; 2: cached vectors per thread;   */
@@ -565,7 +572,8 @@ typedef struct {
                            /* occupancy query allows; 4-6: work units                        */
     int32_t smem_bytes;    /* dynamic shared memory per CTA                                  */
     int32_t lag;           /* kernel 1: reduction-to-backward lag in rows; 3: free ring     */
-                           /* slots at the end of pass 1 (also 8); 7: deferred exchange wait */
+                           /* slots at the end of pass 1 (also 8); 7: deferred exchange wait; */
+                           /* 9: grpo_vp_comm_t.lag (pass 2 after lag - 1 further rows)      */
 } grpo_plan_t;
 
 grpo_status_t grpo_async_last_plan(grpo_plan_t *out);

@@ -528,6 +528,9 @@ grpo_status_t grpo_async_loss_fwd_vp(const grpo_vp_comm_t *comm, int64_t row_beg
                     comm->shard_cols, V);
     if (n_rows < 0 || N <= 0 || V <= 0 || row_begin < 0)
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: n_rows/N/V/row_begin");
+    if (comm->lag < 0 || comm->lag > 4 || (comm->lag >= 2 && comm->dynamic_rows))
+        return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: lag=%d (0..4; 2..4 with static rows only)",
+                    comm->lag);
     if (comm->slots < n_rows)
         return fail(GRPO_ERR_INVALID_ARG, "loss_fwd_vp: n_rows=%lld > comm->slots=%lld",
                     (long long)n_rows, (long long)comm->slots);

@@ -565,6 +565,319 @@ __global__ void __launch_bounds__(NT + 64, MINB) vp_stream_kernel(const VpParams
     }
 }
 
+// The ring kernel with the pass 2 of every row DELAYED by D rows (grpo_vp_comm_t.lag = D + 1,
+// D = 1..3): the consumers run pass 1 of row k, post its warp partials and then pass 2 of row
+// k - D, so the exchange of a row -- posting its partial, waiting for the slowest peer rank --
+// runs in the epilogue warp under D rows of streaming instead of under a look-ahead of one
+// chunk.  No chunk stays resident: pass 1 streams row k with L2 evict_last and pass 2
+// re-loads row k - D (evict_first), which (D + 1) x 74 KB x 296 CTAs (R = 4 at V = 152064;
+// 44 MB at D = 1) keeps in L2.  The producer's order is P1(0) .. P1(D-1), then P1(k), RL(k-D)
+// for k >= D, then the last D re-loads; the row partials, token scales and their mbarriers
+// are rings of NB = D + 1 (row k uses buffer k mod NB; the consumers' pass 2 of row k-D
+// precedes their partial of row k+1, and the epilogue warp handles rows in order, so a
+// buffer is free again when it is rewritten).  Same combine order: bit-identical outputs.
+template <int NT, int MINB, int CHUNK_VECS>
+__global__ void __launch_bounds__(NT + 64, MINB) vp_delay_kernel(const VpParams p, const int ns, const int D) {
+    constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
+    constexpr int U = CHUNK_VECS / NT;
+    constexpr int NW = NT / 32;
+    constexpr int NBMAX = 4;
+    using B = RowwiseBatch<NT, U>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint4 *ring = reinterpret_cast<uint4 *>(smem);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)ns * CHUNK_BYTES);
+    uint64_t *empty = full + ns;
+    __shared__ RowPart red[NBMAX][NW];
+    __shared__ float4 scal[NBMAX];
+    __shared__ __align__(8) uint64_t part_bar[NBMAX];
+    __shared__ __align__(8) uint64_t scal_bar[NBMAX];
+    const int NB = D + 1;
+    const int g_per = gridDim.x / p.n_local;
+    const int lr = blockIdx.x / g_per;  // local rank of this CTA
+    const int g = blockIdx.x - lr * g_per;
+    const int rank = p.rank_begin + lr;
+    const int32_t c0 = rank * p.shard_cols;  // first vocabulary column of this shard
+    const int32_t vc = max(0, min(p.shard_cols, p.V - c0));
+    const int n_vec = (vc + 7) / 8;
+    const int n = (n_vec + CHUNK_VECS - 1) / CHUNK_VECS;  // chunks per row
+    const uint16_t *shard = p.logits[lr];
+    uint16_t *dshard = p.dlogits[lr];
+    const bool two_pass = dshard != nullptr;
+    const int tail_valid = vc - (n_vec - 1) * 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n_mine = g < p.n_rows ? (p.n_rows - g + g_per - 1) / g_per : 0;  // rows of this CTA
+    auto row_of = [&](int64_t k) { return (int64_t)g + k * g_per; };
+
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < ns; ++q) {
+            mbar_init(full + q, 1);
+            mbar_init(empty + q, NW);
+        }
+        for (int b = 0; b < NB; ++b) {
+            mbar_init(part_bar + b, NW);
+            mbar_init(scal_bar + b, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NW) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0 && n > 0) {
+            const uint64_t pol_keep = policy_evict_last(), pol_once = policy_evict_first();
+            const int64_t row_bytes = (int64_t)n_vec * 16;
+            int slot = 0;
+            uint32_t par = 0;
+            auto load_row = [&](int64_t row, uint64_t pol) {
+                const uint8_t *src = reinterpret_cast<const uint8_t *>(shard + row * p.ld);
+                for (int c = 0; c < n; ++c) {
+                    mbar_wait_sleep(empty + slot, par ^ 1u, 64);
+                    const int64_t off = (int64_t)c * CHUNK_BYTES;
+                    const uint32_t bytes = (uint32_t)(row_bytes - off < CHUNK_BYTES ? row_bytes - off : CHUNK_BYTES);
+                    mbar_arrive_expect_tx(full + slot, bytes);
+                    bulk_g2s(ring + (size_t)slot * CHUNK_VECS, src + off, bytes, full + slot, pol);
+                    if (++slot == ns) {
+                        slot = 0;
+                        par ^= 1u;
+                    }
+                }
+            };
+            for (int64_t k = 0; k < n_mine; ++k) {
+                load_row(row_of(k), two_pass ? pol_keep : pol_once);
+                if (two_pass && k >= D) load_row(row_of(k - D), pol_once);
+            }
+            if (two_pass)
+                for (int64_t k = (n_mine > D ? n_mine - D : (int64_t)0); k < n_mine; ++k) load_row(row_of(k), pol_once);
+        }
+        return;
+    }
+
+    if (warp == NW + 1) {
+        // ------------------------------------------------------------ epilogue warp
+        for (int64_t k = 0; k < n_mine; ++k) {
+            const int64_t row = row_of(k);
+            const int b = (int)(k % NB);
+            const uint32_t ph = (uint32_t)(k / NB) & 1u;
+            RowInfo ri;
+            uint16_t zy_bits = 0;
+            int32_t y_loc = -1;
+            bool mine = false;
+            if (lane == 0) {
+                ri = p.rowinfo[row];
+                y_loc = ri.target - c0;
+                mine = ri.target >= 0 && ri.target < p.V && y_loc >= 0 && y_loc < vc;
+                if (mine) zy_bits = shard[row * p.ld + y_loc];
+            }
+            if (n > 0) mbar_wait_sleep(part_bar + b, ph, 128);
+            float cm = (n > 0 && lane < NW) ? red[b][lane].a : -INFINITY;
+            double cs = (n > 0 && lane < NW) ? red[b][lane].s : 0.0;
+            warp_lse2_combine(cm, cs);
+            const bool own_y = __shfl_sync(0xFFFFFFFFu, mine, 0);
+            const float zy = own_y ? __uint_as_float(((uint32_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)zy_bits, 0)) << 16)
+                                   : 0.0f;
+            // ---- the exchange (tagged 64-bit words, see vp_kernel)
+            if (lane < p.world) {
+                const uint64_t hi = (uint64_t)p.tag << 32;
+                ulonglong2 *dst = p.xbuf[lane] + ((p.half + row) * p.world + rank) * 2;
+                const uint64_t sb = (uint64_t)__double_as_longlong(cs) | (own_y ? (1ull << 63) : 0ull);
+                st_relaxed_sys_v2(dst, hi | __float_as_uint(cm), hi | (uint32_t)sb);
+                st_relaxed_sys_v2(dst + 1, hi | (uint32_t)(sb >> 32), hi | __float_as_uint(zy));
+            }
+            float M = -INFINITY, zsrc = 0.0f;
+            double S = 0.0;
+            bool own = false;
+            if (lane < p.world) {
+                const ulonglong2 *src = p.xbuf[rank] + ((p.half + row) * p.world + lane) * 2;
+                ulonglong2 w0, w1;
+                long long spins = 0;
+                for (;;) {
+                    w0 = ld_relaxed_sys_v2(src);
+                    w1 = ld_relaxed_sys_v2(src + 1);
+                    if ((uint32_t)(w0.x >> 32) == p.tag && (uint32_t)(w0.y >> 32) == p.tag &&
+                        (uint32_t)(w1.x >> 32) == p.tag && (uint32_t)(w1.y >> 32) == p.tag)
+                        break;
+                    __nanosleep(32);
+                    if (++spins > (1ll << 27)) __trap();  // a peer never arrived: fail, don't hang
+                }
+                const uint64_t sb = ((w1.x & 0xFFFFFFFFull) << 32) | (w0.y & 0xFFFFFFFFull);
+                M = __uint_as_float((uint32_t)w0.x);
+                S = __longlong_as_double((long long)(sb & ~(1ull << 63)));
+                own = (sb >> 63) != 0ull;
+                zsrc = __uint_as_float((uint32_t)w1.y);
+            }
+            warp_lse2_combine(M, S);  // same inputs in the same lanes on every rank
+            const uint32_t own_mask = __ballot_sync(0xFFFFFFFFu, own);
+            const float zsh = __shfl_sync(0xFFFFFFFFu, zsrc, own_mask ? __ffs(own_mask) - 1 : 0);
+            if (lane == 0) {
+                const float zyv = own_mask != 0u ? zsh : __int_as_float(0x7FC00000);
+                const double l2s = row_l2s(S, M);
+                const float lse2 = M + (float)l2s;
+                const double logp_d = row_logp(zyv, M, l2s);
+                const RowOut o = row_epilogue(logp_d, ri, p.eps_lo, p.eps_hi, p.grad_scale);
+                if (lr == 0) {  // per-row outputs: identical on every rank, written once per call
+                    const float logp = (float)logp_d;
+                    if (p.logp_out) p.logp_out[row] = logp;
+                    if (p.lse_out) p.lse_out[row] = lse2 * kLn2;
+                    if (p.scale_out) p.scale_out[row] = o.s;
+                    p.term_ws[row] = o.term;
+                    p.logp_ws[row] = logp;
+                    p.flag_ws[row] = o.flags;
+                }
+                scal[b] = make_float4(lse2, o.s, o.gy, __int_as_float(mine ? y_loc : -1));
+                mbar_arrive(scal_bar + b);
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    const uint4 neg_inf = make_uint4(kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair, kBf16NegInfPair);
+    int slot = 0;
+    uint32_t par = 0;
+    auto take = [&]() {
+        const int sl = slot;
+        mbar_wait(full + sl, par);
+        if (++slot == ns) {
+            slot = 0;
+            par ^= 1u;
+        }
+        return sl;
+    };
+    auto release = [&](int sl) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + sl);
+    };
+    auto pass1 = [&](int64_t k) {
+        float a = -INFINITY;
+        double s = 0.0;
+        for (int c = 0; c < n; ++c) {
+            const int sl = take();
+            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            uint4 x[U];
+#pragma unroll
+            for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+            if (c == n - 1) {
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int vi = c * CHUNK_VECS + j * NT + threadIdx.x;
+                    if (vi >= n_vec) x[j] = neg_inf;
+                    else if (vi == n_vec - 1 && tail_valid < 8) x[j] = mask_tail(x[j], tail_valid);
+                }
+                B::reduce_first(x, (n_vec - c * CHUNK_VECS + NT - 1) / NT, a, s);
+            } else {
+                B::reduce(x, a, s);
+            }
+            release(sl);
+        }
+        warp_lse2_combine(a, s);
+        const int b = (int)(k % NB);
+        // the epilogue warp has read red[b] for row k - NB (pass 2 of row k - NB waited for
+        // it when two_pass; forward-only waits here)
+        if (!two_pass && k >= NB) mbar_wait(scal_bar + b, (uint32_t)((k - NB) / NB) & 1u);
+        if (lane == 0 && n > 0) {
+            red[b][warp] = RowPart{a, 0.0f, s};
+            mbar_arrive(part_bar + b);
+        }
+    };
+    auto pass2 = [&](int64_t k) {
+        const int64_t row = row_of(k);
+        const int b = (int)(k % NB);
+        mbar_wait(scal_bar + b, (uint32_t)(k / NB) & 1u);
+        const float4 sc4 = scal[b];
+        const float lse2 = sc4.x, sc = sc4.y, gy = sc4.z;
+        const auto gref = B::grad_ref(sc, lse2);
+        const int32_t y = __float_as_int(sc4.w);
+        const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
+        uint16_t *drow = dshard + row * p.ld;
+        uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
+        for (int c = 0; c < n; ++c) {
+            const int sl = take();
+            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            const int v0 = c * CHUNK_VECS + threadIdx.x;
+            if (c != n - 1) {
+                if (sc == 0.0f) {
+#pragma unroll
+                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, make_uint4(0u, 0u, 0u, 0u));
+                } else {
+                    uint4 x[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad_scaled(x[j], gref));
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int vi = v0 + j * NT;
+                    if (vi >= n_vec) break;
+                    const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
+                                               : B::grad_scaled(chunk[j * NT + threadIdx.x], gref);
+                    if (vi == n_vec - 1 && tail_valid < 8) store_tail(drow + (int64_t)vi * 8, d, tail_valid);
+                    else stg_stream(dst4 + vi, d);
+                }
+            }
+            if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
+                drow[y] = f2bf(gy);
+            }
+            release(sl);
+        }
+    };
+    for (int64_t k = 0; k < n_mine; ++k) {
+        pass1(k);
+        if (two_pass && k >= D) pass2(k - D);
+    }
+    if (two_pass)
+        for (int64_t k = (n_mine > D ? n_mine - D : (int64_t)0); k < n_mine; ++k) pass2(k);
+}
+
+template <int NT, int MINB, int CV>
+static cudaError_t launch_vp_delay(VpParams p, const grpo_vp_comm_t *comm, int ns, int D, int64_t n_rows,
+                                   cudaStream_t s, int *launches, grpo_plan_t *plan, char *why,
+                                   size_t why_len) {
+    const size_t smem = (size_t)ns * CV * 16 + 2 * (size_t)ns * 8;
+    auto kern = vp_delay_kernel<NT, MINB, CV>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, n_sm = 148, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 64, smem);
+    if (e != cudaSuccess) return e;
+    // every CTA must be resident (a CTA may wait for a peer rank's CTA of the same index)
+    int64_t g_per = (int64_t)n_sm * (occ < MINB ? occ : MINB) / comm->n_local;
+    if (g_per > n_rows) g_per = n_rows;
+    if (g_per < 1) {
+        if (why) snprintf(why, why_len, "vp delay kernel: no resident CTA per local rank");
+        return cudaErrorInvalidConfiguration;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.gridDim = dim3((unsigned)(g_per * comm->n_local));
+    cfg.blockDim = dim3(NT + 64);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p, ns, D);
+    if (e != cudaSuccess) return e;
+    if (plan) {
+        *plan = grpo_plan_t{};
+        plan->kernel = 9;
+        plan->ctas_per_sm = MINB;
+        plan->grid = (int32_t)(g_per * comm->n_local);
+        plan->vec_per_thread = NT;
+        plan->stages = ns;
+        plan->max_clusters = occ;
+        plan->smem_bytes = (int32_t)smem;
+        plan->lag = D + 1;
+    }
+    *launches += 1;
+    return cudaSuccess;
+}
+
 template <int NT, int MINB, int CV>
 static cudaError_t launch_vp_stream(VpParams p, const grpo_vp_comm_t *comm, int ns, int pf,
                                     int64_t n_rows, cudaStream_t s, int *launches, grpo_plan_t *plan,
@@ -670,7 +983,7 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned lo
                       cudaStream_t s, int *launches,
                       grpo_plan_t *plan, char *why, size_t why_len) {
     if (a.n_rows == 0) return cudaSuccess;
-    const int lag = comm->lag ? 1 : 0;
+    const int lag = comm->lag ? 1 : 0;  // (lag >= 2: the ring kernel with pass 2 delayed by lag - 1 rows)
     VpParams p = {};
     p.world = comm->world;
     p.rank_begin = comm->rank_begin;
@@ -699,15 +1012,28 @@ cudaError_t launch_vp(const LossArgs &a, const grpo_vp_comm_t *comm, unsigned lo
     p.logp_ws = a.logp_ws;
     p.flag_ws = a.flag_ws;
     const int n_vec = (comm->shard_cols + 7) / 8;
-    // long shards (>= 60000 columns), default schedule: the streamed ring kernel with the
-    // loss_fwd auto plan's geometry for that row length (api.cu).  On shorter shards the
-    // per-row wait for the peers' partials is a larger share of the row and the row-wise
-    // kernel is faster (R = 2 x 76032: 3.64 vs 4.0-4.2 ms; R = 4 x 38016: 2.28 vs 2.09-2.18,
-    // DESIGN.md section 9.1)
+    if (comm->lag >= 2) {  // pass 2 delayed by lag - 1 rows (vp_delay_kernel), ring geometry by row length
+        const int D = comm->lag - 1;
+        if (n_vec >= 7500)  // one CTA per SM: (D + 1) rows x 148 CTAs stay in L2 for rows >= 120 KB
+            return launch_vp_delay<512, 1, 2048>(p, comm, 6, D, a.n_rows, s, launches, plan, why, why_len);
+        return launch_vp_delay<256, 2, 1024>(p, comm, 6, D, a.n_rows, s, launches, plan, why, why_len);
+    }
+    // long shards (>= 90000 columns), default schedule: the streamed ring kernel with the
+    // loss_fwd auto plan's geometry for that row length (api.cu); two such rows per SM would
+    // not stay in L2 for a delayed pass 2
     if (!lag && !comm->dynamic_rows && n_vec >= 11250)
         return launch_vp_stream<512, 1, 2048>(p, comm, 6, 3, a.n_rows, s, launches, plan, why, why_len);
+    // shards of 16384 .. 89999 columns (R = 2, 4, 8 at V = 152064): the ring kernel with pass 2
+    // delayed by one row, the row re-read from L2 -- on B200s, 65536 rows, max over ranks:
+    // R = 2 x 76032 (one 512-thread CTA per SM) 3.38 ms vs 3.83 for the look-ahead ring, 1.00x
+    // the single-GPU kernel on one shard; R = 4 x 38016 (two 256-thread CTAs) 1.78 ms vs 2.18
+    // for the row-wise kernel, 1.04x one shard; delays of 2 / 3 rows are slower (the re-read
+    // rows no longer stay in L2), and so is the two-CTA geometry on the R = 2 rows (4.60 ms:
+    // 2 rows x 148 KB x 296 CTAs = 88 MB), DESIGN.md section 9.1
     if (!lag && !comm->dynamic_rows && n_vec >= 7500)
-        return launch_vp_stream<256, 2, 1024>(p, comm, 6, 3, a.n_rows, s, launches, plan, why, why_len);
+        return launch_vp_delay<512, 1, 2048>(p, comm, 6, 1, a.n_rows, s, launches, plan, why, why_len);
+    if (!lag && !comm->dynamic_rows && n_vec >= 2048)
+        return launch_vp_delay<256, 2, 1024>(p, comm, 6, 1, a.n_rows, s, launches, plan, why, why_len);
     // the row-wise kernel's residency rule on the shard's row length (loss_aux.cu)
     if (n_vec >= 14000) return launch_vp_plan<512, 8, 2>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);
     if (n_vec >= 6000) return launch_vp_plan<256, 8, 4>(p, comm, lag, a.n_rows, s, launches, plan, why, why_len);

@@ -118,7 +118,8 @@ def timing(rank, world, dev, rows, steps, warmup):
 
     modes = {}
     for name, lag, dyn in (("static_lag0", 0, 0), ("static_lag1", 1, 0), ("dynamic_lag0", 0, 1),
-                           ("dynamic_lag1", 1, 1)):
+                           ("dynamic_lag1", 1, 1), ("ring_delay1", 2, 0), ("ring_delay2", 3, 0),
+                           ("ring_delay3", 4, 0)):
         comm.lag, comm.dynamic_rows = lag, dyn
         modes[name] = timed(vp)
     comm.lag, comm.dynamic_rows = 0, 0
