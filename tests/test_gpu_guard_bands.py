@@ -73,10 +73,13 @@ def test_loss_kernels_write_only_their_outputs(dev, name):
         assert np.all(pad == 0xC3), (name, tune, "dlogits padding columns")
 
 
-def test_vp_kernels_write_only_their_shards(dev):
-    """The vocabulary-parallel kernels (row-wise and ring), two ranks in one launch."""
+@pytest.mark.parametrize("world,lag", [(2, 0), (4, 0), (2, 3), (4, 2)])
+def test_vp_kernels_write_only_their_shards(dev, world, lag):
+    """The vocabulary-parallel kernels -- row-wise (V = 4099), the delayed-pass-2 ring
+    (152064 at R = 2, 4: one 512-thread / two 256-thread CTAs per SM; lag 2, 3 forced) and
+    the look-ahead ring (262144 at R = 2) -- R ranks in one launch."""
     rng = np.random.default_rng(3)
-    for V in (4099, 152064):
+    for V in ((4099, 152064, 262144) if lag == 0 else (152064,)):
         b = make_batch("mid152k", 3)
         import dataclasses
         b = dataclasses.replace(b, V=V, ld=(V + 7) // 8 * 8, target_ids=(b.target_ids % V).astype(np.int64))
@@ -84,8 +87,8 @@ def test_vp_kernels_write_only_their_shards(dev):
         from synth.gen import f32_to_bf16_bits
         bits = np.zeros((b.T, b.ld), np.uint16)
         bits[:, :V] = f32_to_bf16_bits(z)
-        world = 2
         comm = G.VpGroup.local(world, V, b.T, dev)
+        comm.lag = lag
         sc = comm.shard_cols
         lg = to_dev_bits(bits, dev)
         shards, dsh = [], []
