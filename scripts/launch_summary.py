@@ -23,7 +23,8 @@ for r in rows[1:]:
 all_us = sum(tot.values())
 fill = sum(v for k, v in tot.items() if "fill_kernel" in k)
 print("# launch list: ncu --metrics gpu__time_duration.sum --clock-control none -c 400")
-print("# command: python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e   (prod, V=152064, 1,008,179 rows/step, chunk 131072)")
+print("# command: " + (sys.argv[2] if len(sys.argv) > 2 else "python bench.py --steps 2 --warmup 1 (scripts/profile_round.sh)")
+      + "   (prod, V=152064, 1,008,179 rows/step, chunk 131072)")
 print("# per-launch times are cold-cache and serialised: compare SHARES, not absolutes")
 print("# share_of_all  share_excl_input_fill  launches  total_us  kernel")
 for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
