@@ -124,7 +124,7 @@ typedef struct {
                            /* kernel 3: 256 consumer threads (default 512)                     */
     int32_t stages;        /* 0 auto, else lag+2..8 shared-memory row stages per CTA (kernel 1); */
                            /* kernel 2: 4, 8 or 16 vectors in flight per thread; kernel 3:  */
-                           /* ring slots (0 = as many as fit: 13 of 16 KB, 6 of 32 KB)       */
+                           /* ring slots (0 = 13 of 16 KB, 6 of 32 KB; at most 14 / 7, 224 KB) */
     int32_t lag;           /* 0 auto, else 1..2: rows between a row's reduction and its       */
                            /* backward, hiding the cluster exchange (kernel 1); kernel 3:    */
                            /* ring slots left free at the end of pass 1 (0 = 3)              */

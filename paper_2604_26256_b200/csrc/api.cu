@@ -475,6 +475,10 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
         // 180000 0.933 / 0.951 / 0.859; 200000 0.878 / 0.912 / 0.845; 230000 0.829 / 0.856 /
         // 0.860; 262144 0.805 / 0.844 / 0.943)
         stream_tune.lag = (n_vec_row + 2047) / 2048 > 10 ? 1 : 3;
+        // a seventh slot (224 KB of ring) where 3 are left free: 4 chunks of the row stay
+        // resident instead of 3, pass 2 re-reads less from L2 (prod: +0.5 %, four same-box
+        // A/B pairs, profiles/r02_k3c_variants_t22_t25.txt)
+        if (stream_tune.lag == 3) stream_tune.stages = 7;
         if (V >= 240000) {
             stream_tune.cluster_size = 2;
             stream_tune.lag = 3;

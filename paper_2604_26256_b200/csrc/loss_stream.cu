@@ -372,8 +372,8 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
                           "16 or 32 KB slots and V >= 16384");
         return cudaErrorInvalidValue;
     }
-    const int max_ns = (cps == 2 ? 96 : 208) / ckb;
-    if (!(tune && tune->stages > 0)) p.ns = max_ns;
+    const int max_ns = (cps == 2 ? 96 : 224) / ckb;  // 7 x 32 KB + barriers + static < 227 KB
+    if (!(tune && tune->stages > 0)) p.ns = (cps == 2 ? 96 : 208) / ckb;
     if (p.ns < 2 || p.ns > max_ns || p.pf >= p.ns) {
         if (why) snprintf(why, why_len, "stream kernel: stages %d (2..%d), lag %d (< stages)", p.ns,
                           max_ns, p.pf);

@@ -20,6 +20,7 @@ STREAM_PLANS = [{"kernel": 3, "stages": st, "lag": lg, "ctas_per_sm": nt, "chunk
                                             (2, 1, 0, 16, 0), (5, 2, 0, 16, 0), (8, 3, 256, 16, 0),
                                             (13, 3, 256, 16, 0), (6, 3, 0, 32, 0), (6, 1, 0, 32, 0),
                                             (2, 1, 0, 32, 0), (6, 5, 0, 32, 0), (3, 1, 256, 32, 0),
+                                            (7, 3, 0, 32, 0), (7, 6, 0, 32, 0), (14, 3, 0, 16, 0),
                                             # two CTAs per SM (the auto plan for 34000 <= V < 90000)
                                             (6, 3, 256, 16, 2), (6, 1, 0, 16, 2), (3, 1, 0, 32, 2),
                                             (2, 1, 256, 32, 2))]
@@ -62,7 +63,8 @@ def test_retired_and_invalid_tunes_refused(dev):
     import paper_2604_26256_b200 as Gp
     b, bits = _case("ragged", 2)
     for tune in ({"kernel": 1}, {"kernel": 3, "cluster_size": 4}, {"kernel": 3, "cluster_size": 2,
-                 "ctas_per_sm": 256}, {"kernel": 2, "cluster_size": 8}, {"kernel": 3, "stages": 40}):
+                 "ctas_per_sm": 256}, {"kernel": 2, "cluster_size": 8}, {"kernel": 3, "stages": 40},
+                 {"kernel": 3, "chunk_kb": 32, "stages": 8}):
         with pytest.raises(Gp.GrpoError) as ei:
             run_gpu(b, bits, dev, tune=tune)
         assert ei.value.status == GRPO_ERR_INVALID_ARG, (tune, ei.value)
@@ -313,7 +315,8 @@ def test_odd_vocabulary_sizes(dev, V):
 def test_auto_plan_choice(dev):
     """The auto plan (tune kernel 0): K3b below V = 34000, K3c with two 256-thread CTAs per
     SM and 16 KB slots up to V = 90000, K3c with one CTA per SM and 32 KB slots from there
-    on (one free ring slot past 10 slots of row), each row split over a two-CTA cluster from
+    on (7 slots, 3 free at the end of pass 1; 6 slots, one free, past 10 slots of row), each
+    row split over a two-CTA cluster from
     V = 240000 (DESIGN.md section 8 measurements); an explicitly tuned call is never
     redirected."""
     import paper_2604_26256_b200 as Gp
@@ -327,8 +330,9 @@ def test_auto_plan_choice(dev):
         plan = Gp.grpo_async_last_plan()
         assert plan["kernel"] == kernel, (V, plan)
         if kernel == 3:
-            assert plan["stages"] == 6 and plan["ctas_per_sm"] == cps, (V, plan)
-            assert plan["smem_bytes"] >= 6 * (32768 if cps == 1 else 16384)
+            ns = 7 if cps == 1 and V <= 163840 else 6  # 7 x 32 KB where 3 slots are left free
+            assert plan["stages"] == ns and plan["ctas_per_sm"] == cps, (V, plan)
+            assert plan["smem_bytes"] >= ns * (32768 if cps == 1 else 16384)
             assert plan["vec_per_thread"] == (512 if cps == 1 else 256), (V, plan)
             assert plan["cluster_size"] == (2 if V >= 240000 else 1), (V, plan)
             if cps == 1:
@@ -506,6 +510,7 @@ def _dead_rows_batch(V, seed):
 
 
 DEAD_PLANS = [None, {"kernel": 3}, {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 3},
+              {"kernel": 3, "chunk_kb": 32, "stages": 7, "lag": 3},
               {"kernel": 3, "chunk_kb": 32, "stages": 6, "lag": 1},
               {"kernel": 3, "chunk_kb": 16, "stages": 13, "lag": 3},
               {"kernel": 3, "chunk_kb": 32, "stages": 2, "lag": 1},
