@@ -446,7 +446,7 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
     std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
     if (traced && (e = prof_begin(s, &ev)) != cudaSuccess) return cuda_fail(e, "loss_fwd/profile");
     // kernel 0 (auto), by row length (plans by V):
-    //   V >= 90000          K3c, one CTA per SM, 6 x 32 KB ring slots (V = 152064: 0.96-0.98
+    //   V >= 90000          K3c, one CTA per SM, 7 x 32 KB ring slots (V = 152064: 0.96-0.98
     //                       of the measured copy bandwidth vs 0.88 for K3b);
     //   34000 <= V < 90000  K3c, two CTAs per SM of 256 consumer threads, 6 x 16 KB slots
     //                       each (V = 50688: 0.89 vs 0.84; 76032: 0.93 vs 0.87);
@@ -475,12 +475,17 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
         // 180000 0.933 / 0.951 / 0.859; 200000 0.878 / 0.912 / 0.845; 230000 0.829 / 0.856 /
         // 0.860; 262144 0.805 / 0.844 / 0.943)
         stream_tune.lag = (n_vec_row + 2047) / 2048 > 10 ? 1 : 3;
-        // a seventh slot (224 KB of ring) where 3 are left free: 4 chunks of the row stay
-        // resident instead of 3, pass 2 re-reads less from L2 (prod: +0.5 %, four same-box
-        // A/B pairs, profiles/r02_k3c_variants_t22_t25.txt)
-        if (stream_tune.lag == 3) stream_tune.stages = 7;
-        if (V >= 240000) {
+        // up to 10 slots of row: a seventh slot (224 KB of ring) and 2 left free, 5 chunks of
+        // the row stay resident instead of 3 and pass 2 re-reads less from L2 (prod: 6 / 3 ->
+        // 7 / 3 +0.5 %, 7 / 3 -> 7 / 2 +0.4 %, same-box A/B pairs,
+        // profiles/r02_k3c_variants_t22_t25.txt)
+        if (stream_tune.lag == 3) {
+            stream_tune.stages = 7;
+            stream_tune.lag = 2;
+        }
+        if (V >= 240000) {  // split rows: 7 slots, 3 free (large: +0.9 % over 6 / 3)
             stream_tune.cluster_size = 2;
+            stream_tune.stages = 7;
             stream_tune.lag = 3;
         }
         tune = &stream_tune;

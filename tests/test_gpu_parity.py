@@ -20,7 +20,7 @@ STREAM_PLANS = [{"kernel": 3, "stages": st, "lag": lg, "ctas_per_sm": nt, "chunk
                                             (2, 1, 0, 16, 0), (5, 2, 0, 16, 0), (8, 3, 256, 16, 0),
                                             (13, 3, 256, 16, 0), (6, 3, 0, 32, 0), (6, 1, 0, 32, 0),
                                             (2, 1, 0, 32, 0), (6, 5, 0, 32, 0), (3, 1, 256, 32, 0),
-                                            (7, 3, 0, 32, 0), (7, 6, 0, 32, 0), (14, 3, 0, 16, 0),
+                                            (7, 3, 0, 32, 0), (7, 2, 0, 32, 0), (7, 6, 0, 32, 0), (14, 3, 0, 16, 0),
                                             # two CTAs per SM (the auto plan for 34000 <= V < 90000)
                                             (6, 3, 256, 16, 2), (6, 1, 0, 16, 2), (3, 1, 0, 32, 2),
                                             (2, 1, 256, 32, 2))]
@@ -315,8 +315,8 @@ def test_odd_vocabulary_sizes(dev, V):
 def test_auto_plan_choice(dev):
     """The auto plan (tune kernel 0): K3b below V = 34000, K3c with two 256-thread CTAs per
     SM and 16 KB slots up to V = 90000, K3c with one CTA per SM and 32 KB slots from there
-    on (7 slots, 3 free at the end of pass 1; 6 slots, one free, past 10 slots of row), each
-    row split over a two-CTA cluster from
+    on (7 slots, 2 free at the end of pass 1; 6 slots, one free, past 10 slots of row), each
+    row split over a two-CTA cluster (7 slots, 3 free) from
     V = 240000 (DESIGN.md section 8 measurements); an explicitly tuned call is never
     redirected."""
     import paper_2604_26256_b200 as Gp
@@ -330,13 +330,14 @@ def test_auto_plan_choice(dev):
         plan = Gp.grpo_async_last_plan()
         assert plan["kernel"] == kernel, (V, plan)
         if kernel == 3:
-            ns = 7 if cps == 1 and V <= 163840 else 6  # 7 x 32 KB where 3 slots are left free
+            long_row = cps == 1 and 163840 < V < 240000  # > 10 slots of row: 6 slots, 1 free
+            ns = 6 if cps == 2 or long_row else 7
             assert plan["stages"] == ns and plan["ctas_per_sm"] == cps, (V, plan)
             assert plan["smem_bytes"] >= ns * (32768 if cps == 1 else 16384)
             assert plan["vec_per_thread"] == (512 if cps == 1 else 256), (V, plan)
             assert plan["cluster_size"] == (2 if V >= 240000 else 1), (V, plan)
             if cps == 1:
-                assert plan["lag"] == (1 if 163840 < V < 240000 else 3), (V, plan)
+                assert plan["lag"] == (1 if long_row else 3 if V >= 240000 else 2), (V, plan)
         compare(gpu, ref, b, logits_pad=bits[:, b.V:])
     run_gpu(b, bits, dev, tune={"kernel": 2, "stages": 8})
     assert Gp.grpo_async_last_plan()["kernel"] == 2
@@ -453,7 +454,7 @@ def test_precision_regression_cases(dev, seed):
 
 
 SPLIT_PLANS = [{"kernel": 3, "cluster_size": 2, "chunk_kb": kb, "stages": ns, "lag": pf}
-               for kb, ns, pf in ((32, 6, 3), (32, 6, 1), (32, 2, 1), (16, 13, 3), (16, 3, 2))]
+               for kb, ns, pf in ((32, 7, 3), (32, 6, 3), (32, 6, 1), (32, 2, 1), (16, 13, 3), (16, 3, 2))]
 
 
 @pytest.mark.parametrize("plan", SPLIT_PLANS,
