@@ -19,7 +19,8 @@
 //   epilogue warp           per row: waits for the 16 warp partials, combines them (and,
 //                           with SPLIT = 2, exchanges them with the partner CTA), runs the
 //                           fp64 per-row epilogue (logp, ratio, clip, term, token scale)
-//                           and hands (lse2, s, g_y = s (p_y - 1), y) to the consumers' pass 2.
+//                           and hands (ref = lse2 - log2|s|, s, g_y = s (p_y - 1), y) to the
+//                           consumers' pass 2 (the log2 once per row, not once per thread).
 //
 // The epilogue and the block combine thus run while the consumers stream the next row's
 // first chunks: no per-row barrier among the consumers and no serial section on their
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.ns * CHUNK_BYTES);
     uint64_t *empty = full + p.ns;
     __shared__ RowPart red[2][NW];                 // warp partials, by row parity
-    __shared__ float4 scal[2];                     // (lse2, s, g_y, y) for pass 2, by row parity
+    __shared__ float4 scal[2];                     // (ref, s, g_y, y) for pass 2, by row parity
     __shared__ __align__(8) uint64_t part_bar[2];  // NW warp arrivals: red[b] complete
     __shared__ __align__(8) uint64_t scal_bar[2];  // 1 arrival: scal[b] written
     __shared__ RowPart xbuf[2];
@@ -198,7 +199,8 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                     p.logp_ws[row] = logp;
                     p.flag_ws[row] = o.flags;
                 }
-                scal[b] = make_float4(lse2, o.s, o.gy, __int_as_float(y_valid ? ri.target : -1));
+                scal[b] = make_float4(RowwiseBatch<NT, U>::grad_ref(o.s, lse2).ref, o.s, o.gy,
+                                      __int_as_float(y_valid ? ri.target : -1));
                 mbar_arrive(scal_bar + b);
             }
             __syncwarp();
@@ -272,11 +274,12 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
         // ---- pass 2: resident chunks n-R..n-1 (loads res_base + (c - LA)), then the re-loads
         mbar_wait(scal_bar + b, (rowk >> 1) & 1u);
         const float4 sc4 = scal[b];
-        const float lse2 = sc4.x, sc = sc4.y, gy = sc4.z;
-        const auto gref = RowwiseBatch<NT, U>::grad_ref(sc, lse2);
+        const float sc = sc4.y, gy = sc4.z;
+        const typename RowwiseBatch<NT, U>::GradRef gref{sc4.x, sc < 0.0f ? 0x80008000u : 0u};
         const int32_t yfull = __float_as_int(sc4.w);
         const int32_t y = (yfull >= col0 && yfull < col0 + Vloc) ? yfull - col0 : -1;  // in this slice
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
+        const int res_sl = g.R > 0 ? (res_base + (g.n - g.R - g.LA)) % p.ns : 0;  // slot of chunk n-R
         uint16_t *drow = p.dlogits + row * p.ld + col0;
         uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
         for (int i = 0; i < g.n; ++i) {
@@ -284,7 +287,8 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
             const int c = resident ? g.n - g.R + i : i - g.R;
             int sl;
             if (resident) {
-                sl = (res_base + (c - g.LA)) % p.ns;  // the pass-1 load of chunk c, still in its slot
+                sl = res_sl + i;  // the pass-1 load of chunk c, still in its slot
+                if (sl >= p.ns) sl -= p.ns;
             } else {
                 sl = slot;
                 mbar_wait(full + sl, par);
