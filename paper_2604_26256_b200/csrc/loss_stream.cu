@@ -307,9 +307,16 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                     uint4 x[U];
 #pragma unroll
                     for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+                    if (gref.sign == 0u) {  // s > 0: no sign flip on the packed pairs
+                        const typename RowwiseBatch<NT, U>::GradRef gp{gref.ref, 0u};
 #pragma unroll
-                    for (int j = 0; j < U; ++j)
-                        stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gref));
+                        for (int j = 0; j < U; ++j)
+                            stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gp));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < U; ++j)
+                            stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gref));
+                    }
                 }
             } else {
 #pragma unroll
