@@ -452,6 +452,10 @@ grpo_status_t grpo_async_loss_bwd(const uint16_t *logits, int64_t n_rows, int32_
  *   dhidden bf16 (out_bf16 = 1) or f32 [n_rows, d]; the unfused pipeline's dX GEMM.
  * grpo_async_lmhead_logits -- the plain logits hidden W^T as bf16 [n_rows, ld_out] (the
  *   unfused producer for grpo_async_loss_fwd, and the check of the GEMM).
+ * Scheduling: the forward, dz and dW kernels hand their work units out dynamically from a
+ * unit counter in library-owned device memory (one of 64 slots, zeroed by a 4-byte
+ * cudaMemsetAsync on `stream` before each launch; more than 64 of these launches in flight
+ * at once on different streams would share a slot); results never depend on the order.
  * Errors: GRPO_ERR_INVALID_ARG, GRPO_ERR_ALIGNMENT, GRPO_ERR_WORKSPACE, GRPO_ERR_CUDA.
  */
 size_t grpo_async_lmhead_workspace_size(int64_t n_rows, int32_t V, int32_t N);
