@@ -112,8 +112,7 @@ typedef struct {
 /* Optional tuning of the fused loss kernel (NULL = automatic). */
 typedef struct {
     int32_t kernel;        /* 0 auto: 2 for V < 34000; 3 with 2 CTAs x 6 x 16 KB up to 90000, */
-                           /* else 3 with 1 CTA x 7 x 32 KB slots per SM (6 past 10 slots of */
-                           /* row), rows split over 2                                      */
+                           /* else 3 with 1 CTA x 7 x 32 KB slots per SM, rows split over 2 */
                            /* SMs from V = 240000 (an explicit                               */
                            /* tune with other fields set is never redirected); 1 cluster-    */
                            /* resident; 2 row-wise; 3 one row per SM through a bulk-copy ring */

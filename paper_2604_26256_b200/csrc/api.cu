@@ -479,10 +479,11 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
         // the row stay resident instead of 3 and pass 2 re-reads less from L2 (prod: 6 / 3 ->
         // 7 / 3 +0.5 %, 7 / 3 -> 7 / 2 +0.4 %, same-box A/B pairs,
         // profiles/r02_k3c_variants_t22_t25.txt)
-        if (stream_tune.lag == 3) {
-            stream_tune.stages = 7;
-            stream_tune.lag = 2;
-        }
+        // longer rows: 7 slots, one left free (V = 180000 / 200000 / 220000, 65536-row launches:
+        // 0.961 / 0.933 / 0.893 of the measured copy bandwidth vs 0.951 / 0.922 / 0.896 with 6
+        // slots; profiles/r02_plan_sweep.txt)
+        stream_tune.stages = 7;
+        if (stream_tune.lag == 3) stream_tune.lag = 2;
         if (V >= 240000) {  // split rows: 7 slots, 3 free (large: +0.9 % over 6 / 3)
             stream_tune.cluster_size = 2;
             stream_tune.stages = 7;
