@@ -475,9 +475,11 @@ def main():
         torch.cuda.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+        # the end-to-end result must be the device-timed run's, bit for bit
+        e2e_same = bool(out_host[G.STAT_J].item() == float(stats_h[G.STAT_J]))
         e2e = {"value": T_total * args.steps / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": e2e_ms / args.steps,
+               "ms_per_step": e2e_ms / args.steps, "result_matches_device_run": e2e_same,
                "note": "per step and rank: pinned H2D of the replicated trajectory metadata "
                        "(cu_seqlens, group ids, versions, rewards) and of this rank's token "
                        "arrays (targets, behaviour log-probs, token versions, local packing), "
