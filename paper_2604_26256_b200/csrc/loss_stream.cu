@@ -5,7 +5,7 @@
 // miss L2.  K3c gives each SM one row at a time and moves it with the bulk-copy engine
 // (cp.async.bulk global -> shared, completion on mbarriers) into a FIFO ring of NS
 // slots, so the loads need neither registers nor L1 staging and almost the whole
-// shared memory holds row data.  Three roles:
+// shared memory holds row data.  Four roles:
 //
 //   producer (one thread)   loads, per row k, the pass-1 chunks of row k, then the first
 //                           LA (= 1) chunks of row k+1 (the look-ahead), then the re-loads of
@@ -15,7 +15,9 @@
 //                           were consumed in the previous row's look-ahead), publish the
 //                           warps' partials, pass 1 of row k+1's first LA chunks, then pass
 //                           2 of row k (the R resident chunks, then the re-loads), writing
-//                           dlogits and releasing every slot;
+//                           each chunk's dlogits over its logits in the slot;
+//   store warp (one thread) copies every pass-2 slot to the dlogits row (bulk shared ->
+//                           global) and frees it once the copy has read it;
 //   epilogue warp           per row: waits for the 16 warp partials, combines them (and,
 //                           with SPLIT = 2, exchanges them with the partner CTA), runs the
 //                           fp64 per-row epilogue (logp, ratio, clip, term, token scale)
@@ -33,6 +35,7 @@
 
 #include "common.cuh"
 #include "rowwise.cuh"
+#include "tc.cuh"
 
 namespace grpo {
 namespace k3c {
@@ -82,7 +85,7 @@ __device__ __forceinline__ Geometry geometry(const Params &p, int V, bool two_pa
 // load and its pass-2 re-load, so at V = 262144 (512 KB rows) the re-loads stay in L2;
 // the pair's wait for each other sits in the epilogue warps, off the consumers' path.
 template <int NT, int MINB, int CHUNK_VECS, int SPLIT>
-__global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
+__global__ void __launch_bounds__(NT + 96, MINB) stream_kernel(const Params p) {
     constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr int U = CHUNK_VECS / NT;  // vectors per consumer thread per chunk
     constexpr int NW = NT / 32;
@@ -90,6 +93,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
     uint4 *ring = reinterpret_cast<uint4 *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)p.ns * CHUNK_BYTES);
     uint64_t *empty = full + p.ns;
+    uint64_t *wrote = empty + p.ns;  // pass-2 uses: NW warp arrivals, the slot holds dlogits
     __shared__ RowPart red[2][NW];                 // warp partials, by row parity
     __shared__ float4 scal[2];                     // (ref, s, g_y, y) for pass 2, by row parity
     __shared__ __align__(8) uint64_t part_bar[2];  // NW warp arrivals: red[b] complete
@@ -108,6 +112,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
         for (int s = 0; s < p.ns; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, NW);
+            mbar_init(wrote + s, NW);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(part_bar + b, NW);
@@ -149,6 +154,47 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                 if (two_pass)
                     for (int c = 0; c < g.n - g.R; ++c) load(row, c, true);
             }
+        }
+        return;
+    }
+
+    if (warp == NW + 2) {
+        // ------------------------------------------------------------ store warp
+        // Pass 2 writes each chunk's dlogits over its logits in the ring slot; one thread here
+        // copies the slot to the dlogits row with a bulk copy (shared -> global) and frees the
+        // slot once the copy has read it.  It walks the producer's load order (= the
+        // consumers' order) and acts on the pass-2 uses only: the resident chunks of row k and
+        // its re-loads; a pass-1-only use is freed by the consumers themselves.  The partial
+        // last vector of a row (V % 8 != 0) is stored by its consumer thread instead: a bulk
+        // copy would write the padding columns behind V.
+        if (lane == 0 && two_pass) {
+            const uint64_t pol = policy_evict_first();
+            const int64_t full_bytes = (int64_t)(g.tail_valid < 8 ? g.n_vec - 1 : g.n_vec) * 16;
+            int slot = 0;
+            uint32_t wpar = 0u;  // per slot: parity of its next pass-2 use
+            auto use = [&](int64_t row, int c, bool pass2) {
+                const int sl = slot;
+                if (++slot == p.ns) slot = 0;
+                if (!pass2) return;
+                mbar_wait_sleep(wrote + sl, (wpar >> sl) & 1u, 32);
+                wpar ^= 1u << sl;
+                const int64_t off = (int64_t)c * CHUNK_BYTES;
+                const int64_t end = off + CHUNK_BYTES < full_bytes ? off + CHUNK_BYTES : full_bytes;
+                if (end > off) {
+                    bulk_s2g(reinterpret_cast<uint8_t *>(p.dlogits + row * p.ld + col0) + off,
+                             ring + (size_t)sl * CHUNK_VECS, (uint32_t)(end - off), pol);
+                    tc::bulk_commit();
+                    tc::bulk_wait_read<0>();
+                }
+                mbar_arrive_count(empty + sl, NW);
+            };
+            for (int64_t row = row0; row < p.n_rows; row += rstep) {
+                for (int c = (row == row0 ? 0 : g.LA); c < g.n; ++c) use(row, c, c >= g.n - g.R);
+                if (row + rstep < p.n_rows)
+                    for (int c = 0; c < g.LA; ++c) use(row + rstep, c, false);
+                for (int c = 0; c < g.n - g.R; ++c) use(row, c, true);
+            }
+            tc::bulk_wait_all();
         }
         return;
     }
@@ -281,7 +327,6 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
         const int res_sl = g.R > 0 ? (res_base + (g.n - g.R - g.LA)) % p.ns : 0;  // slot of chunk n-R
         uint16_t *drow = p.dlogits + row * p.ld + col0;
-        uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
         for (int i = 0; i < g.n; ++i) {
             const bool resident = i < g.R;
             const int c = resident ? g.n - g.R + i : i - g.R;
@@ -297,12 +342,15 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                     par ^= 1u;
                 }
             }
-            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            // the chunk's dlogits go over its logits in the slot (each thread rewrites the
+            // vectors it read); the store warp copies the slot out (bulk shared -> global)
+            uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
             const int v0 = c * CHUNK_VECS + threadIdx.x;
+            bool tail_here = false;  // this thread stored the row's partial last vector itself
             if (c != g.n - 1) {  // full chunk: no checks
                 if (sc == 0.0f) {
 #pragma unroll
-                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, make_uint4(0u, 0u, 0u, 0u));
+                    for (int j = 0; j < U; ++j) chunk[j * NT + threadIdx.x] = make_uint4(0u, 0u, 0u, 0u);
                 } else {
                     uint4 x[U];
 #pragma unroll
@@ -311,11 +359,11 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                         const typename RowwiseBatch<NT, U>::GradRef gp{gref.ref, 0u};
 #pragma unroll
                         for (int j = 0; j < U; ++j)
-                            stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gp));
+                            chunk[j * NT + threadIdx.x] = RowwiseBatch<NT, U>::grad_scaled(x[j], gp);
                     } else {
 #pragma unroll
                         for (int j = 0; j < U; ++j)
-                            stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gref));
+                            chunk[j * NT + threadIdx.x] = RowwiseBatch<NT, U>::grad_scaled(x[j], gref);
                     }
                 }
             } else {
@@ -325,19 +373,23 @@ __global__ void __launch_bounds__(NT + 64, MINB) stream_kernel(const Params p) {
                     if (vi >= g.n_vec) break;
                     const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
                                                : RowwiseBatch<NT, U>::grad_scaled(chunk[j * NT + threadIdx.x], gref);
-                    if (vi == g.n_vec - 1 && g.tail_valid < 8) store_tail(drow + (int64_t)vi * 8, d, g.tail_valid);
-                    else stg_stream(dst4 + vi, d);
+                    if (vi == g.n_vec - 1 && g.tail_valid < 8) {
+                        store_tail(drow + (int64_t)vi * 8, d, g.tail_valid);
+                        tail_here = true;
+                    } else {
+                        chunk[j * NT + threadIdx.x] = d;
+                    }
                 }
             }
             // the target's own column (g_y from the fp64 epilogue), rewritten by the thread that
-            // stored its vector, right after it: the 2-byte store then merges into the sector the
-            // vector store left in L2 (hoisted after the loop, it lands on an evicted sector and
-            // the bench loses 1.1 %, measured)
+            // wrote its vector: in the slot, or in global memory behind the partial last vector
             if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
-                drow[y] = f2bf(gy);
+                if (tail_here && (y >> 3) == g.n_vec - 1) drow[y] = f2bf(gy);
+                else reinterpret_cast<uint16_t *>(chunk)[y - c * CHUNK_VECS * 8] = f2bf(gy);
             }
+            tc::fence_proxy_async_smem();  // the generic-proxy writes, visible to the bulk copy
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty + sl);
+            if (lane == 0) mbar_arrive(wrote + sl);
         }
     }
 }
@@ -390,7 +442,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
                           max_ns, p.pf);
         return cudaErrorInvalidValue;
     }
-    const size_t smem = (size_t)p.ns * ckb * 1024 + 2 * (size_t)p.ns * 8;
+    const size_t smem = (size_t)p.ns * ckb * 1024 + 3 * (size_t)p.ns * 8;  // ring + full / empty / wrote
     int dev = 0, n_sm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -405,7 +457,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
         at[0].val.clusterDim.x = 2;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
-        cfg.blockDim = dim3(512 + 64);
+        cfg.blockDim = dim3(512 + 96);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cfg.attrs = at;
@@ -428,7 +480,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
         e = cudaFuncSetAttribute(stream_kernel<NT_, MB_, CV_, 1>,                                         \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
         if (e != cudaSuccess) return e;                                                                \
-        stream_kernel<NT_, MB_, CV_, 1><<<grid, NT_ + 64, smem, s>>>(p);                                  \
+        stream_kernel<NT_, MB_, CV_, 1><<<grid, NT_ + 96, smem, s>>>(p);                                  \
     } while (0)
     if (ckb == 64) {
         GRPO_K3C(512, 1, 4096);
