@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "rowwise.cuh"
+#include "tc.cuh"
 
 namespace grpo {
 
@@ -577,7 +578,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) vp_stream_kernel(const VpParams
 // precedes their partial of row k+1, and the epilogue warp handles rows in order, so a
 // buffer is free again when it is rewritten).  Same combine order: bit-identical outputs.
 template <int NT, int MINB, int CHUNK_VECS>
-__global__ void __launch_bounds__(NT + 64, MINB) vp_delay_kernel(const VpParams p, const int ns, const int D) {
+__global__ void __launch_bounds__(NT + 96, MINB) vp_delay_kernel(const VpParams p, const int ns, const int D) {
     constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr int U = CHUNK_VECS / NT;
     constexpr int NW = NT / 32;
@@ -587,6 +588,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) vp_delay_kernel(const VpParams 
     uint4 *ring = reinterpret_cast<uint4 *>(smem);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)ns * CHUNK_BYTES);
     uint64_t *empty = full + ns;
+    uint64_t *wrote = empty + ns;  // pass-2 uses: NW warp arrivals, the slot holds dlogits
     __shared__ RowPart red[NBMAX][NW];
     __shared__ float4 scal[NBMAX];
     __shared__ __align__(8) uint64_t part_bar[NBMAX];
@@ -612,6 +614,7 @@ __global__ void __launch_bounds__(NT + 64, MINB) vp_delay_kernel(const VpParams 
         for (int q = 0; q < ns; ++q) {
             mbar_init(full + q, 1);
             mbar_init(empty + q, NW);
+            mbar_init(wrote + q, NW);
         }
         for (int b = 0; b < NB; ++b) {
             mbar_init(part_bar + b, NW);
@@ -648,6 +651,48 @@ __global__ void __launch_bounds__(NT + 64, MINB) vp_delay_kernel(const VpParams 
             }
             if (two_pass)
                 for (int64_t k = (n_mine > D ? n_mine - D : (int64_t)0); k < n_mine; ++k) load_row(row_of(k), pol_once);
+        }
+        return;
+    }
+
+    if (warp == NW + 2) {
+        // ------------------------------------------------------------ store warp
+        // as in K3c (loss_stream.cu): pass 2 writes each chunk's dlogits over its re-loaded
+        // logits in the slot; one thread copies the slot to the dlogits row (bulk shared ->
+        // global) and frees it once read, walking the producer's load order (P1(k), then the
+        // re-loads of row k - D); the partial last vector is stored by its consumer thread
+        if (lane == 0 && two_pass && n > 0) {
+            const uint64_t pol = policy_evict_first();
+            const int64_t full_bytes = (int64_t)(tail_valid < 8 ? n_vec - 1 : n_vec) * 16;
+            int slot = 0;
+            uint32_t wpar = 0u;  // per slot: parity of its next pass-2 use
+            auto skip_row = [&]() {
+                slot += n;
+                while (slot >= ns) slot -= ns;
+            };
+            auto store_row = [&](int64_t row) {
+                for (int c = 0; c < n; ++c) {
+                    const int sl = slot;
+                    if (++slot == ns) slot = 0;
+                    mbar_wait_sleep(wrote + sl, (wpar >> sl) & 1u, 32);
+                    wpar ^= 1u << sl;
+                    const int64_t off = (int64_t)c * CHUNK_BYTES;
+                    const int64_t end = off + CHUNK_BYTES < full_bytes ? off + CHUNK_BYTES : full_bytes;
+                    if (end > off) {
+                        bulk_s2g(reinterpret_cast<uint8_t *>(dshard + row * p.ld) + off,
+                                 ring + (size_t)sl * CHUNK_VECS, (uint32_t)(end - off), pol);
+                        tc::bulk_commit();
+                        tc::bulk_wait_read<0>();
+                    }
+                    mbar_arrive_count(empty + sl, NW);
+                }
+            };
+            for (int64_t k = 0; k < n_mine; ++k) {
+                skip_row();  // pass 1 of row k: freed by the consumers
+                if (k >= D) store_row(row_of(k - D));
+            }
+            for (int64_t k = (n_mine > D ? n_mine - D : (int64_t)0); k < n_mine; ++k) store_row(row_of(k));
+            tc::bulk_wait_all();
         }
         return;
     }
@@ -790,21 +835,21 @@ __global__ void __launch_bounds__(NT + 64, MINB) vp_delay_kernel(const VpParams 
         const int32_t y = __float_as_int(sc4.w);
         const int y_chunk = y >= 0 ? (y >> 3) / CHUNK_VECS : -1;
         uint16_t *drow = dshard + row * p.ld;
-        uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
         for (int c = 0; c < n; ++c) {
             const int sl = take();
-            const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+            uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;  // dlogits go over the logits here
             const int v0 = c * CHUNK_VECS + threadIdx.x;
+            bool tail_here = false;
             if (c != n - 1) {
                 if (sc == 0.0f) {
 #pragma unroll
-                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, make_uint4(0u, 0u, 0u, 0u));
+                    for (int j = 0; j < U; ++j) chunk[j * NT + threadIdx.x] = make_uint4(0u, 0u, 0u, 0u);
                 } else {
                     uint4 x[U];
 #pragma unroll
                     for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
 #pragma unroll
-                    for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, B::grad_scaled(x[j], gref));
+                    for (int j = 0; j < U; ++j) chunk[j * NT + threadIdx.x] = B::grad_scaled(x[j], gref);
                 }
             } else {
 #pragma unroll
@@ -813,14 +858,21 @@ __global__ void __launch_bounds__(NT + 64, MINB) vp_delay_kernel(const VpParams 
                     if (vi >= n_vec) break;
                     const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
                                                : B::grad_scaled(chunk[j * NT + threadIdx.x], gref);
-                    if (vi == n_vec - 1 && tail_valid < 8) store_tail(drow + (int64_t)vi * 8, d, tail_valid);
-                    else stg_stream(dst4 + vi, d);
+                    if (vi == n_vec - 1 && tail_valid < 8) {
+                        store_tail(drow + (int64_t)vi * 8, d, tail_valid);
+                        tail_here = true;
+                    } else {
+                        chunk[j * NT + threadIdx.x] = d;
+                    }
                 }
             }
             if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
-                drow[y] = f2bf(gy);
+                if (tail_here && (y >> 3) == n_vec - 1) drow[y] = f2bf(gy);
+                else reinterpret_cast<uint16_t *>(chunk)[y - c * CHUNK_VECS * 8] = f2bf(gy);
             }
-            release(sl);
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(wrote + sl);
         }
     };
     for (int64_t k = 0; k < n_mine; ++k) {
@@ -835,14 +887,14 @@ template <int NT, int MINB, int CV>
 static cudaError_t launch_vp_delay(VpParams p, const grpo_vp_comm_t *comm, int ns, int D, int64_t n_rows,
                                    cudaStream_t s, int *launches, grpo_plan_t *plan, char *why,
                                    size_t why_len) {
-    const size_t smem = (size_t)ns * CV * 16 + 2 * (size_t)ns * 8;
+    const size_t smem = (size_t)ns * CV * 16 + 3 * (size_t)ns * 8;
     auto kern = vp_delay_kernel<NT, MINB, CV>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, n_sm = 148, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 64, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 96, smem);
     if (e != cudaSuccess) return e;
     // every CTA must be resident (a CTA may wait for a peer rank's CTA of the same index)
     int64_t g_per = (int64_t)n_sm * (occ < MINB ? occ : MINB) / comm->n_local;
@@ -856,7 +908,7 @@ static cudaError_t launch_vp_delay(VpParams p, const grpo_vp_comm_t *comm, int n
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.gridDim = dim3((unsigned)(g_per * comm->n_local));
-    cfg.blockDim = dim3(NT + 64);
+    cfg.blockDim = dim3(NT + 96);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
