@@ -474,16 +474,14 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
         // measured copy bandwidth: V = 152064 lag 3 0.955 / lag 1 0.946 / split 0.847;
         // 180000 0.933 / 0.951 / 0.859; 200000 0.878 / 0.912 / 0.845; 230000 0.829 / 0.856 /
         // 0.860; 262144 0.805 / 0.844 / 0.943)
-        stream_tune.lag = (n_vec_row + 2047) / 2048 > 10 ? 1 : 3;
-        // up to 10 slots of row: a seventh slot (224 KB of ring) and 2 left free, 5 chunks of
-        // the row stay resident instead of 3 and pass 2 re-reads less from L2 (prod: 6 / 3 ->
-        // 7 / 3 +0.5 %, 7 / 3 -> 7 / 2 +0.4 %, same-box A/B pairs,
-        // profiles/r02_k3c_variants_t22_t25.txt)
-        // longer rows: 7 slots, one left free (V = 180000 / 200000 / 220000, 65536-row launches:
-        // 0.961 / 0.933 / 0.893 of the measured copy bandwidth vs 0.951 / 0.922 / 0.896 with 6
-        // slots; profiles/r02_plan_sweep.txt)
+        // 7 slots (224 KB of ring), one left free at the end of pass 1: 6 chunks of the row stay
+        // resident and pass 2 re-reads the rest from L2 (prod, same-box A/B pairs: 6 / 3 -> 7 / 3
+        // +0.5 %, 7 / 3 -> 7 / 2 +0.4 %, and with the bulk-copy stores 7 / 2 -> 7 / 1 +0.5 %;
+        // long rows, 65536-row launches: V = 180000 / 200000 / 220000 at 0.961 / 0.933 / 0.893 of
+        // the measured copy bandwidth vs 0.951 / 0.922 / 0.896 with 6 / 1;
+        // profiles/r02_k3c_variants_t22_t25.txt, r02_plan_sweep.txt)
         stream_tune.stages = 7;
-        if (stream_tune.lag == 3) stream_tune.lag = 2;
+        stream_tune.lag = 1;
         if (V >= 240000) {  // split rows: 7 slots, 3 free (large: +0.9 % over 6 / 3)
             stream_tune.cluster_size = 2;
             stream_tune.stages = 7;
