@@ -482,11 +482,9 @@ grpo_status_t grpo_async_loss_fwd_ex(const uint16_t *logits, int64_t row_begin, 
         // profiles/r02_k3c_variants_t22_t25.txt, r02_plan_sweep.txt)
         stream_tune.stages = 7;
         stream_tune.lag = 1;
-        if (V >= 240000) {  // split rows: 7 slots, 3 free (large: +0.9 % over 6 / 3)
-            stream_tune.cluster_size = 2;
-            stream_tune.stages = 7;
-            stream_tune.lag = 3;
-        }
+        // split rows from V = 240000, the same ring (large, same-box pairs: 6 / 3 -> 7 / 3 +0.9 %,
+        // 7 / 3 -> 7 / 1 +0.9 %)
+        if (V >= 240000) stream_tune.cluster_size = 2;
         tune = &stream_tune;
     } else if (auto_stream) {
         stream_tune.kernel = 3;
