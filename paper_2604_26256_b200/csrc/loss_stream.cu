@@ -84,8 +84,10 @@ __device__ __forceinline__ Geometry geometry(const Params &p, int V, bool two_pa
 // hold identical row scalars.  Halving the row halves the time between a chunk's pass-1
 // load and its pass-2 re-load, so at V = 262144 (512 KB rows) the re-loads stay in L2;
 // the pair's wait for each other sits in the epilogue warps, off the consumers' path.
-template <int NT, int MINB, int CHUNK_VECS, int SPLIT>
-__global__ void __launch_bounds__(NT + 96, MINB) stream_kernel(const Params p) {
+// BULK: pass 2's dlogits leave through the ring slots by a store warp's bulk copies (one CTA
+// per SM); otherwise every consumer thread stores its vectors (the two-CTA plan).
+template <int NT, int MINB, int CHUNK_VECS, int SPLIT, bool BULK = (MINB == 1)>
+__global__ void __launch_bounds__(NT + (BULK ? 96 : 64), MINB) stream_kernel(const Params p) {
     constexpr int CHUNK_BYTES = CHUNK_VECS * 16;
     constexpr int U = CHUNK_VECS / NT;  // vectors per consumer thread per chunk
     constexpr int NW = NT / 32;
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(NT + 96, MINB) stream_kernel(const Params p) {
         return;
     }
 
-    if (warp == NW + 2) {
+    if (BULK && warp == NW + 2) {
         // ------------------------------------------------------------ store warp
         // Pass 2 writes each chunk's dlogits over its logits in the ring slot; one thread here
         // copies the slot to the dlogits row with a bulk copy (shared -> global) and frees the
@@ -342,54 +344,97 @@ __global__ void __launch_bounds__(NT + 96, MINB) stream_kernel(const Params p) {
                     par ^= 1u;
                 }
             }
-            // the chunk's dlogits go over its logits in the slot (each thread rewrites the
-            // vectors it read); the store warp copies the slot out (bulk shared -> global)
-            uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
-            const int v0 = c * CHUNK_VECS + threadIdx.x;
-            bool tail_here = false;  // this thread stored the row's partial last vector itself
-            if (c != g.n - 1) {  // full chunk: no checks
-                if (sc == 0.0f) {
-#pragma unroll
-                    for (int j = 0; j < U; ++j) chunk[j * NT + threadIdx.x] = make_uint4(0u, 0u, 0u, 0u);
+            if constexpr (BULK) {
+                // the chunk's dlogits go over its logits in the slot (each thread rewrites the
+                // vectors it read); the store warp copies the slot out (bulk shared -> global)
+                uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+                const int v0 = c * CHUNK_VECS + threadIdx.x;
+                bool tail_here = false;  // this thread stored the row's partial last vector itself
+                if (c != g.n - 1) {  // full chunk: no checks
+                    if (sc == 0.0f) {
+    #pragma unroll
+                        for (int j = 0; j < U; ++j) chunk[j * NT + threadIdx.x] = make_uint4(0u, 0u, 0u, 0u);
+                    } else {
+                        uint4 x[U];
+    #pragma unroll
+                        for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+                        if (gref.sign == 0u) {  // s > 0: no sign flip on the packed pairs
+                            const typename RowwiseBatch<NT, U>::GradRef gp{gref.ref, 0u};
+    #pragma unroll
+                            for (int j = 0; j < U; ++j)
+                                chunk[j * NT + threadIdx.x] = RowwiseBatch<NT, U>::grad_scaled(x[j], gp);
+                        } else {
+    #pragma unroll
+                            for (int j = 0; j < U; ++j)
+                                chunk[j * NT + threadIdx.x] = RowwiseBatch<NT, U>::grad_scaled(x[j], gref);
+                        }
+                    }
                 } else {
-                    uint4 x[U];
-#pragma unroll
-                    for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
-                    if (gref.sign == 0u) {  // s > 0: no sign flip on the packed pairs
-                        const typename RowwiseBatch<NT, U>::GradRef gp{gref.ref, 0u};
-#pragma unroll
-                        for (int j = 0; j < U; ++j)
-                            chunk[j * NT + threadIdx.x] = RowwiseBatch<NT, U>::grad_scaled(x[j], gp);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < U; ++j)
-                            chunk[j * NT + threadIdx.x] = RowwiseBatch<NT, U>::grad_scaled(x[j], gref);
+    #pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int vi = v0 + j * NT;
+                        if (vi >= g.n_vec) break;
+                        const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
+                                                   : RowwiseBatch<NT, U>::grad_scaled(chunk[j * NT + threadIdx.x], gref);
+                        if (vi == g.n_vec - 1 && g.tail_valid < 8) {
+                            store_tail(drow + (int64_t)vi * 8, d, g.tail_valid);
+                            tail_here = true;
+                        } else {
+                            chunk[j * NT + threadIdx.x] = d;
+                        }
                     }
                 }
+                // the target's own column (g_y from the fp64 epilogue), rewritten by the thread that
+                // wrote its vector: in the slot, or in global memory behind the partial last vector
+                if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
+                    if (tail_here && (y >> 3) == g.n_vec - 1) drow[y] = f2bf(gy);
+                    else reinterpret_cast<uint16_t *>(chunk)[y - c * CHUNK_VECS * 8] = f2bf(gy);
+                }
+                tc::fence_proxy_async_smem();  // the generic-proxy writes, visible to the bulk copy
+                __syncwarp();
+                if (lane == 0) mbar_arrive(wrote + sl);
             } else {
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int vi = v0 + j * NT;
-                    if (vi >= g.n_vec) break;
-                    const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
-                                               : RowwiseBatch<NT, U>::grad_scaled(chunk[j * NT + threadIdx.x], gref);
-                    if (vi == g.n_vec - 1 && g.tail_valid < 8) {
-                        store_tail(drow + (int64_t)vi * 8, d, g.tail_valid);
-                        tail_here = true;
+                // direct stores (the two-CTA plan: its 16 KB slots and 2 x 352 threads lost 3 % at
+                // V = 50688 with the store warp, t67)
+                const uint4 *chunk = ring + (size_t)sl * CHUNK_VECS;
+                uint4 *dst4 = reinterpret_cast<uint4 *>(drow);
+                const int v0 = c * CHUNK_VECS + threadIdx.x;
+                if (c != g.n - 1) {
+                    if (sc == 0.0f) {
+    #pragma unroll
+                        for (int j = 0; j < U; ++j) stg_stream(dst4 + v0 + j * NT, make_uint4(0u, 0u, 0u, 0u));
                     } else {
-                        chunk[j * NT + threadIdx.x] = d;
+                        uint4 x[U];
+    #pragma unroll
+                        for (int j = 0; j < U; ++j) x[j] = chunk[j * NT + threadIdx.x];
+                        if (gref.sign == 0u) {
+                            const typename RowwiseBatch<NT, U>::GradRef gp{gref.ref, 0u};
+    #pragma unroll
+                            for (int j = 0; j < U; ++j)
+                                stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gp));
+                        } else {
+    #pragma unroll
+                            for (int j = 0; j < U; ++j)
+                                stg_stream(dst4 + v0 + j * NT, RowwiseBatch<NT, U>::grad_scaled(x[j], gref));
+                        }
+                    }
+                } else {
+    #pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int vi = v0 + j * NT;
+                        if (vi >= g.n_vec) break;
+                        const uint4 d = sc == 0.0f ? make_uint4(0u, 0u, 0u, 0u)
+                                                   : RowwiseBatch<NT, U>::grad_scaled(chunk[j * NT + threadIdx.x], gref);
+                        if (vi == g.n_vec - 1 && g.tail_valid < 8) store_tail(drow + (int64_t)vi * 8, d, g.tail_valid);
+                        else stg_stream(dst4 + vi, d);
                     }
                 }
+                if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
+                    drow[y] = f2bf(gy);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + sl);
             }
-            // the target's own column (g_y from the fp64 epilogue), rewritten by the thread that
-            // wrote its vector: in the slot, or in global memory behind the partial last vector
-            if (y_chunk == c && sc != 0.0f && ((y >> 3) - c * CHUNK_VECS) % NT == (int)threadIdx.x) {
-                if (tail_here && (y >> 3) == g.n_vec - 1) drow[y] = f2bf(gy);
-                else reinterpret_cast<uint16_t *>(chunk)[y - c * CHUNK_VECS * 8] = f2bf(gy);
-            }
-            tc::fence_proxy_async_smem();  // the generic-proxy writes, visible to the bulk copy
-            __syncwarp();
-            if (lane == 0) mbar_arrive(wrote + sl);
         }
     }
 }
@@ -480,7 +525,7 @@ cudaError_t launch_fused_stream(const LossArgs &a, const grpo_tune_t *tune, cuda
         e = cudaFuncSetAttribute(stream_kernel<NT_, MB_, CV_, 1>,                                         \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
         if (e != cudaSuccess) return e;                                                                \
-        stream_kernel<NT_, MB_, CV_, 1><<<grid, NT_ + 96, smem, s>>>(p);                                  \
+        stream_kernel<NT_, MB_, CV_, 1><<<grid, NT_ + (MB_ == 1 ? 96 : 64), smem, s>>>(p);                                  \
     } while (0)
     if (ckb == 64) {
         GRPO_K3C(512, 1, 4096);
